@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark: the H2 potential-energy surface (BASELINE.json configs 1-2)
+plus the gate-apply HBM roofline (config 4), one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Our arm (default):
+  value      seconds per PES (100 bonds x 200 Adam iterations, Hartree-Fock +
+             Jordan-Wigner + VQE), max over ranks, inputs resident in HBM:
+             the fused kernel alone (vqf_pes_launch) timed with CUDA events
+             on the launching stream, L2 flushed (256 MiB write) between steps
+             outside the event brackets.  N ranks split the bonds with
+             split_chunks (strong scaling; no collective on the data path).
+  e2e        the same metric through the public C ABI (vqf_run_sweep) with
+             host buffers: H2D of the inputs and D2H of all results inside
+             the timed region, host wall clock, max over ranks.
+  roofline   the RY gate kernel on an n = 30 fp64 state (16 GiB >> L2),
+             algorithmic bytes 2 * 2^30 * 16 per launch / CUDA-event time.
+  cpu_baseline  the reference's own run_sweep (oracle/_ref, the unmodified
+             headers) on all host cores, rank 0 at N = 1 only.
+--impl reference: the reference's own CPU run_sweep on the host cores,
+  rank 0 only (other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "H2 PES s (100 bonds×200 iters) at 1/2/4/8 GPU; gate-apply GB/s vs HBM peak"
+WORKLOAD = "H2 STO-3G PES: 100 bonds 0.1-3.0 A x 200 Adam iterations (HF + JW + VQE), BASELINE configs 1/2"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def base_config(n_gpus):
+    return {
+        "workload": WORKLOAD,
+        "bonds": 100,
+        "iterations": 200,
+        "ansatz": "DoubleExcitation(0,1,2,3) on |1100>, 1 parameter",
+        "parallelism": f"bond-sharded over {n_gpus} GPU(s) with split_chunks(100, {n_gpus}); no collective on the data path",
+        "l2": "PES: 256 MiB L2 flush between timed steps (outside event brackets); gate roofline: 16 GiB state > 126 MB L2",
+    }
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms while active (the recipe's clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.dev), "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) < 9:
+                        continue
+                    try:
+                        sm.append(float(parts[1]))
+                        smax.append(float(parts[2]))
+                    except ValueError:
+                        continue
+                    for name, val in zip(names, parts[5:9]):
+                        if val.lower() == "active":
+                            reasons.add(name)
+            os.unlink(self.path)
+        except OSError:
+            pass
+        if sm:
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(smax), reasons=sorted(reasons), samples=len(sm))
+        return out
+
+
+# ------------------------------------------------------------- reference
+def reference_pes_seconds(ref, steps, warmup, workers):
+    for _ in range(warmup):
+        ref.run_sweep(workers=workers)
+    t = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        r = ref.run_sweep(workers=workers)
+        t.append(time.perf_counter() - t0)
+        assert r["all_ok"]
+    return statistics.mean(t), t
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from oracle.oracle import load_ref
+
+    ref = load_ref()
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libvqf_ref.so was not built"}))
+        return
+    cores = os.cpu_count() or 1
+    mean_s, _ = reference_pes_seconds(ref, args.steps, max(args.warmup, 1), cores)
+    sample = f"full workload (100 bonds x 200 iters, HF+JW included) per step, reference run_sweep workers={cores}"
+    line = {
+        "metric": METRIC, "value": mean_s, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic: H2 Hamiltonians built from the bond grid (no external data)",
+        "config": base_config(args.gpus), "impl": "reference",
+        "cpu_baseline": {"value": mean_s, "unit": "s", "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": mean_s, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ ours
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(kernel_key):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
+def gate_roofline(V, torch, device, n, steps, warmup):
+    """RY on wires cycling 0..n-1 of an n-qubit fp64 state; per-launch CUDA
+    events on the launching stream."""
+    stream = torch.cuda.Stream(device=device)
+    psi = V.StateVector(n, device=device)
+    psi.set_stream(stream.cuda_stream)
+    V.apply_circuit(psi, [V.Gate.ry(0.3, q) for q in range(min(n, 4))])  # dense-ish start
+    S = (1 << n) * 16
+    launches = max(steps, 1) * 4
+    for i in range(warmup * 4):
+        V.apply_gate(psi, V.Gate.ry(0.1, i % n))
+    torch.cuda.synchronize(device)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(launches)]
+    wires = [(7 * i) % n for i in range(launches)]  # spread over high and low strides
+    with torch.cuda.stream(stream):
+        for (a, b), w in zip(evs, wires):
+            a.record(stream)
+            V.apply_gate(psi, V.Gate.ry(0.01, w))
+            b.record(stream)
+    torch.cuda.synchronize(device)
+    ms = [a.elapsed_time(b) for a, b in evs]
+    per_wire = {}
+    for w, t in zip(wires, ms):
+        per_wire.setdefault(w, []).append(t)
+    avg_ms = statistics.mean(ms)
+    del psi
+    return {"n_qubits": n, "state_bytes": S, "alg_bytes_per_launch": 2 * S, "avg_ms": avg_ms,
+            "gbps": 2 * S / (avg_ms * 1e-3) / 1e9, "launches": launches,
+            "worst_wire_gbps": min(2 * S / (statistics.mean(v) * 1e-3) / 1e9 for v in per_wire.values()),
+            "best_wire_gbps": max(2 * S / (statistics.mean(v) * 1e-3) / 1e9 for v in per_wire.values())}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2601_09951_b200 import vqeforge as V
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    V.init(local_rank)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(local_rank)
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(local_rank)
+    cfg = V.SweepConfig(chunk_index=rank, n_chunks=world)
+    plan = V.PesPlan(cfg, device=local_rank)
+    stream = torch.cuda.Stream(device=local_rank)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
+    for _ in range(max(args.warmup, 3)):
+        plan.launch(stream.cuda_stream)
+    torch.cuda.synchronize(local_rank)
+
+    # ---- value: device-resident PES, K steps
+    clocks.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    launches0 = V.kernel_launches()
+    with torch.cuda.stream(stream):
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            plan.launch(stream.cuda_stream)
+            b.record(stream)
+    barrier()
+    gpu_launches = V.kernel_launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    pes_s = max_over_ranks(statistics.mean(step_ms) * 1e-3)
+    rep = plan.read()
+
+    # ---- e2e: public C ABI with host buffers (H2D + kernel + D2H per step)
+    buf = V.SweepBuffers(V.SweepConfig(chunk_index=rank, n_chunks=world), trajectories=True)
+    for _ in range(max(args.warmup, 3)):
+        buf.run()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        buf.run()
+    barrier()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    h2d, d2h = int(buf.rep.h2d_bytes), int(buf.rep.d2h_bytes)
+    e2e_rep = buf.report()
+
+    # ---- gate-apply roofline (each rank a replica; rank 0 reported)
+    gate = gate_roofline(V, torch, local_rank, args.gate_qubits, args.steps, args.warmup) if args.gate_qubits else None
+    clk = clocks.stop()
+
+    # ---- gather results, check parity against the reference's fixture
+    pts = [(p.bond_angstrom, p.energy_hartree, p.iterations, p.ok) for p in rep.points]
+    e2e_pts = [(p.bond_angstrom, p.energy_hartree, p.iterations, p.ok) for p in e2e_rep.points]
+    if dist is not None:
+        allp = [None] * world
+        dist.all_gather_object(allp, (pts, e2e_pts))
+        pts = [x for r in allp for x in r[0]]
+        e2e_pts = [x for r in allp for x in r[1]]
+    if rank != 0:
+        return
+    with open(os.path.join(ROOT, "tests", "golden", "pes_default.json")) as f:
+        gold = json.load(f)
+    parity = {
+        "max_abs_dE_vs_reference": max(abs(p[1] - e) for p, e in zip(pts, gold["energy"])),
+        "bond_grid_bitwise": [p[0] for p in pts] == gold["bond"],
+        "iterations_equal": [p[2] for p in pts] == gold["iterations"],
+        "e2e_equals_value_run": pts == e2e_pts,
+        "all_ok": all(p[3] for p in pts),
+    }
+    peak, peak_src = load_peaks()
+    line = {
+        "metric": METRIC, "value": pes_s, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": pes_s * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic: H2 Hamiltonians built on device from the bond grid (no external data)",
+        "config": base_config(world),
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world},
+        "gpu_launches": int(gpu_launches),
+        "parity": parity,
+        "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
+    }
+    if gate is not None:
+        line["roofline"] = {
+            "bound": "hbm", "achieved": gate["gbps"], "peak": peak, "unit": "GB/s", "frac": gate["gbps"] / peak,
+            "traffic": load_traffic("k_gate1_ry"), "kernel": "k_gate1<double, RY> (paper_2601_09951_b200/csrc/sv.cu)",
+            "per_launch": f"alg bytes = 2 x 2^{gate['n_qubits']} x 16 B = {gate['alg_bytes_per_launch']} B; "
+                          f"avg {gate['avg_ms']:.3f} ms over {gate['launches']} launches, wires spread 0..{gate['n_qubits'] - 1}",
+            "peak_source": peak_src,
+            "wire_range_gbps": [gate["worst_wire_gbps"], gate["best_wire_gbps"]],
+        }
+        line["config"]["gate_roofline_workload"] = f"RY on an n={gate['n_qubits']} fp64 state (2^{gate['n_qubits']} x 16 B)"
+    line["pes_kernel"] = {"bound": "latency", "note": "100 bonds x 256 B states live in registers/shared memory; "
+                          "one CTA per bond, 200 dependent Adam iterations", "device_ms": pes_s * 1e3}
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle.oracle import load_ref
+
+        ref = load_ref()
+        if ref is not None:
+            cores = os.cpu_count() or 1
+            reps, t_spent, times = 0, 0.0, []
+            while (t_spent < args.cpu_seconds and reps < 500) or reps < 3:
+                t0 = time.perf_counter()
+                ref.run_sweep(workers=cores)
+                dt = time.perf_counter() - t0
+                times.append(dt)
+                t_spent += dt
+                reps += 1
+            line["cpu_baseline"] = {"value": statistics.mean(times), "unit": "s", "cores": cores, "kind": "reference",
+                                    "sample": f"{reps} repetitions of the full workload (reference run_sweep, "
+                                              f"workers={cores}), {t_spent:.1f} s of CPU wall time"}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--gate-qubits", type=int, default=30)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

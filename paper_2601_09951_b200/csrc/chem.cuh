@@ -1,0 +1,373 @@
+// H2 / STO-3G Hamiltonian construction shared by the host API
+// (vqf_build_h2_hamiltonian) and the fused on-device PES kernel
+// (vqe_small.cu).  Semantics follow the reference chem.hpp:
+//   sto3g_hydrogen  :66-89     boys_f0      :93-99
+//   primitives      :142-182   ao_integrals :218-249
+//   run_hartree_fock:280-372   jordan_wigner:380-467
+// B200 restructuring:
+//  - every bond-independent transcendental (contraction norms, pow(pi/p,1.5),
+//    pow(pi,2.5)) is evaluated ONCE on the host with the host libm and passed
+//    in ChemConsts, so those values are bitwise the reference's;
+//  - the 16 x 81 ERI primitives are independent and are spread over a CTA;
+//  - Jordan-Wigner is done in symplectic (x, z) form: every ladder-operator
+//    product coefficient is +-w / 2^k times a power of i, exact in binary
+//    floating point, so contributions are generated directly by index and
+//    merged per Pauli string in the reference's generation order
+//    (canonicalize merges in order of first appearance, pauli.hpp:180-190).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#endif
+
+namespace vqf {
+namespace chem {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kAngstromToBohr = 1.8897259886;  // chem.hpp:32
+constexpr double kMinBond = 0.05, kMaxBond = 10.0;  // chem.hpp:33-34
+constexpr int kScfMax = 100;                       // chem.hpp:35
+constexpr double kScfTol = 1e-10;                  // chem.hpp:36
+constexpr int kNumContrib = 1 + 8 * 4 + 64 * 16;   // JW contributions (fixed slots)
+
+struct ChemConsts {
+  double alpha[3];
+  double coef[3];         // normalised contraction coefficients
+  double pow_pi_p15[3][3];  // pow(pi / (alpha_i + alpha_j), 1.5)
+  double pow_pi_25;       // pow(pi, 2.5)
+};
+
+// Host only: the reference's sto3g_hydrogen normalisation (chem.hpp:66-89).
+inline ChemConsts make_consts() {
+  ChemConsts k;
+  const double alpha[3] = {3.42525091, 0.62391373, 0.16885540};
+  const double contraction[3] = {0.15432897, 0.53532814, 0.44463454};
+  for (int i = 0; i < 3; ++i) {
+    k.alpha[i] = alpha[i];
+    k.coef[i] = contraction[i] * std::pow(2.0 * alpha[i] / kPi, 0.75);
+  }
+  double self = 0.0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const double p = alpha[i] + alpha[j];
+      self += k.coef[i] * k.coef[j] * std::pow(kPi / p, 1.5);
+    }
+  const double scale = 1.0 / std::sqrt(self);
+  for (int i = 0; i < 3; ++i) k.coef[i] *= scale;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) k.pow_pi_p15[i][j] = std::pow(kPi / (alpha[i] + alpha[j]), 1.5);
+  k.pow_pi_25 = std::pow(kPi, 2.5);
+  return k;
+}
+
+__host__ __device__ inline double boys_f0(double t) {
+  if (t < 1e-12) return 1.0 - t / 3.0 + t * t / 10.0 - t * t * t / 42.0;
+  const double sq = sqrt(t);
+  return 0.5 * sqrt(kPi / t) * erf(sq);
+}
+
+// Centres lie on the z axis (chem.hpp:219-220); dist2 = dz^2 exactly.
+__host__ __device__ inline double d2z(double a, double b) {
+  const double dz = a - b;
+  return dz * dz;
+}
+__host__ __device__ inline double cz(double a, double A, double b, double B) { return (a * A + b * B) / (a + b); }
+
+__host__ __device__ inline double overlap_prim(const ChemConsts& k, int i, int j, double A, double B) {
+  const double a = k.alpha[i], b = k.alpha[j], p = a + b, mu = a * b / p;
+  return k.pow_pi_p15[i][j] * exp(-mu * d2z(A, B));
+}
+__host__ __device__ inline double kinetic_prim(const ChemConsts& k, int i, int j, double A, double B) {
+  const double a = k.alpha[i], b = k.alpha[j], p = a + b, mu = a * b / p, r2 = d2z(A, B);
+  return mu * (3.0 - 2.0 * mu * r2) * k.pow_pi_p15[i][j] * exp(-mu * r2);
+}
+__host__ __device__ inline double nuclear_prim(const ChemConsts& k, int i, int j, double A, double B, double C) {
+  const double a = k.alpha[i], b = k.alpha[j], p = a + b, mu = a * b / p;
+  const double P = cz(a, A, b, B);
+  return -2.0 * kPi / p * exp(-mu * d2z(A, B)) * boys_f0(p * d2z(P, C));
+}
+__host__ __device__ inline double eri_prim(const ChemConsts& k, int i, double A, int j, double B, int l, double C,
+                                           int m, double D) {
+  const double a = k.alpha[i], b = k.alpha[j], c = k.alpha[l], d = k.alpha[m];
+  const double p = a + b, q = c + d;
+  const double P = cz(a, A, b, B), Q = cz(c, C, d, D);
+  const double pref = 2.0 * k.pow_pi_25 / (p * q * sqrt(p + q));
+  return pref * exp(-(a * b / p) * d2z(A, B)) * exp(-(c * d / q) * d2z(C, D)) * boys_f0(p * q / (p + q) * d2z(P, Q));
+}
+
+// One (ijkl, xyzw) ERI primitive term c_x c_y c_z c_w * prim, with
+// idx = ijkl * 81 + ((x*3 + y)*3 + z)*3 + w (contract4's loop order).
+__host__ __device__ inline double eri_term(const ChemConsts& k, double bond_bohr, int idx) {
+  const int ijkl = idx / 81, r = idx % 81;
+  const int i = ijkl >> 3, j = (ijkl >> 2) & 1, l = (ijkl >> 1) & 1, m = ijkl & 1;
+  const int x = r / 27, y = (r / 9) % 3, z = (r / 3) % 3, w = r % 3;
+  const double Z[2] = {0.0, bond_bohr};
+  return k.coef[x] * k.coef[y] * k.coef[z] * k.coef[w] * eri_prim(k, x, Z[i], y, Z[j], z, Z[l], w, Z[m]);
+}
+
+struct AoInts {
+  double S[2][2], T[2][2], V[2][2], eri[16];
+};
+
+// One-electron integrals for AO pair (i, j) (chem.hpp:226-239).
+__host__ __device__ inline void one_electron(const ChemConsts& k, double bond_bohr, int i, int j, AoInts& out) {
+  const double Z[2] = {0.0, bond_bohr};
+  double s = 0.0, t = 0.0;
+  for (int x = 0; x < 3; ++x)
+    for (int y = 0; y < 3; ++y) s += k.coef[x] * k.coef[y] * overlap_prim(k, x, y, Z[i], Z[j]);
+  for (int x = 0; x < 3; ++x)
+    for (int y = 0; y < 3; ++y) t += k.coef[x] * k.coef[y] * kinetic_prim(k, x, y, Z[i], Z[j]);
+  double v = 0.0;
+  for (int n = 0; n < 2; ++n) {
+    double vn = 0.0;
+    for (int x = 0; x < 3; ++x)
+      for (int y = 0; y < 3; ++y) vn += k.coef[x] * k.coef[y] * nuclear_prim(k, x, y, Z[i], Z[j], Z[n]);
+    v += vn;
+  }
+  out.S[i][j] = s;
+  out.T[i][j] = t;
+  out.V[i][j] = v;
+}
+
+// Symmetric 2x2 eigen-decomposition, eigenvalues ascending, unit columns.
+__host__ __device__ inline void sym2(const double A[2][2], double ev[2], double V[2][2]) {
+  const double p = A[0][0], q = A[1][1], r = 0.5 * (A[0][1] + A[1][0]);
+  const double mean = 0.5 * (p + q), half = 0.5 * (p - q);
+  const double rad = sqrt(half * half + r * r);
+  ev[0] = mean - rad;
+  ev[1] = mean + rad;
+  if (rad == 0.0) {
+    V[0][0] = 1.0;
+    V[0][1] = 0.0;
+    V[1][0] = 0.0;
+    V[1][1] = 1.0;
+    return;
+  }
+  double ux = r, uy = ev[0] - p;
+  const double vx = ev[0] - q, vy = r;
+  if (vx * vx + vy * vy > ux * ux + uy * uy) {
+    ux = vx;
+    uy = vy;
+  }
+  const double nrm = sqrt(ux * ux + uy * uy);
+  ux /= nrm;
+  uy /= nrm;
+  V[0][0] = ux;
+  V[1][0] = uy;
+  V[0][1] = -uy;
+  V[1][1] = ux;
+}
+
+__host__ __device__ inline void mm2(const double A[2][2], const double B[2][2], double C[2][2]) {
+  double R[2][2];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) R[i][j] = A[i][0] * B[0][j] + A[i][1] * B[1][j];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) C[i][j] = R[i][j];
+}
+__host__ __device__ inline void tr2(const double A[2][2], double B[2][2]) {
+  const double R[2][2] = {{A[0][0], A[1][0]}, {A[0][1], A[1][1]}};
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) B[i][j] = R[i][j];
+}
+
+struct HfOut {
+  double hmo[2][2];  // core Hamiltonian in the MO basis
+  double eri_mo[16]; // physicist <ij|kl>, index ((i*2+j)*2+k)*2+l
+  double e_nuc, hf_energy, e_elec;
+  int scf_iterations;
+  int converged;
+};
+
+__host__ __device__ inline void g_matrix(const double P[2][2], const double* eri, double G[2][2]) {
+  for (int mu = 0; mu < 2; ++mu)
+    for (int nu = 0; nu < 2; ++nu) {
+      double g = 0.0;
+      for (int lam = 0; lam < 2; ++lam)
+        for (int sig = 0; sig < 2; ++sig)
+          g += P[lam][sig] * (eri[((mu * 2 + nu) * 2 + sig) * 2 + lam] - 0.5 * eri[((mu * 2 + lam) * 2 + sig) * 2 + nu]);
+      G[mu][nu] = g;
+    }
+}
+
+// SCF loop + final Fock build (chem.hpp:285-348), serial.  Leaves the MO
+// coefficients in C for the ERI transform.
+__host__ __device__ inline void scf(const AoInts& I, double bond_bohr, HfOut& o, double C[2][2]) {
+  double H[2][2];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) H[i][j] = I.T[i][j] + I.V[i][j];
+  double sev[2], SV[2][2], VD[2][2], SVt[2][2], X[2][2], Xt[2][2];
+  sym2(I.S, sev, SV);
+  const double d0 = 1.0 / sqrt(sev[0]), d1 = 1.0 / sqrt(sev[1]);
+  for (int i = 0; i < 2; ++i) {
+    VD[i][0] = SV[i][0] * d0;
+    VD[i][1] = SV[i][1] * d1;
+  }
+  tr2(SV, SVt);
+  mm2(VD, SVt, X);
+  tr2(X, Xt);
+  double P[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, F[2][2], G[2][2];
+  C[0][0] = C[0][1] = C[1][0] = C[1][1] = 0.0;
+  double e_elec = 0.0;
+  int converged = 0, iterations = 0;
+  for (int iter = 1; iter <= kScfMax; ++iter) {
+    g_matrix(P, I.eri, G);
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j) F[i][j] = H[i][j] + G[i][j];
+    double T1[2][2], Fp[2][2], fev[2], FV[2][2];
+    mm2(Xt, F, T1);
+    mm2(T1, X, Fp);
+    sym2(Fp, fev, FV);
+    mm2(X, FV, C);
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j) P[i][j] = (2.0 * C[i][0]) * C[j][0];
+    double s = 0.0;
+    for (int j = 0; j < 2; ++j)
+      for (int i = 0; i < 2; ++i) s += P[i][j] * (H[i][j] + F[i][j]);
+    const double e_new = 0.5 * s;
+    iterations = iter;
+    if (iter > 1 && fabs(e_new - e_elec) < kScfTol) {
+      e_elec = e_new;
+      converged = 1;
+      break;
+    }
+    e_elec = e_new;
+  }
+  o.converged = converged;
+  o.scf_iterations = iterations;
+  g_matrix(P, I.eri, G);
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) F[i][j] = H[i][j] + G[i][j];
+  double s = 0.0;
+  for (int j = 0; j < 2; ++j)
+    for (int i = 0; i < 2; ++i) s += P[i][j] * (H[i][j] + F[i][j]);
+  o.e_elec = 0.5 * s;
+  o.e_nuc = 1.0 / bond_bohr;
+  o.hf_energy = o.e_elec + o.e_nuc;
+  double Ct[2][2], T2[2][2];
+  tr2(C, Ct);
+  mm2(Ct, H, T2);
+  mm2(T2, C, o.hmo);
+}
+
+// MO chemist integral (pq|rs) (chem.hpp:352-365); idx = ((p*2+q)*2+r)*2+s.
+__host__ __device__ inline double mo_chem(const double C[2][2], const double* eri, int idx) {
+  const int p = idx >> 3, q = (idx >> 2) & 1, r = (idx >> 1) & 1, s = idx & 1;
+  double val = 0.0;
+  for (int mu = 0; mu < 2; ++mu)
+    for (int nu = 0; nu < 2; ++nu)
+      for (int lam = 0; lam < 2; ++lam)
+        for (int sig = 0; sig < 2; ++sig)
+          val += C[mu][p] * C[nu][q] * C[lam][r] * C[sig][s] * eri[((mu * 2 + nu) * 2 + lam) * 2 + sig];
+  return val;
+}
+
+// Pauli string on 4 qubits in symplectic form: bit q of x / z for qubit q.
+// Per-qubit product phase follows axis_product (pauli.hpp:134-150):
+// X*Y = iZ and cyclic, reversed -i, equal -> identity.
+__host__ __device__ inline int axis_of(int x, int z) { return x ? (z ? 2 : 1) : (z ? 3 : 0); }
+
+// Multiplies (x1,z1) by (x2,z2) in place; returns the phase power of i.
+__host__ __device__ inline int pauli_mul(int& x, int& z, int x2, int z2) {
+  int m = 0;
+  for (int q = 0; q < 4; ++q) {
+    const int a = axis_of((x >> q) & 1, (z >> q) & 1), b = axis_of((x2 >> q) & 1, (z2 >> q) & 1);
+    if (a != 0 && b != 0 && a != b) m += (((b - a + 3) % 3) == 1) ? 1 : 3;
+  }
+  x ^= x2;
+  z ^= z2;
+  return m & 3;
+}
+
+// Ladder operator JW term (chem.hpp:380-393): choice 0 -> 0.5 Z..Z X_p,
+// choice 1 -> (dagger ? -0.5i : +0.5i) Z..Z Y_p.  Returns the phase power
+// of the unit coefficient (0 for 0.5, 3 for -0.5i, 1 for +0.5i).
+__host__ __device__ inline int ladder(int p, int dagger, int choice, int& x, int& z) {
+  x = 1 << p;
+  z = ((1 << p) - 1) | (choice ? (1 << p) : 0);
+  return choice ? (dagger ? 3 : 1) : 0;
+}
+
+// Contribution #idx of the JW expansion in the reference's generation order
+// (chem.hpp:434-461 loops, accumulate_product's factor-major expansion):
+//   idx 0            nuclear repulsion * I
+//   idx 1..32        (p,q) same-spin pairs x 4 factor choices
+//   idx 33..1056     (p,q,r,s) spin-allowed quadruples x 16 choices
+// Writes key = x | z << 4 and the complex value; returns 0 for a slot the
+// reference skips (zero integral) so it contributes nothing.
+__host__ __device__ inline int jw_contribution(int idx, const double hmo[2][2], const double* eri_mo, double e_nuc,
+                                               int& key, double& re, double& im) {
+  double w;
+  int m = 0, x = 0, z = 0;
+  if (idx == 0) {
+    key = 0;
+    re = e_nuc;
+    im = 0.0;
+    return 1;
+  }
+  if (idx <= 32) {
+    const int pair = (idx - 1) >> 2, sub = (idx - 1) & 3;
+    // same-spin (p, q) pairs in loop order: p in 0..3, q in 0..3, p%2 == q%2
+    const int p = pair >> 1, q = ((pair & 1) << 1) | (p & 1);
+    w = hmo[p >> 1][q >> 1];
+    if (w == 0.0) return 0;
+    int fx, fz;
+    m = ladder(p, 1, (sub >> 1) & 1, x, z);
+    m += ladder(q, 0, sub & 1, fx, fz);
+    m += pauli_mul(x, z, fx, fz);
+    w *= 0.25;
+  } else {
+    const int quad = (idx - 33) >> 4, sub = (idx - 33) & 15;
+    // spin-allowed (p,q,r,s): p, q free; r = same spin as p; s = same spin as q.
+    // Loop order p, q, r, s; quad = ((p*4 + q)*2 + rr)*2 + ss.
+    const int p = quad >> 4, q = (quad >> 2) & 3, rr = (quad >> 1) & 1, ss = quad & 1;
+    const int r = (rr << 1) | (p & 1), s = (ss << 1) | (q & 1);
+    w = eri_mo[(((p >> 1) * 2 + (q >> 1)) * 2 + (r >> 1)) * 2 + (s >> 1)];
+    if (w == 0.0) return 0;
+    w = 0.5 * w;
+    // factors: create p, create q, annihilate s, annihilate r
+    const int ops[4] = {p, q, s, r};
+    const int dag[4] = {1, 1, 0, 0};
+    m = ladder(ops[0], dag[0], (sub >> 3) & 1, x, z);
+    for (int f = 1; f < 4; ++f) {
+      int fx, fz;
+      m += ladder(ops[f], dag[f], (sub >> (3 - f)) & 1, fx, fz);
+      m += pauli_mul(x, z, fx, fz);
+    }
+    w *= 0.0625;
+  }
+  key = x | (z << 4);
+  switch (m & 3) {
+    case 0: re = w; im = 0.0; break;
+    case 1: re = 0.0; im = w; break;
+    case 2: re = -w; im = 0.0; break;
+    default: re = 0.0; im = -w; break;
+  }
+  return 1;
+}
+
+// Lexicographic (index, axis) order of the sparse form of a 4-qubit key
+// (axes_less, pauli.hpp:99-106) as a sortable integer: per qubit ascending,
+// emit (q, axis) for non-identity axes; compare sequences.  Encoded as a
+// base-16 number of up to 4 digits (q*3 + axis), left-aligned, shorter
+// prefixes first.
+__host__ __device__ inline uint32_t key_order(int key) {
+  uint32_t code = 0;
+  int len = 0;
+  for (int q = 0; q < 4; ++q) {
+    const int a = axis_of((key >> q) & 1, (key >> (4 + q)) & 1);
+    if (a) {
+      code = code * 16 + static_cast<uint32_t>(q * 3 + a);  // 1..12, never 0
+      ++len;
+    }
+  }
+  for (; len < 4; ++len) code *= 16;  // empty digits sort first
+  return code;
+}
+
+}  // namespace chem
+}  // namespace vqf

@@ -1,0 +1,919 @@
+// Host drivers of the VQE hot path: prepare_ansatz / energy / gradient /
+// run_vqe (vqe.hpp:65-254), run_sweep (sweep.hpp:128-178) and
+// run_scaling_study (sweep.hpp:265-307), over two device engines:
+//   * the register-resident batched engine (vqe_small.cu) for n <= 5 — the
+//     H2 PES runs there, chemistry included, one launch per worker;
+//   * the HBM state-vector engine (sv.cu) for wider registers: all 2P+1
+//     parameter-shift circuits of an iteration are one batched state, so each
+//     gate position is one launch over every circuit.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <iostream>
+#include <memory>
+#include <thread>
+
+#include "chem_host.h"
+#include "pauli_host.h"
+#include "sv.cuh"
+#include "vqe_small.cuh"
+
+namespace vqf {
+
+namespace {
+
+constexpr double kShift = 1.5707963267948966;  // std::numbers::pi / 2 (vqe.hpp:115)
+
+using Clock = std::chrono::steady_clock;
+
+double seconds_since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+void check_adam(const vqf_adam_config* c) {
+  if (c == nullptr) throw_invalid("null adam config");
+}
+
+std::string nonfinite_msg(int iter, const double* theta, uint32_t P) {
+  std::string msg = "non-finite energy at iteration " + std::to_string(iter) + "; theta =";
+  for (uint32_t k = 0; k < P; ++k) msg += " " + fstr(theta[k]);
+  return msg;
+}
+
+std::string imag_msg(double v) { return "expectation has imaginary residue " + fstr(v); }
+
+// Validates (kind, layers, n) the way prepare_ansatz does (vqe.hpp:68-75).
+uint32_t ansatz_params(int32_t kind, uint32_t layers, uint32_t n) {
+  if (kind != VQF_ANSATZ_H2_DOUBLE_EXCITATION && kind != VQF_ANSATZ_HARDWARE_EFFICIENT)
+    throw Error(VQF_LOGIC_ERROR, "unknown ansatz kind");
+  return kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION ? 1u : layers * n;
+}
+
+void check_ansatz_register(int32_t kind, uint32_t n) {
+  if (kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION && n != 4)
+    throw_invalid("H2 double-excitation ansatz requires 4 qubits");
+}
+
+// ------------------------------------------------------------------------
+// Per-(thread, device) workspace: a stream, pinned staging buffers and
+// device buffers that grow monotonically, so steady-state calls allocate
+// nothing.
+struct Workspace {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void* dev = nullptr;
+  size_t dev_cap = 0;
+  void* pin = nullptr;
+  size_t pin_cap = 0;
+  ~Workspace() {
+    if (device < 0) return;
+    cudaSetDevice(device);
+    if (dev) cudaFree(dev);
+    if (pin) cudaFreeHost(pin);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void reserve(size_t dev_bytes, size_t pin_bytes) {
+    if (dev_bytes > dev_cap) {
+      if (dev) VQF_CUDA(cudaFree(dev));
+      VQF_CUDA(cudaMalloc(&dev, dev_bytes));
+      dev_cap = dev_bytes;
+    }
+    if (pin_bytes > pin_cap) {
+      if (pin) VQF_CUDA(cudaFreeHost(pin));
+      VQF_CUDA(cudaMallocHost(&pin, pin_bytes));
+      pin_cap = pin_bytes;
+    }
+  }
+};
+
+Workspace& workspace(int device) {
+  thread_local std::vector<std::unique_ptr<Workspace>> pool;
+  for (auto& w : pool)
+    if (w->device == device) return *w;
+  auto w = std::make_unique<Workspace>();
+  VQF_CUDA(cudaSetDevice(device));
+  VQF_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+  VQF_CUDA(cudaEventCreate(&w->ev0));
+  VQF_CUDA(cudaEventCreate(&w->ev1));
+  w->device = device;
+  pool.push_back(std::move(w));
+  return *pool.back();
+}
+
+// Carves typed slices out of one contiguous byte range (16-byte aligned).
+struct Carver {
+  size_t off = 0;
+  template <typename T>
+  size_t take(size_t count) {
+    off = (off + 15) & ~size_t{15};
+    const size_t at = off;
+    off += count * sizeof(T);
+    return at;
+  }
+};
+
+// ------------------------------------------------------------------------
+// Small-register batched engine: shared by run_vqe (batch 1), run_vqe_batch
+// and run_sweep (PES mode).
+struct SmallJob {
+  uint32_t batch = 0;
+  int32_t n_qubits = 4, kind = 0, layers = 0;
+  uint32_t P = 1;
+  vqf_adam_config adam{};
+  bool pes = false;
+  // inputs
+  std::vector<double> bonds;          // PES
+  std::vector<int32_t> status_in;     // PES: kStatusBond pre-marked
+  std::vector<MaskTerm> terms;        // generic
+  std::vector<uint32_t> term_off;     // generic
+  std::vector<double> init_theta;     // optional, batch * P
+  bool want_ham = false;
+  // outputs (host)
+  std::vector<double> energy, theta, traj, err_val, err_theta, ham_coeffs, hf;
+  std::vector<int32_t> iters, converged, status, err_iter, ham_keys, ham_count;
+  double device_seconds = 0.0;
+};
+
+// Device layout of one small-engine job: inputs, then fixed-size outputs,
+// then the trajectories (last, so a caller that does not want them skips
+// their D2H copy).  One H2D copy in, one D2H copy out.
+struct SmallStage {
+  size_t o_bc1, o_bc2, o_bonds, o_terms, o_toff, o_init, o_status, in_end;
+  size_t o_energy, o_theta, o_iters, o_conv, o_errv, o_erri, o_errt, o_hk, o_hc, o_hn, o_hf, o_traj, out_end, total;
+  uint32_t stride = 1;
+  std::vector<double> bc1, bc2;
+
+  explicit SmallStage(const SmallJob& j) {
+    const uint32_t B = j.batch, P = j.P;
+    const int32_t T = j.adam.max_iterations;
+    stride = static_cast<uint32_t>(std::max(T, 0)) + 1;
+    host::bias_tables(j.adam, T, bc1, bc2);
+    Carver c;
+    o_bc1 = c.take<double>(bc1.size());
+    o_bc2 = c.take<double>(bc2.size());
+    o_bonds = c.take<double>(j.pes ? B : 0);
+    o_terms = c.take<MaskTerm>(j.terms.size());
+    o_toff = c.take<uint32_t>(j.term_off.size());
+    o_init = c.take<double>(j.init_theta.size());
+    o_status = c.take<int32_t>(B);
+    in_end = c.off;
+    o_energy = c.take<double>(B);
+    o_theta = c.take<double>((size_t)B * P);
+    o_iters = c.take<int32_t>(B);
+    o_conv = c.take<int32_t>(B);
+    o_errv = c.take<double>(B);
+    o_erri = c.take<int32_t>(B);
+    o_errt = c.take<double>((size_t)B * P);
+    o_hk = c.take<int32_t>(j.want_ham ? (size_t)B * 16 : 0);
+    o_hc = c.take<double>(j.want_ham ? (size_t)B * 16 : 0);
+    o_hn = c.take<int32_t>(j.want_ham ? B : 0);
+    o_hf = c.take<double>(j.want_ham ? (size_t)B * 4 : 0);
+    out_end = c.off;
+    o_traj = c.take<double>((size_t)B * stride);
+    total = c.off;
+  }
+
+  void pack(const SmallJob& j, unsigned char* pin) const {
+    const uint32_t B = j.batch;
+    std::memcpy(pin + o_bc1, bc1.data(), bc1.size() * sizeof(double));
+    std::memcpy(pin + o_bc2, bc2.data(), bc2.size() * sizeof(double));
+    if (j.pes) std::memcpy(pin + o_bonds, j.bonds.data(), B * sizeof(double));
+    if (!j.terms.empty()) std::memcpy(pin + o_terms, j.terms.data(), j.terms.size() * sizeof(MaskTerm));
+    if (!j.term_off.empty()) std::memcpy(pin + o_toff, j.term_off.data(), j.term_off.size() * sizeof(uint32_t));
+    if (!j.init_theta.empty())
+      std::memcpy(pin + o_init, j.init_theta.data(), j.init_theta.size() * sizeof(double));
+    if (j.status_in.empty())
+      std::memset(pin + o_status, 0, B * sizeof(int32_t));
+    else
+      std::memcpy(pin + o_status, j.status_in.data(), B * sizeof(int32_t));
+  }
+
+  SmallParams params(const SmallJob& j, unsigned char* dev) const {
+    SmallParams p{};
+    p.n_qubits = j.n_qubits;
+    p.ansatz_kind = j.kind;
+    p.layers = j.layers;
+    p.n_params = static_cast<int32_t>(j.P);
+    p.max_iterations = j.adam.max_iterations;
+    p.has_tol = j.adam.has_gradient_tolerance;
+    p.tol = j.adam.gradient_tolerance;
+    p.lr = j.adam.learning_rate;
+    p.beta1 = j.adam.beta1;
+    p.beta2 = j.adam.beta2;
+    p.eps = j.adam.epsilon;
+    p.bc1 = reinterpret_cast<const double*>(dev + o_bc1);
+    p.bc2 = reinterpret_cast<const double*>(dev + o_bc2);
+    p.bonds = reinterpret_cast<const double*>(dev + o_bonds);
+    p.chem = chem::consts();
+    p.terms = reinterpret_cast<const MaskTerm*>(dev + o_terms);
+    p.term_off = reinterpret_cast<const uint32_t*>(dev + o_toff);
+    p.init_theta = j.init_theta.empty() ? nullptr : reinterpret_cast<const double*>(dev + o_init);
+    p.energy = reinterpret_cast<double*>(dev + o_energy);
+    p.theta_out = reinterpret_cast<double*>(dev + o_theta);
+    p.traj = reinterpret_cast<double*>(dev + o_traj);
+    p.traj_stride = static_cast<int32_t>(stride);
+    p.iters = reinterpret_cast<int32_t*>(dev + o_iters);
+    p.converged = reinterpret_cast<int32_t*>(dev + o_conv);
+    p.status = reinterpret_cast<int32_t*>(dev + o_status);
+    p.err_val = reinterpret_cast<double*>(dev + o_errv);
+    p.err_iter = reinterpret_cast<int32_t*>(dev + o_erri);
+    p.err_theta = reinterpret_cast<double*>(dev + o_errt);
+    if (j.want_ham) {
+      p.ham_keys = reinterpret_cast<int32_t*>(dev + o_hk);
+      p.ham_coeffs = reinterpret_cast<double*>(dev + o_hc);
+      p.ham_count = reinterpret_cast<int32_t*>(dev + o_hn);
+      p.hf_out = reinterpret_cast<double*>(dev + o_hf);
+    }
+    return p;
+  }
+
+  // Bytes of the D2H copy (status .. outputs [.. trajectories]).
+  size_t d2h_bytes(bool traj) const { return (traj ? total : out_end) - o_status; }
+
+  void unpack(SmallJob& j, const unsigned char* pin, bool traj) const {
+    const uint32_t B = j.batch, P = j.P;
+    auto grab = [&](auto& vec, size_t off, size_t count) {
+      using T0 = typename std::decay_t<decltype(vec)>::value_type;
+      vec.resize(count);
+      if (count) std::memcpy(vec.data(), pin + off, count * sizeof(T0));
+    };
+    grab(j.status, o_status, B);
+    grab(j.energy, o_energy, B);
+    grab(j.theta, o_theta, (size_t)B * P);
+    grab(j.iters, o_iters, B);
+    grab(j.converged, o_conv, B);
+    grab(j.err_val, o_errv, B);
+    grab(j.err_iter, o_erri, B);
+    grab(j.err_theta, o_errt, (size_t)B * P);
+    if (j.want_ham) {
+      grab(j.ham_keys, o_hk, (size_t)B * 16);
+      grab(j.ham_coeffs, o_hc, (size_t)B * 16);
+      grab(j.ham_count, o_hn, B);
+      grab(j.hf, o_hf, (size_t)B * 4);
+    }
+    if (traj) grab(j.traj, o_traj, (size_t)B * stride);
+  }
+};
+
+// Stage, launch and read back one job on the thread's workspace stream.
+// Returns the H2D / D2H byte counts through the optional pointers.
+void run_small(SmallJob& j, int device, bool want_traj = true, size_t* h2d = nullptr, size_t* d2h = nullptr) {
+  Workspace& ws = workspace(device);
+  VQF_CUDA(cudaSetDevice(device));
+  const SmallStage st(j);
+  ws.reserve(st.total, st.total);
+  auto* pin = static_cast<unsigned char*>(ws.pin);
+  auto* dev = static_cast<unsigned char*>(ws.dev);
+  st.pack(j, pin);
+  const SmallParams p = st.params(j, dev);
+  VQF_CUDA(cudaMemcpyAsync(dev, pin, st.in_end, cudaMemcpyHostToDevice, ws.stream));
+  VQF_CUDA(cudaEventRecord(ws.ev0, ws.stream));
+  launch_vqe_small(p, j.batch, j.pes, ws.stream);
+  VQF_CUDA(cudaEventRecord(ws.ev1, ws.stream));
+  VQF_CUDA(cudaMemcpyAsync(pin + st.o_status, dev + st.o_status, st.d2h_bytes(want_traj), cudaMemcpyDeviceToHost,
+                           ws.stream));
+  VQF_CUDA(cudaStreamSynchronize(ws.stream));
+  float ms = 0.f;
+  VQF_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
+  j.device_seconds = ms * 1e-3;
+  st.unpack(j, pin, want_traj);
+  if (h2d) *h2d = st.in_end;
+  if (d2h) *d2h = st.d2h_bytes(want_traj);
+}
+
+std::string small_error(const SmallJob& j, uint32_t b, double bond) {
+  switch (j.status[b]) {
+    case kStatusImag: return imag_msg(j.err_val[b]);
+    case kStatusNonFinite: return nonfinite_msg(j.err_iter[b], j.err_theta.data() + (size_t)b * j.P, j.P);
+    case kStatusScf: return chem::nonconvergence_msg(bond);
+    case kStatusHermitian: return chem::nonhermitian_msg(j.err_val[b]);
+    default: return "unknown device status " + std::to_string(j.status[b]);
+  }
+}
+
+void fill_result(const SmallJob& j, uint32_t b, vqf_vqe_result* r) {
+  const int32_t T = j.adam.max_iterations;
+  const uint32_t stride = static_cast<uint32_t>(T) + 1;
+  const int32_t it = j.iters[b];
+  const bool conv = j.converged[b] != 0;
+  r->energy = j.energy[b];
+  if (r->theta) std::memcpy(r->theta, j.theta.data() + (size_t)b * j.P, j.P * sizeof(double));
+  const uint32_t len = conv ? static_cast<uint32_t>(it) + 1 : static_cast<uint32_t>(T) + 1;
+  if (r->trajectory) {
+    if (r->trajectory_capacity < len) throw_invalid("vqe_result: trajectory capacity too small");
+    std::memcpy(r->trajectory, j.traj.data() + (size_t)b * stride, len * sizeof(double));
+  }
+  r->trajectory_len = len;
+  r->iterations_run = it;
+  // one energy + 2P shifts per gradient iteration, +1 final when not
+  // converged (vqe.hpp:215, :230, :244-247)
+  const uint64_t grads = conv ? static_cast<uint64_t>(it) + 1 : static_cast<uint64_t>(T);
+  r->circuit_evaluations = grads * (1 + 2 * (uint64_t)j.P) + (conv ? 0 : 1);
+}
+
+// ------------------------------------------------------------------------
+// HBM engine: prepare every circuit of `thetas` (NC rows of P angles) into
+// an NC-entry batch and evaluate <H>.  Angles go through the host libm
+// (std::cos/std::sin of 0.5*angle, as apply_gate does) into per-entry tables.
+struct HbmEngine {
+  uint32_t n, P, layers;
+  int32_t kind;
+  int device;
+  vqf_statevector* sv = nullptr;
+  std::vector<double> cs;  // [param][entry] (cos, sin)
+  HbmEngine(uint32_t n_, int32_t kind_, uint32_t layers_, uint32_t batch, int device_)
+      : n(n_), P(ansatz_params(kind_, layers_, n_)), layers(layers_), kind(kind_), device(device_) {
+    if (vqf_sv_create(n, batch, VQF_F64, device, &sv) != VQF_OK) throw Error(VQF_CUDA_ERROR, vqf_last_error());
+  }
+  ~HbmEngine() { vqf_sv_destroy(sv); }
+  HbmEngine(const HbmEngine&) = delete;
+
+  // Prepares circuits; `angle(j, e)` gives parameter j's angle in entry e.
+  template <typename F>
+  void prepare(F&& angle) {
+    const uint32_t B = sv->batch;
+    cs.resize((size_t)std::max(P, 1u) * B * 2);
+    for (uint32_t j = 0; j < P; ++j)
+      for (uint32_t e = 0; e < B; ++e) {
+        const double a = angle(j, e);
+        cs[2 * ((size_t)j * B + e)] = std::cos(0.5 * a);
+        cs[2 * ((size_t)j * B + e) + 1] = std::sin(0.5 * a);
+      }
+    sv_ensure_cs(sv, cs.size());
+    VQF_CUDA(cudaMemcpyAsync(sv->cs_dev, cs.data(), cs.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             sv->stream));
+    const double* csd = sv->cs_dev;
+    if (kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION) {
+      sv_reset(sv, 12);  // basis_state(4, {1,1,0,0})
+      GateArgs g{VQF_GATE_DOUBLE_EXCITATION, 4, {0, 1, 2, 3}, 0, 0, csd};
+      sv_apply(sv, g);
+      return;
+    }
+    sv_reset(sv, 0);
+    uint32_t k = 0;
+    for (uint32_t layer = 0; layer < layers; ++layer) {
+      for (uint32_t q = 0; q < n; ++q, ++k) {
+        GateArgs g{VQF_GATE_RY, 1, {q, 0, 0, 0}, 0, 0, csd + 2 * (size_t)k * B};
+        sv_apply(sv, g);
+      }
+      for (uint32_t q = 0; q + 1 < n; ++q) {
+        GateArgs g{VQF_GATE_CNOT, 2, {q, q + 1, 0, 0}, 0, 0, nullptr};
+        sv_apply(sv, g);
+      }
+    }
+  }
+};
+
+size_t free_device_bytes(int device) {
+  size_t fr = 0, tot = 0;
+  VQF_CUDA(cudaSetDevice(device));
+  VQF_CUDA(cudaMemGetInfo(&fr, &tot));
+  return fr;
+}
+
+// Runs all 2P+1 circuits of one parameter-shift iteration; E[c] complex.
+// Uses one NC-entry batch when it fits in 60% of free memory, else NC
+// sequential single-entry evaluations.
+struct ShiftEvaluator {
+  uint32_t n, P, NC;
+  int32_t kind;
+  uint32_t layers;
+  int device;
+  std::unique_ptr<HbmEngine> eng;
+  bool batched;
+  ShiftEvaluator(uint32_t n_, int32_t kind_, uint32_t layers_, int device_)
+      : n(n_), P(ansatz_params(kind_, layers_, n_)), NC(2 * P + 1), kind(kind_), layers(layers_), device(device_) {
+    const double need = (double)NC * (double)(uint64_t{1} << n) * 16.0;
+    batched = need < 0.6 * (double)free_device_bytes(device);
+    eng = std::make_unique<HbmEngine>(n, kind, layers, batched ? NC : 1, device);
+  }
+  // circuits [c_begin, c_end) of the shift family around theta
+  void run(const std::vector<double>& theta, const CompiledHam& h, int c_count, std::vector<double>& E) {
+    E.assign(2 * (size_t)c_count, 0.0);
+    const auto angle_of = [&](uint32_t j, uint32_t c) {
+      double t = theta[j];
+      if (c == 2 * j + 1) t = theta[j] + kShift;
+      if (c == 2 * j + 2) t = theta[j] - kShift;
+      return t;
+    };
+    if (batched) {
+      eng->prepare([&](uint32_t j, uint32_t e) { return e < (uint32_t)c_count ? angle_of(j, e) : theta[j]; });
+      std::vector<double> tot(2 * (size_t)NC);
+      sv_expectation(eng->sv, h, tot.data());
+      std::copy(tot.begin(), tot.begin() + 2 * c_count, E.begin());
+      return;
+    }
+    for (int c = 0; c < c_count; ++c) {
+      eng->prepare([&](uint32_t j, uint32_t) { return angle_of(j, c); });
+      double tot[2];
+      sv_expectation(eng->sv, h, tot);
+      E[2 * c] = tot[0];
+      E[2 * c + 1] = tot[1];
+    }
+  }
+};
+
+void run_vqe_hbm(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const vqf_adam_config& cfg,
+                 const std::vector<double>& init, int device, vqf_vqe_result* r) {
+  const uint32_t n = h->n_qubits;
+  const CompiledHam ch = compile_hamiltonian(h);
+  ShiftEvaluator ev(n, kind, layers, device);
+  const uint32_t P = ev.P;
+  std::vector<double> theta = init.empty() ? std::vector<double>(P, 0.0) : init;
+  std::vector<double> m(P, 0.0), v(P, 0.0), grad(P), tn(P), mn(P), vn(P), E;
+  int64_t step = 0;
+  uint32_t len = 0;
+  bool converged = false;
+  r->iterations_run = 0;
+  r->circuit_evaluations = 0;
+  auto push = [&](double e) {
+    if (r->trajectory) {
+      if (len >= r->trajectory_capacity) throw_invalid("vqe_result: trajectory capacity too small");
+      r->trajectory[len] = e;
+    }
+    ++len;
+  };
+  double last = 0.0;
+  for (int iter = 0; iter < cfg.max_iterations; ++iter) {
+    ev.run(theta, ch, static_cast<int>(ev.NC), E);
+    if (std::abs(E[1]) >= 1e-10) throw_runtime(imag_msg(E[1]));
+    ++r->circuit_evaluations;
+    if (!std::isfinite(E[0])) throw_runtime(nonfinite_msg(iter, theta.data(), P));
+    push(E[0]);
+    last = E[0];
+    for (uint32_t c = 1; c < ev.NC; ++c)
+      if (std::abs(E[2 * c + 1]) >= 1e-10) throw_runtime(imag_msg(E[2 * c + 1]));
+    for (uint32_t k = 0; k < P; ++k) grad[k] = 0.5 * (E[2 * (2 * k + 1)] - E[2 * (2 * k + 2)]);
+    r->circuit_evaluations += 2 * (uint64_t)P;
+    if (cfg.has_gradient_tolerance) {
+      double g_inf = 0.0;
+      for (double g : grad) g_inf = std::max(g_inf, std::abs(g));
+      if (g_inf < cfg.gradient_tolerance) {
+        converged = true;
+        break;
+      }
+    }
+    host::adam_step(m.data(), v.data(), step, grad.data(), theta.data(), P, cfg, tn.data(), mn.data(), vn.data(),
+                    &step);
+    theta = tn;
+    m = mn;
+    v = vn;
+    r->iterations_run = iter + 1;
+  }
+  if (!converged) {
+    ev.run(theta, ch, 1, E);
+    if (std::abs(E[1]) >= 1e-10) throw_runtime(imag_msg(E[1]));
+    ++r->circuit_evaluations;
+    if (!std::isfinite(E[0])) throw_runtime(nonfinite_msg(cfg.max_iterations, theta.data(), P));
+    push(E[0]);
+    last = E[0];
+  }
+  r->energy = last;
+  r->trajectory_len = len;
+  if (r->theta) std::memcpy(r->theta, theta.data(), P * sizeof(double));
+}
+
+bool small_ok(uint32_t n, uint32_t P) { return n <= (uint32_t)kSmallMaxN && P <= (uint32_t)kSmallMaxP; }
+
+void run_vqe_impl(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const vqf_adam_config* cfg,
+                  const double* init, uint32_t n_init, int32_t method, int32_t device, vqf_vqe_result* r) {
+  const auto t0 = Clock::now();
+  check_adam(cfg);
+  if (h == nullptr || r == nullptr) throw_invalid("null argument");
+  const uint32_t n = h->n_qubits;
+  const uint32_t P = ansatz_params(kind, layers, n);
+  if (n_init != 0 && n_init != P) throw_invalid("initial parameter count mismatch");
+  check_ansatz_register(kind, n);
+  if (method != VQF_GRAD_PARAMETER_SHIFT && method != VQF_GRAD_ADJOINT) throw_invalid("unknown gradient method");
+  std::vector<double> init_v(init, init + n_init);
+  if (small_ok(n, P)) {
+    SmallJob j;
+    j.batch = 1;
+    j.n_qubits = static_cast<int32_t>(n);
+    j.kind = kind;
+    j.layers = static_cast<int32_t>(layers);
+    j.P = P;
+    j.adam = *cfg;
+    const CompiledHam ch = compile_hamiltonian(h);
+    j.terms = ch.terms;
+    j.term_off = {0, static_cast<uint32_t>(ch.terms.size())};
+    j.init_theta = init_v;
+    run_small(j, device);
+    if (j.status[0] != kStatusOk) throw_runtime(small_error(j, 0, 0.0));
+    fill_result(j, 0, r);
+  } else {
+    run_vqe_hbm(h, kind, layers, *cfg, init_v, device, r);
+  }
+  r->wall_seconds = seconds_since(t0);
+}
+
+
+// ------------------------------------------------------------ sweep pieces
+struct SweepSlice {
+  std::vector<double> grid;
+  uint64_t lo = 0, hi = 0;
+};
+
+// bond_grid (sweep.hpp:68-85) and this rank's split_chunks slice of it.
+SweepSlice sweep_slice(const vqf_sweep_config& cfg) {
+  if (cfg.n_points < 1) throw_invalid("grid needs >= 1 point");
+  if (cfg.d_max < cfg.d_min) throw_invalid("d_max < d_min");
+  SweepSlice s;
+  s.grid.resize(cfg.n_points);
+  host::bond_grid(cfg.d_min, cfg.d_max, cfg.n_points, s.grid.data());
+  s.lo = 0;
+  s.hi = s.grid.size();
+  if (cfg.n_chunks > 1) {
+    if (cfg.chunk_index < 0 || cfg.chunk_index >= cfg.n_chunks) throw_invalid("chunk_index out of range");
+    std::vector<uint64_t> be(2 * (size_t)cfg.n_chunks);
+    host::split_chunks(s.grid.size(), cfg.n_chunks, be.data());
+    s.lo = be[2 * cfg.chunk_index];
+    s.hi = be[2 * cfg.chunk_index + 1];
+  }
+  return s;
+}
+
+std::vector<int32_t> sweep_devices(const vqf_sweep_config& cfg) {
+  std::vector<int32_t> devices;
+  if (cfg.devices != nullptr && cfg.n_devices > 0) {
+    devices.assign(cfg.devices, cfg.devices + cfg.n_devices);
+  } else {
+    int nd = 0;
+    VQF_CUDA(cudaGetDeviceCount(&nd));
+    const int use = cfg.n_devices > 0 ? std::min(cfg.n_devices, nd) : nd;
+    for (int d = 0; d < use; ++d) devices.push_back(d);
+  }
+  if (devices.empty()) throw Error(VQF_CUDA_ERROR, "CUDA: no device available");
+  return devices;
+}
+
+// PES job for grid points [b0, b1): bonds outside the supported range are
+// rejected on the host with the BondLengthOutOfRange text (chem.hpp:281-284)
+// and skipped by the kernel.
+SmallJob pes_job(const vqf_sweep_config& cfg, const std::vector<double>& grid, uint64_t b0, uint64_t b1,
+                 std::vector<std::string>& errors) {
+  SmallJob j;
+  j.batch = static_cast<uint32_t>(b1 - b0);
+  j.n_qubits = 4;
+  j.kind = VQF_ANSATZ_H2_DOUBLE_EXCITATION;
+  j.P = 1;
+  j.adam = cfg.adam;
+  j.pes = true;
+  j.bonds.assign(grid.begin() + b0, grid.begin() + b1);
+  j.status_in.assign(j.batch, 0);
+  for (uint32_t b = 0; b < j.batch; ++b) {
+    try {
+      chem::check_bond(j.bonds[b]);
+    } catch (const Error& e) {
+      j.status_in[b] = kStatusBond;
+      errors[b0 + b] = e.what();
+    }
+  }
+  return j;
+}
+
+// Writes points [b0, b1) of the report (SweepPoint, sweep.hpp:48-56).
+void pes_fill(const SmallJob& j, const vqf_sweep_config& cfg, const std::vector<double>& grid, uint64_t b0,
+              uint64_t b1, std::vector<std::string>& errors, vqf_sweep_report* rep) {
+  const uint32_t stride = static_cast<uint32_t>(std::max(cfg.adam.max_iterations, 0)) + 1;
+  for (uint64_t i = b0; i < b1; ++i) {
+    const uint32_t b = static_cast<uint32_t>(i - b0);
+    rep->bond_angstrom[i] = grid[i];
+    rep->energy_hartree[i] = std::nan("");
+    rep->theta_star[i] = std::nan("");
+    rep->iterations[i] = 0;
+    rep->ok[i] = 0;
+    if (rep->wall_seconds) rep->wall_seconds[i] = j.device_seconds;
+    if (j.status.empty() || j.status[b] == kStatusBond) continue;
+    if (j.status[b] != kStatusOk) {
+      errors[i] = small_error(j, b, j.bonds[b]);
+      continue;
+    }
+    rep->energy_hartree[i] = j.energy[b];
+    rep->theta_star[i] = j.theta[b];
+    rep->iterations[i] = j.iters[b];
+    rep->ok[i] = 1;
+    if (rep->trajectories && !j.traj.empty())
+      std::memcpy(rep->trajectories + i * stride, j.traj.data() + (size_t)b * stride, stride * sizeof(double));
+  }
+}
+
+void pes_finish(const SweepSlice& sl, const std::vector<std::string>& errors, vqf_sweep_report* rep) {
+  int all_ok = 1;
+  for (uint64_t i = sl.lo; i < sl.hi; ++i) {
+    all_ok = all_ok && rep->ok[i];
+    if (rep->errors && rep->error_stride) {
+      char* dst = rep->errors + i * rep->error_stride;
+      std::strncpy(dst, errors[i].c_str(), rep->error_stride - 1);
+      dst[rep->error_stride - 1] = '\0';
+    }
+  }
+  rep->all_ok = all_ok;
+}
+
+}  // namespace
+
+}  // namespace vqf
+
+// Device-resident PES plan (vqf_pes_create).
+struct vqf_pes_plan {
+  vqf_sweep_config cfg{};
+  int device = 0;
+  vqf::SweepSlice slice;
+  std::vector<std::string> errors;
+  vqf::SmallJob job;
+  std::unique_ptr<vqf::SmallStage> stage;
+  vqf::SmallParams params{};
+  cudaStream_t stream = nullptr;
+  cudaStream_t last_stream = nullptr;
+  void* dev = nullptr;
+  void* pin = nullptr;
+};
+
+using namespace vqf;
+
+extern "C" {
+
+int vqf_prepare_ansatz(int32_t kind, uint32_t layers, const double* theta, uint32_t n_theta, vqf_sv sv) {
+  return guarded([&] {
+    if (sv == nullptr) throw_invalid("null state vector");
+    const uint32_t P = ansatz_params(kind, layers, sv->n_qubits);
+    if (n_theta != P) throw_invalid("parameter count mismatch for ansatz");
+    check_ansatz_register(kind, sv->n_qubits);
+    VQF_CUDA(cudaSetDevice(sv->device));
+    if (kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION) {
+      sv_reset(sv, 12);
+      GateArgs g{VQF_GATE_DOUBLE_EXCITATION, 4, {0, 1, 2, 3}, std::cos(0.5 * theta[0]), std::sin(0.5 * theta[0]),
+                 nullptr};
+      sv_apply(sv, g);
+    } else {
+      sv_reset(sv, 0);
+      const uint32_t n = sv->n_qubits;
+      uint32_t k = 0;
+      for (uint32_t layer = 0; layer < layers; ++layer) {
+        for (uint32_t q = 0; q < n; ++q, ++k) {
+          GateArgs g{VQF_GATE_RY, 1, {q, 0, 0, 0}, std::cos(0.5 * theta[k]), std::sin(0.5 * theta[k]), nullptr};
+          sv_apply(sv, g);
+        }
+        for (uint32_t q = 0; q + 1 < n; ++q) {
+          GateArgs g{VQF_GATE_CNOT, 2, {q, q + 1, 0, 0}, 0, 0, nullptr};
+          sv_apply(sv, g);
+        }
+      }
+    }
+    VQF_CUDA(cudaStreamSynchronize(sv->stream));
+  });
+}
+
+int vqf_energy(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h, int32_t kind, uint32_t layers,
+               int32_t device, double* out) {
+  return guarded([&] {
+    if (h == nullptr || out == nullptr) throw_invalid("null argument");
+    const uint32_t P = ansatz_params(kind, layers, h->n_qubits);
+    if (n_theta != P) throw_invalid("parameter count mismatch for ansatz");
+    check_ansatz_register(kind, h->n_qubits);
+    const CompiledHam ch = compile_hamiltonian(h);
+    HbmEngine eng(h->n_qubits, kind, layers, 1, device);
+    eng.prepare([&](uint32_t j, uint32_t) { return theta[j]; });
+    double tot[2];
+    sv_expectation(eng.sv, ch, tot);
+    if (std::abs(tot[1]) >= 1e-10) throw_runtime(imag_msg(tot[1]));
+    *out = tot[0];
+  });
+}
+
+int vqf_gradient(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h, int32_t kind, uint32_t layers,
+                 int32_t method, int32_t device, double* grad_out) {
+  return guarded([&] {
+    if (h == nullptr || grad_out == nullptr) throw_invalid("null argument");
+    const uint32_t P = ansatz_params(kind, layers, h->n_qubits);
+    if (n_theta != P) throw_invalid("parameter count mismatch for ansatz");
+    check_ansatz_register(kind, h->n_qubits);
+    if (method != VQF_GRAD_PARAMETER_SHIFT && method != VQF_GRAD_ADJOINT) throw_invalid("unknown gradient method");
+    const CompiledHam ch = compile_hamiltonian(h);
+    ShiftEvaluator ev(h->n_qubits, kind, layers, device);
+    std::vector<double> th(theta, theta + n_theta), E;
+    ev.run(th, ch, static_cast<int>(ev.NC), E);
+    for (uint32_t c = 1; c < ev.NC; ++c)
+      if (std::abs(E[2 * c + 1]) >= 1e-10) throw_runtime(imag_msg(E[2 * c + 1]));
+    for (uint32_t k = 0; k < P; ++k) grad_out[k] = 0.5 * (E[2 * (2 * k + 1)] - E[2 * (2 * k + 2)]);
+  });
+}
+
+int vqf_run_vqe(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const vqf_adam_config* config,
+                const double* init, uint32_t n_init, int32_t method, int32_t device, vqf_vqe_result* result) {
+  return guarded([&] { run_vqe_impl(h, kind, layers, config, init, n_init, method, device, result); });
+}
+
+int vqf_run_vqe_batch(const vqf_hamiltonian* hs, uint32_t batch, int32_t kind, uint32_t layers,
+                      const vqf_adam_config* config, int32_t device, vqf_vqe_result* results) {
+  return guarded([&] {
+    check_adam(config);
+    if (batch == 0) return;
+    if (hs == nullptr || results == nullptr) throw_invalid("null argument");
+    const uint32_t n = hs[0].n_qubits;
+    const uint32_t P = ansatz_params(kind, layers, n);
+    check_ansatz_register(kind, n);
+    for (uint32_t b = 1; b < batch; ++b)
+      if (hs[b].n_qubits != n) throw_invalid("run_vqe_batch: all problems must share the register size");
+    if (!small_ok(n, P)) {
+      for (uint32_t b = 0; b < batch; ++b)
+        run_vqe_impl(&hs[b], kind, layers, config, nullptr, 0, VQF_GRAD_PARAMETER_SHIFT, device, &results[b]);
+      return;
+    }
+    const auto t0 = Clock::now();
+    SmallJob j;
+    j.batch = batch;
+    j.n_qubits = static_cast<int32_t>(n);
+    j.kind = kind;
+    j.layers = static_cast<int32_t>(layers);
+    j.P = P;
+    j.adam = *config;
+    j.term_off.push_back(0);
+    for (uint32_t b = 0; b < batch; ++b) {
+      const CompiledHam ch = compile_hamiltonian(&hs[b]);
+      j.terms.insert(j.terms.end(), ch.terms.begin(), ch.terms.end());
+      j.term_off.push_back(static_cast<uint32_t>(j.terms.size()));
+    }
+    run_small(j, device);
+    for (uint32_t b = 0; b < batch; ++b)
+      if (j.status[b] != kStatusOk) throw_runtime(small_error(j, b, 0.0));
+    const double wall = seconds_since(t0);
+    for (uint32_t b = 0; b < batch; ++b) {
+      fill_result(j, b, &results[b]);
+      results[b].wall_seconds = wall;
+    }
+  });
+}
+
+int vqf_run_sweep(const vqf_sweep_config* cfg, vqf_sweep_report* rep) {
+  return guarded([&] {
+    if (cfg == nullptr || rep == nullptr) throw_invalid("null argument");
+    if (cfg->workers < 1) throw_invalid("workers must be >= 1");  // sweep.hpp:129
+    const auto start = Clock::now();
+    const SweepSlice sl = sweep_slice(*cfg);
+    const int W = cfg->workers;
+    std::vector<uint64_t> wbe(2 * (size_t)W);
+    host::split_chunks(sl.hi - sl.lo, W, wbe.data());
+    const std::vector<int32_t> devices = sweep_devices(*cfg);
+
+    std::vector<std::string> errors(sl.grid.size());
+    std::vector<double> dev_secs(W, 0.0);
+    std::vector<size_t> h2d(W, 0), d2h(W, 0);
+    std::vector<std::exception_ptr> fails(W);
+    auto worker = [&](int w) {
+      try {
+        const auto tw = Clock::now();
+        const uint64_t b0 = sl.lo + wbe[2 * w], b1 = sl.lo + wbe[2 * w + 1];
+        SmallJob j = pes_job(*cfg, sl.grid, b0, b1, errors);
+        if (j.batch > 0) {
+          run_small(j, devices[w % devices.size()], rep->trajectories != nullptr, &h2d[w], &d2h[w]);
+          dev_secs[w] = j.device_seconds;
+        }
+        pes_fill(j, *cfg, sl.grid, b0, b1, errors, rep);
+        if (rep->per_worker_seconds) rep->per_worker_seconds[w] = seconds_since(tw);
+      } catch (...) {
+        fails[w] = std::current_exception();
+      }
+    };
+    if (W == 1) {
+      worker(0);
+    } else {
+      std::vector<std::thread> pool;
+      pool.reserve(W);
+      for (int w = 0; w < W; ++w) pool.emplace_back(worker, w);
+      for (auto& t : pool) t.join();
+    }
+    for (auto& f : fails)
+      if (f) std::rethrow_exception(f);
+    pes_finish(sl, errors, rep);
+    rep->device_seconds = *std::max_element(dev_secs.begin(), dev_secs.end());
+    rep->h2d_bytes = 0;
+    rep->d2h_bytes = 0;
+    for (int w = 0; w < W; ++w) {
+      rep->h2d_bytes += h2d[w];
+      rep->d2h_bytes += d2h[w];
+    }
+    rep->total_wall_seconds = seconds_since(start);
+  });
+}
+
+int vqf_pes_create(const vqf_sweep_config* cfg, int32_t device, vqf_pes* out) {
+  return guarded([&] {
+    if (cfg == nullptr || out == nullptr) throw_invalid("null argument");
+    auto plan = std::make_unique<vqf_pes_plan>();
+    plan->cfg = *cfg;
+    plan->cfg.devices = nullptr;
+    plan->device = device;
+    plan->slice = sweep_slice(*cfg);
+    plan->errors.assign(plan->slice.grid.size(), std::string());
+    plan->job = pes_job(*cfg, plan->slice.grid, plan->slice.lo, plan->slice.hi, plan->errors);
+    plan->stage = std::make_unique<SmallStage>(plan->job);
+    VQF_CUDA(cudaSetDevice(device));
+    VQF_CUDA(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+    VQF_CUDA(cudaMalloc(&plan->dev, std::max<size_t>(plan->stage->total, 16)));
+    VQF_CUDA(cudaMallocHost(&plan->pin, std::max<size_t>(plan->stage->total, 16)));
+    plan->stage->pack(plan->job, static_cast<unsigned char*>(plan->pin));
+    plan->params = plan->stage->params(plan->job, static_cast<unsigned char*>(plan->dev));
+    VQF_CUDA(cudaMemcpyAsync(plan->dev, plan->pin, plan->stage->in_end, cudaMemcpyHostToDevice, plan->stream));
+    VQF_CUDA(cudaStreamSynchronize(plan->stream));
+    *out = plan.release();
+  });
+}
+
+int vqf_pes_launch(vqf_pes plan, void* stream) {
+  return guarded([&] {
+    if (plan == nullptr) throw_invalid("null plan");
+    if (plan->job.batch == 0) return;
+    VQF_CUDA(cudaSetDevice(plan->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->stream;
+    launch_vqe_small(plan->params, plan->job.batch, true, s);
+    plan->last_stream = s;
+  });
+}
+
+int vqf_pes_read(vqf_pes plan, vqf_sweep_report* rep) {
+  return guarded([&] {
+    if (plan == nullptr || rep == nullptr) throw_invalid("null argument");
+    VQF_CUDA(cudaSetDevice(plan->device));
+    auto* pin = static_cast<unsigned char*>(plan->pin);
+    auto* dev = static_cast<unsigned char*>(plan->dev);
+    const SmallStage& st = *plan->stage;
+    const bool traj = rep->trajectories != nullptr;
+    cudaStream_t s = plan->last_stream ? plan->last_stream : plan->stream;
+    if (plan->job.batch > 0) {
+      VQF_CUDA(cudaMemcpyAsync(pin + st.o_status, dev + st.o_status, st.d2h_bytes(traj), cudaMemcpyDeviceToHost, s));
+      VQF_CUDA(cudaStreamSynchronize(s));
+      st.unpack(plan->job, pin, traj);
+    }
+    std::vector<std::string> errors = plan->errors;
+    pes_fill(plan->job, plan->cfg, plan->slice.grid, plan->slice.lo, plan->slice.hi, errors, rep);
+    pes_finish(plan->slice, errors, rep);
+    rep->h2d_bytes = 0;
+    rep->d2h_bytes = plan->job.batch > 0 ? st.d2h_bytes(traj) : 0;
+  });
+}
+
+int vqf_pes_destroy(vqf_pes plan) {
+  return guarded([&] {
+    if (plan == nullptr) return;
+    cudaSetDevice(plan->device);
+    if (plan->stream) cudaStreamSynchronize(plan->stream);
+    if (plan->dev) cudaFree(plan->dev);
+    if (plan->pin) cudaFreeHost(plan->pin);
+    if (plan->stream) cudaStreamDestroy(plan->stream);
+    delete plan;
+  });
+}
+
+int vqf_run_scaling_study(const vqf_scaling_config* cfg, vqf_scaling_record* records) {
+  return guarded([&] {
+    if (cfg == nullptr || records == nullptr) throw_invalid("null argument");
+    for (uint32_t i = 0; i < cfg->n_widths; ++i) {  // sweep.hpp:267-275
+      const uint32_t n = cfg->qubits[i];
+      if (n < 2) throw_invalid("scaling study needs >= 2 qubits");
+      if (n > 26 && !cfg->force)
+        throw_invalid("refusing " + std::to_string(n) + " qubits (> 26, state alone exceeds 1 GiB); pass force to override");
+    }
+    for (uint32_t i = 0; i < cfg->n_widths; ++i) {
+      const uint32_t n = cfg->qubits[i];
+      if (n > 22)
+        std::cerr << "warning: " << n << " qubits needs " << vqf_memory_estimate(n) / (1024.0 * 1024.0 * 1024.0)
+                  << " GiB of state\n";
+      const auto terms = cfg->z_sum_mode ? host::build_z_sum(n) : host::build_tfim(n, cfg->coupling, cfg->field);
+      std::vector<double> coeffs(2 * terms.size());
+      std::vector<uint32_t> offs(terms.size() + 1), qs;
+      std::vector<uint8_t> ax;
+      for (size_t t = 0; t < terms.size(); ++t) {
+        coeffs[2 * t] = terms[t].coeff.real();
+        coeffs[2 * t + 1] = terms[t].coeff.imag();
+        for (const auto& [q, a] : terms[t].axes) {
+          qs.push_back(q);
+          ax.push_back(a);
+        }
+        offs[t + 1] = static_cast<uint32_t>(qs.size());
+      }
+      vqf_hamiltonian h{n, static_cast<uint32_t>(terms.size()), coeffs.data(), offs.data(), qs.data(), ax.data()};
+      vqf_adam_config adam{0.01, 0.9, 0.999, 1e-8, 200, 0, 0.0};
+      adam.learning_rate = cfg->learning_rate;
+      adam.max_iterations = cfg->iterations;
+      const uint32_t P = cfg->layers * n;
+      std::vector<double> init(P, cfg->theta_init), theta(P);
+      vqf_vqe_result r{};
+      r.theta = theta.data();
+      const auto t0 = Clock::now();
+      run_vqe_impl(&h, VQF_ANSATZ_HARDWARE_EFFICIENT, cfg->layers, &adam, init.data(), P, cfg->gradient_method,
+                   cfg->device, &r);
+      records[i].n_qubits = n;
+      records[i].state_bytes = vqf_memory_estimate(n);
+      records[i].runtime_seconds = seconds_since(t0);
+      records[i].final_energy = r.energy;
+      records[i].iterations_run = r.iterations_run;
+    }
+  });
+}
+
+}  // extern "C"

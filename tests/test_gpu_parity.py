@@ -1,0 +1,392 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the CPU oracle
+and the reference's golden fixtures.  Bar (BASELINE.json north_star):
+energies within 1e-10 Ha in fp64 (1e-5 in fp32), bit-identical iteration
+counts and bond grid, results independent of GPU/worker count.
+Amplitudes: 1e-12 per amplitude (the reference's own test tolerance,
+test_statevector.cpp:150-166)."""
+from __future__ import annotations
+
+import math
+import random
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Ham, random_hamiltonian, random_state
+from vqf_helpers import ham_from_text
+
+pytestmark = pytest.mark.gpu
+
+E_TOL = 1e-10   # fp64 energies (north_star)
+A_TOL = 1e-12   # amplitudes (test_statevector.cpp:166)
+
+
+def to_v(V, h: Ham):
+    return V.QubitHamiltonian(h.n_qubits, [V.PauliTerm(c, a) for c, a in h.terms])
+
+
+def rand_gates(pr, n, count, kinds=(0, 1, 2, 3, 4)):
+    out = []
+    for _ in range(count):
+        k = pr.choice([k for k in kinds if [1, 1, 2, 4, 2][k] <= n])
+        ws = pr.sample(range(n), [1, 1, 2, 4, 2][k])
+        out.append((k, pr.uniform(-3.14, 3.14), ws))
+    return out
+
+
+def gpu_gate(V, k, angle, ws):
+    return V.Gate(k, angle, tuple(ws))
+
+
+# ------------------------------------------------------------ state vector
+def test_basis_state_and_reset(gpu):
+    V = gpu
+    psi = V.basis_state(4, [1, 1, 0, 0])
+    a = psi.amplitudes
+    assert a[12] == 1 and np.count_nonzero(a) == 1
+    assert V.basis_state(2, [0, 1]).amplitudes[1] == 1
+    with pytest.raises(ValueError, match="bit count"):
+        V.basis_state(2, [0, 1, 0])
+    z = V.StateVector(3)
+    assert z.amplitudes[0] == 1 and abs(z.norm() - 1.0) < 1e-15
+
+
+@pytest.mark.parametrize("n", [4, 5, 7, 10, 13])
+def test_gates_match_oracle(gpu, orc, n):
+    V = gpu
+    rng = np.random.default_rng(100 + n)
+    pr = random.Random(200 + n)
+    psi0 = random_state(rng, n)
+    gates = rand_gates(pr, n, 40, kinds=(0, 1, 2, 3))
+    want = orc.apply_gates(n, psi0, gates)
+    psi = V.StateVector(n)
+    psi.amplitudes = psi0
+    V.apply_circuit(psi, [gpu_gate(V, *g) for g in gates])
+    got = psi.amplitudes
+    assert np.max(np.abs(got - want)) < A_TOL
+    # per-gate too (each kind on every wire position class)
+    psi.amplitudes = psi0
+    cur = psi0
+    for g in gates[:8]:
+        V.apply_gate(psi, gpu_gate(V, *g))
+        cur = orc.apply_gates(n, cur, [g])
+        assert np.max(np.abs(psi.amplitudes - cur)) < A_TOL
+
+
+def test_gate_goldens(gpu, golden):
+    V = gpu
+    for c in golden("gates_expectation.json")["cases"]:
+        n = c["n"]
+        psi = V.StateVector(n)
+        psi.amplitudes = np.array([complex(*x) for x in c["psi"]])
+        V.apply_circuit(psi, [V.Gate(k, a, tuple(w)) for k, a, w in c["gates"]])
+        want = np.array([complex(*x) for x in c["out"]])
+        assert np.max(np.abs(psi.amplitudes - want)) < A_TOL
+        h, _ = ham_from_text(V, n, c["hamiltonian"]["text"])
+        assert abs(V.expectation(psi, h) - c["expectation_out"]) < E_TOL
+
+
+def test_single_excitation_properties(gpu):
+    """SingleExcitation (appended kind): Givens on |10>,|01>, angles add,
+    norm preserved."""
+    V = gpu
+    psi = V.basis_state(2, [1, 0])
+    V.apply_gate(psi, V.Gate.single_excitation(0.6, 0, 1))
+    a = psi.amplitudes
+    assert abs(a[2].real - math.cos(0.3)) < 1e-15 and abs(a[1].real - math.sin(0.3)) < 1e-15
+    rng = np.random.default_rng(3)
+    x = random_state(rng, 6)
+    p, q = V.StateVector(6), V.StateVector(6)
+    p.amplitudes = x
+    q.amplitudes = x
+    V.apply_circuit(p, [V.Gate.single_excitation(0.4, 1, 4), V.Gate.single_excitation(-1.1, 1, 4)])
+    V.apply_gate(q, V.Gate.single_excitation(-0.7, 1, 4))
+    assert np.max(np.abs(p.amplitudes - q.amplitudes)) < 1e-12
+    assert abs(p.norm() - 1.0) < 1e-12
+
+
+def test_gate_validation(gpu):
+    V = gpu
+    psi = V.StateVector(2)
+    with pytest.raises(ValueError, match="exceeds register"):
+        V.apply_gate(psi, V.Gate.pauli_x(2))
+    with pytest.raises(ValueError, match="duplicate gate wire"):
+        V.apply_gate(psi, V.Gate.cnot(0, 0))
+    with pytest.raises(ValueError, match="exceeds register"):
+        V.apply_gate(psi, V.Gate.double_excitation(1.0, 0, 1, 2, 3))
+    with pytest.raises(ValueError, match="wire count"):
+        V.apply_gate(psi, V.Gate(1, 0.1, (0, 1)))
+
+
+@pytest.mark.parametrize("n", [1, 4, 6, 9, 12])
+def test_expectation_matches_oracle(gpu, orc, n):
+    V = gpu
+    rng = np.random.default_rng(300 + n)
+    for trial in range(5):
+        pr = random.Random(1000 * n + trial)
+        h = orc.canonicalize(random_hamiltonian(pr, n, 12 if trial else 40, real=True))
+        psi0 = random_state(rng, n)
+        psi = V.StateVector(n)
+        psi.amplitudes = psi0
+        assert abs(V.expectation(psi, to_v(V, h)) - orc.expectation(n, psi0, h)) < E_TOL
+
+
+def test_expectation_tfim_and_diagonal(gpu, orc):
+    V = gpu
+    for n in [2, 5, 11, 16]:
+        h = orc.build_tfim(n, 1.0, 0.7)
+        psi0 = random_state(np.random.default_rng(n), n)
+        psi = V.StateVector(n)
+        psi.amplitudes = psi0
+        assert abs(V.expectation(psi, to_v(V, h)) - orc.expectation(n, psi0, h)) < E_TOL
+    # test_statevector.cpp:185-196
+    z = V.QubitHamiltonian(1, [V.PauliTerm(1.0, [(0, 3)])])
+    assert abs(V.expectation(V.StateVector(1), z) - 1.0) < 1e-15
+    ones = V.basis_state(4, [1, 1, 1, 1])
+    assert abs(V.expectation(ones, V.build_z_sum(4)) + 4.0) < 1e-15
+    with pytest.raises(ValueError, match="qubit count mismatch"):
+        V.expectation(V.StateVector(2), V.QubitHamiltonian(3, [V.PauliTerm(1.0, [(0, 3)])]))
+
+
+def test_expectation_imaginary_residue_raises(gpu):
+    V = gpu
+    psi = V.StateVector(2)
+    V.apply_gate(psi, V.Gate.ry(0.7, 0))
+    h = V.QubitHamiltonian(2, [V.PauliTerm(1j, [])])  # non-Hermitian: <psi|iI|psi> = i
+    with pytest.raises(RuntimeError, match="imaginary residue"):
+        V.expectation(psi, h)
+
+
+def test_norm_preserved_random_circuit(gpu):
+    # test_statevector.cpp:168-175 at larger widths
+    V = gpu
+    pr = random.Random(20260803)
+    for n in [4, 16, 22]:
+        psi = V.StateVector(n)
+        V.apply_circuit(psi, [gpu_gate(V, *g) for g in rand_gates(pr, n, 60)])
+        assert abs(psi.norm() - 1.0) < 1e-10
+
+
+def test_f32_state_within_tolerance(gpu, orc):
+    V = gpu
+    n = 12
+    rng = np.random.default_rng(11)
+    pr = random.Random(12)
+    psi0 = random_state(rng, n)
+    gates = rand_gates(pr, n, 30, kinds=(0, 1, 2, 3))
+    h = orc.build_tfim(n, 1.0, 1.0)
+    want = orc.expectation(n, orc.apply_gates(n, psi0, gates), h)
+    psi = V.StateVector(n, dtype="f32")
+    psi.amplitudes = psi0
+    V.apply_circuit(psi, [gpu_gate(V, *g) for g in gates])
+    assert abs(V.expectation(psi, to_v(V, h)) - want) < 1e-5
+
+
+# -------------------------------------------------------------------- vqe
+def test_prepare_ansatz_and_energy(gpu, orc, ref):
+    V = gpu
+    H2 = V.AnsatzSpec.h2_double_excitation()
+    a = V.prepare_ansatz(H2, [math.pi], 4).amplitudes
+    assert abs(a[3].real - 1) < 1e-15 and abs(a[12]) < 1e-15  # test_vqe.cpp:49-52
+    for th in [-2.0, 0.3, 1.7]:
+        a = V.prepare_ansatz(H2, [th], 4).amplitudes
+        assert np.count_nonzero(np.delete(a, [3, 12])) == 0
+    with pytest.raises(ValueError, match="parameter count"):
+        V.prepare_ansatz(H2, [0.0, 0.0], 4)
+    with pytest.raises(ValueError, match="requires 4 qubits"):
+        V.prepare_ansatz(H2, [0.0], 6)
+    hea = V.AnsatzSpec.hardware_efficient(2)
+    th = np.random.default_rng(1).uniform(-3, 3, 12)
+    assert np.max(np.abs(V.prepare_ansatz(hea, th, 6).amplitudes - orc.prepare_ansatz(1, 2, th, 6))) < A_TOL
+    # test_vqe.cpp:82-89 E(0) = HF energy
+    for d in [0.5, 0.7414, 1.6]:
+        h = to_v(V, ref.build_h2_hamiltonian(d))
+        assert abs(V.energy([0.0], h, H2) - ref.hartree_fock(d)["hf_energy"]) < E_TOL
+    h = ref.build_tfim(6, 1.0, 1.0)
+    assert abs(V.energy(th, to_v(V, h), hea) - orc.energy(1, 2, th, h)) < E_TOL
+
+
+def test_gradient_matches_oracle(gpu, orc):
+    V = gpu
+    rng = np.random.default_rng(20260811)
+    for d in [0.6, 1.3, 2.4]:
+        h = orc.build_h2_hamiltonian(d)
+        th = [rng.uniform(-3, 3)]
+        g = V.gradient(th, to_v(V, h), V.AnsatzSpec.h2_double_excitation())
+        assert abs(g[0] - orc.gradient(0, 0, th, h)[0]) < E_TOL
+    h = orc.build_tfim(7, 1.0, 1.0)
+    th = rng.uniform(-1, 1, 14)
+    g = V.gradient(th, to_v(V, h), V.AnsatzSpec.hardware_efficient(2))
+    assert np.max(np.abs(g - orc.gradient(1, 2, th, h))) < E_TOL
+    # test_vqe.cpp:108-117
+    g = V.gradient([0.0] * 4, V.build_z_sum(4), V.AnsatzSpec.hardware_efficient(1))
+    assert np.max(np.abs(g)) < 1e-12
+
+
+def test_run_vqe_h2_matches_golden(gpu, golden, ref):
+    V = gpu
+    g = golden("vqe_runs.json")["h2"]
+    H2 = V.AnsatzSpec.h2_double_excitation()
+    for d, want in g.items():
+        h = to_v(V, ref.build_h2_hamiltonian(float(d)))
+        r = V.run_vqe(h, H2)
+        assert r.iterations_run == 200 and len(r.trajectory) == 201
+        assert r.circuit_evaluations == want["circuit_evaluations"] == 601
+        assert np.max(np.abs(np.array(r.trajectory) - want["trajectory"])) < E_TOL
+        assert abs(r.energy - want["energy"]) < E_TOL and r.energy == r.trajectory[-1]
+        assert abs(r.theta[0] - want["theta"][0]) < 1e-8
+
+
+def test_run_vqe_tolerance_mode_iterations(gpu, ref):
+    V = gpu
+    H2 = V.AnsatzSpec.h2_double_excitation()
+    cfg = V.AdamConfig(max_iterations=5000, gradient_tolerance=1e-8)
+    for d in [0.7414, 1.2, 2.6]:  # test_vqe.cpp:152-169
+        h = ref.build_h2_hamiltonian(d)
+        want = ref.run_vqe(h, max_iter=5000, tol=1e-8)
+        r = V.run_vqe(to_v(V, h), H2, cfg)
+        assert r.iterations_run == want["iterations_run"]
+        assert len(r.trajectory) == r.iterations_run + 1
+        assert abs(r.energy - want["energy"]) < E_TOL
+    r = V.run_vqe(to_v(V, ref.build_h2_hamiltonian(0.7414)), H2, V.AdamConfig(gradient_tolerance=1e3))
+    assert r.iterations_run == 0 and len(r.trajectory) == 1 and r.circuit_evaluations == 3
+    r = V.run_vqe(to_v(V, ref.build_h2_hamiltonian(0.9)), H2, V.AdamConfig(max_iterations=5))
+    assert r.circuit_evaluations == 16
+
+
+def test_run_vqe_errors_and_init(gpu, ref):
+    V = gpu
+    H2 = V.AnsatzSpec.h2_double_excitation()
+    bad = V.QubitHamiltonian(4, [V.PauliTerm(complex(float("nan"), 0.0), [])])
+    with pytest.raises(RuntimeError, match=r"non-finite energy at iteration 0; theta = 0\.000000"):
+        V.run_vqe(bad, H2)
+    h = to_v(V, ref.build_h2_hamiltonian(0.7414))
+    with pytest.raises(ValueError, match="initial parameter count mismatch"):
+        V.run_vqe(h, H2, V.AdamConfig(), [0.1, 0.2])
+    r = V.run_vqe(h, H2, V.AdamConfig(max_iterations=0), [0.25])
+    assert r.theta == [0.25] and abs(r.energy - V.energy([0.25], h, H2)) < E_TOL
+    a = V.run_vqe(h, H2, V.AdamConfig(max_iterations=80))
+    b = V.run_vqe(h, H2, V.AdamConfig(max_iterations=80))
+    assert a.trajectory == b.trajectory and a.theta == b.theta  # test_vqe.cpp:216-226
+
+
+@pytest.mark.parametrize("key", ["tfim4", "zsum5", "tfim6", "tfim8"])
+def test_run_vqe_hea_matches_golden(gpu, golden, key):
+    V = gpu
+    g = golden("vqe_runs.json")["hea"][key]
+    n = g["hamiltonian"]["n_qubits"]
+    h, _ = ham_from_text(V, n, g["hamiltonian"]["text"])
+    r = V.run_vqe(h, V.AnsatzSpec.hardware_efficient(g["layers"]),
+                  V.AdamConfig(learning_rate=g["lr"], max_iterations=g["max_iterations"]), [g["theta_init"]] * (2 * n))
+    assert np.max(np.abs(np.array(r.trajectory) - g["trajectory"])) < E_TOL
+    assert np.max(np.abs(np.array(r.theta) - g["theta"])) < 1e-9
+    assert r.circuit_evaluations == g["circuit_evaluations"]
+
+
+def test_run_vqe_batch(gpu, ref):
+    V = gpu
+    hs = [to_v(V, ref.build_h2_hamiltonian(d)) for d in [0.4, 0.8, 1.5, 2.9]]
+    rs = V.run_vqe_batch(hs, V.AnsatzSpec.h2_double_excitation(), V.AdamConfig(max_iterations=50))
+    for h, r in zip(hs, rs):
+        one = V.run_vqe(h, V.AnsatzSpec.h2_double_excitation(), V.AdamConfig(max_iterations=50))
+        assert r.trajectory == one.trajectory and r.theta == one.theta  # batch position independent
+
+
+# ------------------------------------------------------------------ sweep
+def test_run_sweep_default_matches_reference(gpu, golden):
+    """The north-star workload: 100 bonds x 200 iterations."""
+    V = gpu
+    p = golden("pes_default.json")
+    rep = V.run_sweep(V.SweepConfig(), trajectories=True)
+    assert rep.all_ok
+    assert [pt.bond_angstrom for pt in rep.points] == p["bond"]  # bitwise grid
+    assert [pt.iterations for pt in rep.points] == p["iterations"]
+    err = max(abs(pt.energy_hartree - e) for pt, e in zip(rep.points, p["energy"]))
+    assert err < E_TOL, err
+    i = int(np.argmin([pt.energy_hartree for pt in rep.points]))
+    assert 0.70 <= rep.points[i].bond_angstrom <= 0.78 and abs(rep.points[i].energy_hartree + 1.137) < 0.005
+    assert all(len(pt.trajectory) == 201 for pt in rep.points)
+
+
+def test_run_sweep_tolerance_mode_iterations(gpu, golden):
+    V = gpu
+    t = golden("pes_default.json")["tol_mode"]
+    rep = V.run_sweep(V.SweepConfig(adam=V.AdamConfig(max_iterations=5000, gradient_tolerance=1e-8)))
+    assert [pt.iterations for pt in rep.points] == t["iterations"]  # bit-identical counts
+    assert max(abs(pt.energy_hartree - e) for pt, e in zip(rep.points, t["energy"])) < E_TOL
+
+
+def test_run_sweep_worker_and_chunk_independence(gpu):
+    # test_sweep.cpp:101-129 / acceptance criterion 8
+    V = gpu
+    base = dict(d_min=0.5, d_max=2.0, n_points=8, adam=V.AdamConfig(max_iterations=25))
+    reps = [V.run_sweep(V.SweepConfig(workers=w, **base)) for w in (1, 2, 3)]
+    for rep in reps:
+        assert rep.all_ok and len(rep.per_worker_seconds) >= 1
+        for a, b in zip(rep.points, reps[0].points):
+            assert (a.bond_angstrom, a.energy_hartree, a.theta_star, a.iterations) == \
+                   (b.bond_angstrom, b.energy_hartree, b.theta_star, b.iterations)
+    # rank-sharded (one process per GPU) slices reassemble the same points
+    pts = []
+    for r in range(3):
+        pts += V.run_sweep(V.SweepConfig(chunk_index=r, n_chunks=3, **base)).points
+    assert [(p.bond_angstrom, p.energy_hartree, p.iterations) for p in pts] == \
+           [(p.bond_angstrom, p.energy_hartree, p.iterations) for p in reps[0].points]
+
+
+def test_run_sweep_failing_point(gpu):
+    # test_sweep.cpp:131-143
+    V = gpu
+    rep = V.run_sweep(V.SweepConfig(d_min=0.01, d_max=1.0, n_points=2, adam=V.AdamConfig(max_iterations=10)))
+    assert not rep.all_ok and not rep.points[0].ok and rep.points[0].error
+    assert "outside" in rep.points[0].error and math.isnan(rep.points[0].energy_hartree)
+    assert rep.points[1].ok
+    with pytest.raises(ValueError, match="workers must be >= 1"):
+        V.run_sweep(V.SweepConfig(workers=0))
+
+
+def test_scaling_study_zsum(gpu, golden):
+    # test_sweep.cpp:195-212 configuration vs the reference's fixture
+    V = gpu
+    g = golden("scaling_zsum.json")
+    c = g["config"]
+    recs = V.run_scaling_study(V.ScalingConfig(qubits=c["qubits"], layers=c["layers"], iterations=c["iterations"],
+                                               learning_rate=c["learning_rate"], z_sum_mode=True))
+    for r, w in zip(recs, g["records"]):
+        assert r["n_qubits"] == w["n_qubits"] and r["state_bytes"] == w["state_bytes"]
+        assert r["iterations_run"] == w["iterations_run"]
+        assert abs(r["final_energy"] - w["final_energy"]) < E_TOL
+    with pytest.raises(ValueError, match="refusing 28 qubits"):
+        V.run_scaling_study(V.ScalingConfig(qubits=[28]))
+    with pytest.raises(ValueError, match=">= 2 qubits"):
+        V.run_scaling_study(V.ScalingConfig(qubits=[1]))
+
+
+def test_scaling_study_tfim_wide_matches_oracle(gpu, orc):
+    """HBM engine path (n > 5) for run_scaling_study semantics."""
+    V = gpu
+    for n in [8, 12]:
+        h = orc.build_tfim(n, 1.0, 1.0)
+        want = orc.run_vqe(h, kind=1, layers=2, lr=0.05, max_iter=3, init=[0.1] * (2 * n))
+        rec = V.run_scaling_study(V.ScalingConfig(qubits=[n], iterations=3))[0]
+        assert abs(rec["final_energy"] - want["energy"]) < E_TOL and rec["iterations_run"] == 3
+
+
+# ------------------------------------------- full-size property checks
+def test_large_register_properties(gpu):
+    """n = 28 (4 GiB fp64): oracle-free, size-independent properties:
+    norm preserved, RY(a)RY(b) = RY(a+b) up to rounding, X X = I exactly,
+    DE(t) DE(-t) = I, expectation of Z-sum on |0..0> = n."""
+    V = gpu
+    n = 28
+    psi = V.StateVector(n)
+    V.apply_circuit(psi, [V.Gate.ry(0.3, q) for q in range(n)])
+    assert abs(psi.norm() - 1.0) < 1e-10
+    e = V.expectation(psi, V.build_z_sum(n))
+    assert abs(e - n * math.cos(0.3)) < 1e-9
+    V.apply_circuit(psi, [V.Gate.pauli_x(0), V.Gate.pauli_x(0), V.Gate.cnot(3, 27), V.Gate.cnot(3, 27)])
+    assert abs(V.expectation(psi, V.build_z_sum(n)) - e) < 1e-12
+    V.apply_circuit(psi, [V.Gate.double_excitation(0.9, 0, 1, 2, 3), V.Gate.double_excitation(-0.9, 0, 1, 2, 3)])
+    V.apply_circuit(psi, [V.Gate.ry(-0.3, q) for q in range(n)])
+    z = V.expectation(psi, V.build_z_sum(n))
+    assert abs(z - n) < 1e-9
