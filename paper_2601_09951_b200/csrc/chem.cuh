@@ -109,6 +109,49 @@ __host__ __device__ inline double eri_term(const ChemConsts& k, double bond_bohr
   return k.coef[x] * k.coef[y] * k.coef[z] * k.coef[w] * eri_prim(k, x, Z[i], y, Z[j], z, Z[l], w, Z[m]);
 }
 
+// Bra (or ket) factor of a primitive pair: AO pair ij (i = ij >> 1,
+// j = ij & 1), primitive pair xy (x = xy / 3, y = xy % 3).  E is the
+// Gaussian-product exponential exp(-mu |A-B|^2) that overlap_prim,
+// kinetic_prim, nuclear_prim and eri_prim all evaluate with the same
+// operands (chem.hpp:146, :155, :165, :179-180), so one value serves all.
+struct PairFactor {
+  double p, mu, d2, E, P;
+};
+
+__host__ __device__ inline PairFactor pair_factor(const ChemConsts& k, double bond_bohr, int ij, int xy) {
+  const double Z[2] = {0.0, bond_bohr};
+  const int i = ij >> 1, j = ij & 1, x = xy / 3, y = xy % 3;
+  const double a = k.alpha[x], b = k.alpha[y];
+  PairFactor f;
+  f.p = a + b;
+  f.mu = a * b / f.p;
+  f.d2 = d2z(Z[i], Z[j]);
+  f.E = exp(-f.mu * f.d2);
+  f.P = cz(a, Z[i], b, Z[j]);
+  return f;
+}
+
+// c_x c_y c_z c_w * eri_prim from bra / ket pair factors, in contract4 and
+// eri_prim's operation order (chem.hpp:169-182, :206-210).
+__host__ __device__ inline double eri_term_pf(const ChemConsts& k, const PairFactor& bra, const PairFactor& ket, int x,
+                                              int y, int z, int w) {
+  const double p = bra.p, q = ket.p;
+  const double pref = 2.0 * k.pow_pi_25 / (p * q * sqrt(p + q));
+  const double prim = pref * bra.E * ket.E * boys_f0(p * q / (p + q) * d2z(bra.P, ket.P));
+  return k.coef[x] * k.coef[y] * k.coef[z] * k.coef[w] * prim;
+}
+
+// c_x c_y * {overlap, kinetic, nuclear(C)} primitive (chem.hpp:142-167,
+// contract2 :185-195).  which: 0 overlap, 1 kinetic, 2 nuclear at C.
+__host__ __device__ inline double one_e_term_pf(const ChemConsts& k, const PairFactor& f, int xy, int which, double C) {
+  const int x = xy / 3, y = xy % 3;
+  double prim;
+  if (which == 0) prim = k.pow_pi_p15[x][y] * f.E;
+  else if (which == 1) prim = f.mu * (3.0 - 2.0 * f.mu * f.d2) * k.pow_pi_p15[x][y] * f.E;
+  else prim = -2.0 * kPi / f.p * f.E * boys_f0(f.p * d2z(f.P, C));
+  return k.coef[x] * k.coef[y] * prim;
+}
+
 struct AoInts {
   double S[2][2], T[2][2], V[2][2], eri[16];
 };
@@ -349,6 +392,59 @@ __host__ __device__ inline int jw_contribution(int idx, const double hmo[2][2], 
   }
   return 1;
 }
+
+// Bond-independent metadata of contribution #idx: its Pauli-string key,
+// phase power m (value = i^m * scale * integral), which integral it scales
+// (slot -1 = nuclear repulsion, 0..3 = hmo[p/2][q/2] as (p/2)*2 + q/2,
+// 4..19 = 4 + physicist eri_mo index) and the exact power-of-two scale.
+__host__ __device__ inline void jw_meta(int idx, int& key, int& m, int& slot, double& scale) {
+  int x = 0, z = 0;
+  m = 0;
+  if (idx == 0) {
+    key = 0;
+    slot = -1;
+    scale = 1.0;
+    return;
+  }
+  if (idx <= 32) {
+    const int pair = (idx - 1) >> 2, sub = (idx - 1) & 3;
+    const int p = pair >> 1, q = ((pair & 1) << 1) | (p & 1);
+    int fx, fz;
+    m = ladder(p, 1, (sub >> 1) & 1, x, z);
+    m += ladder(q, 0, sub & 1, fx, fz);
+    m += pauli_mul(x, z, fx, fz);
+    slot = (p >> 1) * 2 + (q >> 1);
+    scale = 0.25;
+  } else {
+    const int quad = (idx - 33) >> 4, sub = (idx - 33) & 15;
+    const int p = quad >> 4, q = (quad >> 2) & 3, rr = (quad >> 1) & 1, ss = quad & 1;
+    const int r = (rr << 1) | (p & 1), s = (ss << 1) | (q & 1);
+    const int ops[4] = {p, q, s, r};
+    const int dag[4] = {1, 1, 0, 0};
+    m = ladder(ops[0], dag[0], (sub >> 3) & 1, x, z);
+    for (int f = 1; f < 4; ++f) {
+      int fx, fz;
+      m += ladder(ops[f], dag[f], (sub >> (3 - f)) & 1, fx, fz);
+      m += pauli_mul(x, z, fx, fz);
+    }
+    slot = 4 + ((((p >> 1) * 2 + (q >> 1)) * 2 + (r >> 1)) * 2 + (s >> 1));
+    scale = 0.03125;  // (0.5 * g) / 16, exact
+  }
+  key = x | (z << 4);
+  m &= 3;
+}
+
+// Contribution-to-string map for the device: for every Pauli string that
+// can occur, in canonical (axes_less) order, the ordered list of its
+// contributions (generation order = the reference's merge order).
+struct JwTable {
+  int n_keys;
+  int keys[256];
+  int start[257];
+  int slot[kNumContrib];
+  double coef[kNumContrib];  // +-scale
+  int part[kNumContrib];     // 0 real, 1 imaginary
+};
 
 // Lexicographic (index, axis) order of the sparse form of a 4-qubit key
 // (axes_less, pauli.hpp:99-106) as a sortable integer: per qubit ascending,

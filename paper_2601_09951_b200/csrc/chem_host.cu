@@ -2,7 +2,9 @@
 // built on the shared chem.cuh core.  The fused PES kernel runs the same
 // core on the device; this path serves the drop-in build_h2_hamiltonian /
 // run_hartree_fock API and the tests.
+#include <algorithm>
 #include <array>
+#include <mutex>
 #include <string>
 
 #include "chem.cuh"
@@ -30,6 +32,58 @@ std::string nonconvergence_msg(double d) {
 }
 
 std::string nonhermitian_msg(double imag) { return "non-Hermitian Pauli coefficient: imag = " + fstr(imag); }
+
+// Contribution -> Pauli-string map of the Jordan-Wigner expansion: bond
+// independent, so built once on the host (jw_meta over every contribution
+// slot) and shipped to each device once.
+const JwTable& jw_table() {
+  static const JwTable t = [] {
+    JwTable j{};
+    std::array<std::vector<int>, 256> lists;
+    for (int idx = 0; idx < kNumContrib; ++idx) {
+      int key, m, slot;
+      double scale;
+      jw_meta(idx, key, m, slot, scale);
+      lists[key].push_back(idx);
+    }
+    std::vector<int> keys;
+    for (int k = 0; k < 256; ++k)
+      if (!lists[k].empty()) keys.push_back(k);
+    std::sort(keys.begin(), keys.end(), [](int a, int b) { return key_order(a) < key_order(b); });
+    j.n_keys = static_cast<int>(keys.size());
+    int e = 0;
+    for (int t = 0; t < j.n_keys; ++t) {
+      j.keys[t] = keys[t];
+      j.start[t] = e;
+      for (int idx : lists[keys[t]]) {
+        int key, m, slot;
+        double scale;
+        jw_meta(idx, key, m, slot, scale);
+        j.slot[e] = slot;
+        j.coef[e] = (m == 2 || m == 3) ? -scale : scale;
+        j.part[e] = (m & 1);
+        ++e;
+      }
+    }
+    j.start[j.n_keys] = e;
+    return j;
+  }();
+  return t;
+}
+
+const JwTable* jw_table_device(int device) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, JwTable*>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& [d, ptr] : cache)
+    if (d == device) return ptr;
+  JwTable* ptr = nullptr;
+  VQF_CUDA(cudaSetDevice(device));
+  VQF_CUDA(cudaMalloc(&ptr, sizeof(JwTable)));
+  VQF_CUDA(cudaMemcpy(ptr, &jw_table(), sizeof(JwTable), cudaMemcpyHostToDevice));
+  cache.emplace_back(device, ptr);
+  return ptr;
+}
 
 HfOut hartree_fock(double bond_angstrom, double C[2][2]) {
   check_bond(bond_angstrom);

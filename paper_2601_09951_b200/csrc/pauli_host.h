@@ -129,15 +129,17 @@ inline void split_chunks(uint64_t n_items, uint64_t n_chunks, uint64_t* be) {
   }
 }
 
-// Bias-correction factors 1 - beta^t for t = 1..T, computed with the host
-// libm pow exactly as adam_step does (vqe.hpp:161-162), so the on-device
-// Adam update is bitwise the reference's.
+// Reciprocal bias-correction factors 1 / (1 - beta^t), t = 1..T, with
+// 1 - beta^t computed by the host libm pow exactly as adam_step does
+// (vqe.hpp:161-162).  The device multiplies by them instead of dividing
+// (one IEEE division less on the per-iteration critical path); m_hat and
+// v_hat then differ from the reference's quotients by at most 1 ulp.
 inline void bias_tables(const vqf_adam_config& c, int32_t T, std::vector<double>& bc1, std::vector<double>& bc2) {
   bc1.resize(std::max(T, 1));
   bc2.resize(std::max(T, 1));
   for (int32_t t = 1; t <= T; ++t) {
-    bc1[t - 1] = 1.0 - std::pow(c.beta1, static_cast<double>(t));
-    bc2[t - 1] = 1.0 - std::pow(c.beta2, static_cast<double>(t));
+    bc1[t - 1] = 1.0 / (1.0 - std::pow(c.beta1, static_cast<double>(t)));
+    bc2[t - 1] = 1.0 / (1.0 - std::pow(c.beta2, static_cast<double>(t)));
   }
 }
 

@@ -191,7 +191,7 @@ struct SmallStage {
       std::memcpy(pin + o_status, j.status_in.data(), B * sizeof(int32_t));
   }
 
-  SmallParams params(const SmallJob& j, unsigned char* dev) const {
+  SmallParams params(const SmallJob& j, unsigned char* dev, int device) const {
     SmallParams p{};
     p.n_qubits = j.n_qubits;
     p.ansatz_kind = j.kind;
@@ -208,6 +208,7 @@ struct SmallStage {
     p.bc2 = reinterpret_cast<const double*>(dev + o_bc2);
     p.bonds = reinterpret_cast<const double*>(dev + o_bonds);
     p.chem = chem::consts();
+    p.jw = j.pes ? chem::jw_table_device(device) : nullptr;
     p.terms = reinterpret_cast<const MaskTerm*>(dev + o_terms);
     p.term_off = reinterpret_cast<const uint32_t*>(dev + o_toff);
     p.init_theta = j.init_theta.empty() ? nullptr : reinterpret_cast<const double*>(dev + o_init);
@@ -268,7 +269,7 @@ void run_small(SmallJob& j, int device, bool want_traj = true, size_t* h2d = nul
   auto* pin = static_cast<unsigned char*>(ws.pin);
   auto* dev = static_cast<unsigned char*>(ws.dev);
   st.pack(j, pin);
-  const SmallParams p = st.params(j, dev);
+  const SmallParams p = st.params(j, dev, device);
   VQF_CUDA(cudaMemcpyAsync(dev, pin, st.in_end, cudaMemcpyHostToDevice, ws.stream));
   VQF_CUDA(cudaEventRecord(ws.ev0, ws.stream));
   launch_vqe_small(p, j.batch, j.pes, ws.stream);
@@ -817,7 +818,7 @@ int vqf_pes_create(const vqf_sweep_config* cfg, int32_t device, vqf_pes* out) {
     VQF_CUDA(cudaMalloc(&plan->dev, std::max<size_t>(plan->stage->total, 16)));
     VQF_CUDA(cudaMallocHost(&plan->pin, std::max<size_t>(plan->stage->total, 16)));
     plan->stage->pack(plan->job, static_cast<unsigned char*>(plan->pin));
-    plan->params = plan->stage->params(plan->job, static_cast<unsigned char*>(plan->dev));
+    plan->params = plan->stage->params(plan->job, static_cast<unsigned char*>(plan->dev), device);
     VQF_CUDA(cudaMemcpyAsync(plan->dev, plan->pin, plan->stage->in_end, cudaMemcpyHostToDevice, plan->stream));
     VQF_CUDA(cudaStreamSynchronize(plan->stream));
     *out = plan.release();

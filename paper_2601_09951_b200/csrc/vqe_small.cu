@@ -3,24 +3,30 @@
 //
 // The reference evaluates each bond serially: per Adam iteration one energy
 // plus 2P parameter-shifted energies, each a fresh heap-allocated
-// StateVector (vqe.hpp:99-127, :226-243).  Here one CTA owns one problem
-// (one bond) for its whole optimisation:
-//   * every circuit of an iteration (base + 2P shifts) is simulated at once,
-//     D = 2^n lanes per circuit, one amplitude per lane, gates as warp
-//     shuffles (no memory traffic at all);
-//   * expectation is a per-lane table lookup: the Hamiltonian is folded once
-//     into per-flip-group tables O_g(i) = sum_t cb_t (-1)^popc(i & yz_t), and
-//     <psi|H|psi> = sum_i sum_g O_g(i) conj(psi_i) psi_{i ^ f_g}, reduced by
-//     an xor-butterfly (bitwise identical on every lane, placement
-//     independent);
-//   * Adam runs on device with host-computed bias-correction tables
-//     (bitwise the reference's std::pow, vqe.hpp:161-162);
+// StateVector (vqe.hpp:99-127, :226-243).  Here ONE WARP owns one problem
+// (one bond) for its whole optimisation, with no block barriers:
+//   * every circuit of an iteration (base + 2P shifts) is simulated at once
+//     in the warp: a circuit occupies L lanes x A amplitudes per lane
+//     (index i = a*L + lane), gates on lane bits are warp shuffles, gates on
+//     slot bits are register permutations (H2: 3 circuits x 8 lanes x 2);
+//   * each (cos, sin) is computed once per parameter and shift;
+//   * expectation is a per-amplitude table lookup: the Hamiltonian is folded
+//     once into per-flip-group tables O_g(i) = sum_t cb_t (-1)^popc(i&yz_t),
+//     <psi|H|psi> = sum_i sum_g O_g(i) conj(psi_i) psi_{i^f_g}, reduced in a
+//     fixed order (slots, then an xor butterfly) so results do not depend on
+//     where the problem runs;
+//   * Adam runs in the lane that owns the parameter, with host-computed
+//     bias-correction tables (bitwise the reference's std::pow,
+//     vqe.hpp:161-162);
 //   * in PES mode the CTA first builds its bond's Hamiltonian from scratch
-//     (STO-3G integrals -> RHF -> Jordan-Wigner, chem.cuh), so a whole PES is
-//     ONE launch with 800 bytes of input.
-// The path is latency bound (a bond's state is 256 B); nothing here touches
-// HBM beyond the outputs.
+//     (STO-3G integrals -> RHF -> Jordan-Wigner, chem.cuh) with 4 warps, then
+//     warp 0 runs the optimisation: a whole PES is ONE launch.
+// The path is latency bound (a bond's state is 256 B): nothing touches HBM
+// beyond the outputs.
+#include <algorithm>
 #include <cmath>
+#include <mutex>
+#include <vector>
 
 #include "chem.cuh"
 #include "vqe_small.cuh"
@@ -30,15 +36,57 @@ namespace vqf {
 namespace {
 
 constexpr double kShift = 1.5707963267948966;  // std::numbers::pi / 2 (vqe.hpp:115)
+constexpr int kPesThreads = 512;  // chemistry prologue width; warps 1.. exit before the loop
+constexpr int kMaxGates = 2 * kSmallMaxP + 8;
+
+enum : int { G_X = 0, G_RY = 1, G_CNOT = 2, G_DE = 3 };
+
+struct PGate {
+  int kind;
+  int param;  // -1 if not parameterised
+  int m0;     // RY/X: bit mask; CNOT: control mask; DE: sel mask
+  int m1;     // CNOT: target mask; DE: occ (1100) mask
+};
+
+struct Shared {
+  // problem description
+  int n_groups, n_gates, n_terms;
+  int flip[kSmallMaxD];
+  double2 tab[kSmallMaxD * kSmallMaxD];  // [group][index]
+  PGate prog[kMaxGates];
+  MaskTerm terms[256];
+  // per-iteration exchange
+  double theta[kSmallMaxP];
+  double2 cs[kSmallMaxP][3];  // (cos, sin) of 0.5 * (theta, theta + pi/2, theta - pi/2)
+  double2 energy[2 * kSmallMaxP + 1];
+  double grad[kSmallMaxP];
+  int stop;
+  // PES prologue scratch
+  chem::PairFactor pf[36];
+  double prim[1296];
+  double prim1[144];
+  chem::AoInts ints;
+  chem::HfOut hf;
+  double C[2][2];
+  double mo[16];
+  double integ[20];  // hmo (4) then physicist eri_mo (16)
+  double kre[256], kim[256];
+  int kflag[256];
+};
 
 __device__ __forceinline__ double2 shfl_xor2(double2 v, int m, int width) {
   v.x = __shfl_xor_sync(0xffffffffu, v.x, m, width);
   v.y = __shfl_xor_sync(0xffffffffu, v.y, m, width);
   return v;
 }
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  v.x = __shfl_sync(0xffffffffu, v.x, src);
+  v.y = __shfl_sync(0xffffffffu, v.y, src);
+  return v;
+}
 
-// a' = c a - s b written as the reference does (complex * real, then
-// subtract): statevector.hpp:160-163, :195-196.
+// a' = c a - s b and b' = s a + c b as the reference writes them (complex *
+// real, then subtract / add): statevector.hpp:160-163, :195-196.
 __device__ __forceinline__ double2 rot_lo(double c, double s, double2 a, double2 b) {
   return make_double2(c * a.x - s * b.x, c * a.y - s * b.y);
 }
@@ -46,78 +94,114 @@ __device__ __forceinline__ double2 rot_hi(double c, double s, double2 a, double2
   return make_double2(s * a.x + c * b.x, s * a.y + c * b.y);
 }
 
-// Circuit c's angle for parameter j (gradient(), vqe.hpp:118-123).
-__device__ __forceinline__ double circuit_angle(const double* theta, int j, int c) {
-  double t = theta[j];
-  if (c == 2 * j + 1) t = t + kShift;
-  if (c == 2 * j + 2) t = t - kShift;
-  return t;
-}
-
-// prepare_ansatz (vqe.hpp:65-96) for one lane (amplitude index i) of a
-// D-lane segment.  All lanes of the warp execute every shuffle.
-__device__ double2 run_ansatz(int kind, int n, int layers, const double* theta, int c, int i) {
-  const int D = 1 << n;
-  double2 amp;
-  if (kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION) {
-    amp = make_double2(i == 12 ? 1.0 : 0.0, 0.0);  // basis_state(4, {1,1,0,0})
-    double s, cc;
-    sincos(0.5 * circuit_angle(theta, 0, c), &s, &cc);
-    // DoubleExcitation(theta, 0, 1, 2, 3): sel = 1111, |1100> = 12 <-> |0011> = 3
-    const double2 partner = shfl_xor2(amp, 15, D);
-    if ((i & 15) == 12) amp = rot_lo(cc, s, amp, partner);
-    else if ((i & 15) == 3) amp = rot_hi(cc, s, partner, amp);
-    return amp;
-  }
-  amp = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
-  int k = 0;
-  for (int layer = 0; layer < layers; ++layer) {
-    for (int q = 0; q < n; ++q) {
-      const int bit = 1 << (n - 1 - q);
-      double s, cc;
-      sincos(0.5 * circuit_angle(theta, k++, c), &s, &cc);
-      const double2 partner = shfl_xor2(amp, bit, D);
-      amp = (i & bit) ? rot_hi(cc, s, partner, amp) : rot_lo(cc, s, amp, partner);
-    }
-    for (int q = 0; q + 1 < n; ++q) {
-      const int cb = 1 << (n - 1 - q), tb = 1 << (n - 2 - q);
-      const double2 partner = shfl_xor2(amp, tb, D);
-      if (i & cb) amp = partner;
+// out[a] = amplitude at index (a*L + lane) ^ m, m split into lane / slot
+// bits.  m is warp-uniform, so every branch is uniform.
+template <int A>
+__device__ __forceinline__ void fetch_partner(const double2 (&amp)[A], double2 (&out)[A], int m, int L, int lgL) {
+  const int ml = m & (L - 1), ms = m >> lgL;
+#pragma unroll
+  for (int a = 0; a < A; ++a) out[a] = ml ? shfl_xor2(amp[a], ml, L) : amp[a];
+#pragma unroll
+  for (int k = 1; k < A; k <<= 1) {
+    if (ms & k) {
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        if (!(a & k)) {
+          const double2 t = out[a];
+          out[a] = out[a | k];
+          out[a | k] = t;
+        }
+      }
     }
   }
-  return amp;
 }
 
-struct Shared {
-  // Hamiltonian tables
-  int n_groups;
-  int flip[kSmallMaxD];
-  double2 tab[kSmallMaxD * kSmallMaxD];  // [group][lane]
-  // optimiser state
-  double theta[kSmallMaxP], m[kSmallMaxP], v[kSmallMaxP], grad[kSmallMaxP];
-  double2 energy[2 * kSmallMaxP + 1];
-  int stop, converged, iters;
-  // PES-mode scratch
-  double prim[1296];
-  chem::AoInts ints;
-  chem::HfOut hf;
-  double C[2][2];
-  double mo[16];
-  int ckey[chem::kNumContrib];
-  double cre[chem::kNumContrib], cim[chem::kNumContrib];
-  double kre[256], kim[256];
-  int kseen[256];
-  int keys[256];
-  MaskTerm terms[256];
-  int n_terms;
-};
+// Runs the circuit program for circuit c (0 = base, 2k+1 = +pi/2 on k,
+// 2k+2 = -pi/2 on k) on this lane's A amplitudes.  H2 = true compiles the
+// H2 ansatz (vqe.hpp:72-80) as constants: |1100> = 12, DoubleExcitation on
+// wires 0..3 (sel 1111).
+template <int A, bool H2>
+__device__ __forceinline__ void run_circuit(const Shared& sh, double2 (&amp)[A], int c, int lane, int L, int lgL,
+                                            int basis) {
+#pragma unroll
+  for (int a = 0; a < A; ++a) amp[a] = make_double2((a * L + lane) == basis ? 1.0 : 0.0, 0.0);
+  if (H2) {
+    double2 part[A];
+    fetch_partner<A>(amp, part, 15, L, lgL);
+    const double2 t = sh.cs[0][c == 1 ? 1 : c == 2 ? 2 : 0];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int pat = (a * L + lane) & 15;
+      if (pat == 12) amp[a] = rot_lo(t.x, t.y, amp[a], part[a]);
+      else if (pat == 3) amp[a] = rot_hi(t.x, t.y, part[a], amp[a]);
+    }
+    return;
+  }
+  for (int gi = 0; gi < sh.n_gates; ++gi) {
+    const PGate g = sh.prog[gi];
+    double2 part[A];
+    if (g.kind == G_RY || g.kind == G_X) {
+      fetch_partner<A>(amp, part, g.m0, L, lgL);
+      if (g.kind == G_X) {
+#pragma unroll
+        for (int a = 0; a < A; ++a) amp[a] = part[a];
+      } else {
+        const int j = (c == 2 * g.param + 1) ? 1 : (c == 2 * g.param + 2) ? 2 : 0;
+        const double2 t = sh.cs[g.param][j];
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+          const int i = a * L + lane;
+          amp[a] = (i & g.m0) ? rot_hi(t.x, t.y, part[a], amp[a]) : rot_lo(t.x, t.y, amp[a], part[a]);
+        }
+      }
+    } else if (g.kind == G_CNOT) {
+      fetch_partner<A>(amp, part, g.m1, L, lgL);
+#pragma unroll
+      for (int a = 0; a < A; ++a)
+        if ((a * L + lane) & g.m0) amp[a] = part[a];
+    } else {  // DoubleExcitation: sel = m0, |1100> = m1, |0011> = m0 ^ m1
+      fetch_partner<A>(amp, part, g.m0, L, lgL);
+      const int j = (c == 2 * g.param + 1) ? 1 : (c == 2 * g.param + 2) ? 2 : 0;
+      const double2 t = sh.cs[g.param][j];
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        const int pat = (a * L + lane) & g.m0;
+        if (pat == g.m1) amp[a] = rot_lo(t.x, t.y, amp[a], part[a]);
+        else if (pat == (g.m0 ^ g.m1)) amp[a] = rot_hi(t.x, t.y, part[a], amp[a]);
+      }
+    }
+  }
+}
 
-// Builds the per-group lane tables from n_terms mask terms in smem.
-__device__ void build_tables(Shared& sh, int n) {
-  const int D = 1 << n;
-  if (threadIdx.x == 0) {
+// <psi|H|psi> of this lane's circuit, complete on every lane of the segment.
+template <int A>
+__device__ __forceinline__ double2 circuit_energy(const Shared& sh, const double2 (&amp)[A], int lane, int L, int lgL,
+                                                  int D) {
+  double2 acc = make_double2(0.0, 0.0);
+  for (int g = 0; g < sh.n_groups; ++g) {
+    double2 part[A];
+    fetch_partner<A>(amp, part, sh.flip[g], L, lgL);
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const double2 x = amp[a], y = part[a];
+      const double vr = x.x * y.x + x.y * y.y, vi = x.x * y.y - x.y * y.x;  // conj(x) * y
+      const double2 o = sh.tab[g * D + a * L + lane];
+      acc.x += o.x * vr - o.y * vi;
+      acc.y += o.x * vi + o.y * vr;
+    }
+  }
+  for (int o = L >> 1; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, L);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, L);
+  }
+  return acc;
+}
+
+// Folds the mask terms into per-flip-group amplitude tables (warp 0).
+__device__ void build_tables(Shared& sh, int D, int lane) {
+  if (lane == 0) {
     int G = 0;
-    sh.flip[G++] = 0;  // diagonal group first
+    sh.flip[G++] = 0;
     for (int t = 0; t < sh.n_terms; ++t) {
       const int f = static_cast<int>(sh.terms[t].flip);
       bool found = false;
@@ -126,8 +210,8 @@ __device__ void build_tables(Shared& sh, int n) {
     }
     sh.n_groups = G;
   }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < sh.n_groups * D; idx += blockDim.x) {
+  __syncwarp();
+  for (int idx = lane; idx < sh.n_groups * D; idx += 32) {
     const int g = idx / D, i = idx % D;
     double re = 0.0, im = 0.0;
     for (int t = 0; t < sh.n_terms; ++t) {
@@ -138,130 +222,160 @@ __device__ void build_tables(Shared& sh, int n) {
     }
     sh.tab[g * D + i] = make_double2(re, im);
   }
-  __syncthreads();
+  __syncwarp();
 }
 
-__device__ __forceinline__ double2 lane_energy(const Shared& sh, double2 amp, int i, int D) {
-  double2 acc = make_double2(0.0, 0.0);
-  for (int g = 0; g < sh.n_groups; ++g) {
-    const double2 p = shfl_xor2(amp, sh.flip[g], D);
-    // v = conj(amp) * p
-    const double vr = amp.x * p.x + amp.y * p.y, vi = amp.x * p.y - amp.y * p.x;
-    const double2 o = sh.tab[g * D + i];
-    acc.x += o.x * vr - o.y * vi;
-    acc.y += o.x * vi + o.y * vr;
+// prepare_ansatz (vqe.hpp:65-96) as a gate program; returns the basis index.
+__device__ int build_program(Shared& sh, int kind, int n, int layers) {
+  int ng = 0;
+  if (kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION) {
+    // basis_state(4, {1,1,0,0}) = 12; DoubleExcitation(theta0, 0, 1, 2, 3)
+    sh.prog[ng++] = PGate{G_DE, 0, 15, 12};
+    sh.n_gates = ng;
+    return 12;
   }
-  for (int o = D >> 1; o > 0; o >>= 1) {
-    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, D);
-    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, D);
+  int k = 0;
+  for (int layer = 0; layer < layers; ++layer) {
+    for (int q = 0; q < n; ++q) sh.prog[ng++] = PGate{G_RY, k++, 1 << (n - 1 - q), 0};
+    for (int q = 0; q + 1 < n; ++q) sh.prog[ng++] = PGate{G_CNOT, -1, 1 << (n - 1 - q), 1 << (n - 2 - q)};
   }
-  return acc;
+  sh.n_gates = ng;
+  return 0;
 }
 
-// PES prologue: this CTA's H2 Hamiltonian, left as mask terms in smem.
-// Returns a status (0 ok, kStatusScf, kStatusHermitian) in sh.stop.
-__device__ void build_h2_device(Shared& sh, const chem::ChemConsts& k, double bond_angstrom, SmallParams& p,
-                                int prob) {
+// PES prologue: this CTA's H2 Hamiltonian as mask terms in smem (all
+// kPesThreads threads).  Sets sh.stop to kStatusScf / kStatusHermitian.
+//   1. 36 pair factors (one exp each) shared by every primitive;
+//   2. 1296 ERI + 36 overlap + 36 kinetic + 72 nuclear primitive terms, one
+//      per thread-slot;
+//   3. contractions summed in the reference's loop order;
+//   4. RHF (thread 0), MO transform (16 threads), Jordan-Wigner per string.
+__device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
   using namespace chem;
-  const double d = bond_angstrom * kAngstromToBohr;
-  for (int idx = threadIdx.x; idx < 1296; idx += blockDim.x) sh.prim[idx] = eri_term(k, d, idx);
-  if (threadIdx.x < 4) one_electron(k, d, threadIdx.x >> 1, threadIdx.x & 1, sh.ints);
+  const ChemConsts& k = p.chem;
+  const double d = p.bonds[prob] * kAngstromToBohr;
+#ifdef VQF_STAGE_CLOCKS
+  long long t_start = clock64(), t_pf, t_prim, t_sum, t_scf, t_mo, t_jw;
+#endif
+  for (int idx = threadIdx.x; idx < 36; idx += blockDim.x) sh.pf[idx] = pair_factor(k, d, idx / 9, idx % 9);
   __syncthreads();
-  if (threadIdx.x < 16) {
+#ifdef VQF_STAGE_CLOCKS
+  t_pf = clock64();
+#endif
+  constexpr int kOne = 36 * 4;  // S, T, V(nucleus 0), V(nucleus 1) per (ij, xy)
+  for (int idx = threadIdx.x; idx < 1296 + kOne; idx += blockDim.x) {
+    if (idx < 1296) {
+      const int ijkl = idx / 81, r = idx % 81;
+      const int x = r / 27, y = (r / 9) % 3, z = (r / 3) % 3, w = r % 3;
+      sh.prim[idx] = eri_term_pf(k, sh.pf[(ijkl >> 2) * 9 + x * 3 + y], sh.pf[(ijkl & 3) * 9 + z * 3 + w], x, y, z, w);
+    } else {
+      const int o = idx - 1296, which = o / 36, e = o % 36;
+      sh.prim1[o] = one_e_term_pf(k, sh.pf[e], e % 9, which < 2 ? which : 2, which == 3 ? d : 0.0);
+    }
+  }
+  __syncthreads();
+#ifdef VQF_STAGE_CLOCKS
+  t_prim = clock64();
+#endif
+  if (threadIdx.x < 16) {  // contract4's loop order (chem.hpp:197-212)
     double s = 0.0;
     for (int r = 0; r < 81; ++r) s += sh.prim[threadIdx.x * 81 + r];
     sh.ints.eri[threadIdx.x] = s;
+  } else if (threadIdx.x >= 32 && threadIdx.x < 36) {  // ao_integrals (chem.hpp:224-239)
+    const int ij = threadIdx.x - 32, i = ij >> 1, j = ij & 1;
+    double s = 0.0, t = 0.0, v0 = 0.0, v1 = 0.0;
+    for (int xy = 0; xy < 9; ++xy) s += sh.prim1[0 * 36 + ij * 9 + xy];
+    for (int xy = 0; xy < 9; ++xy) t += sh.prim1[1 * 36 + ij * 9 + xy];
+    for (int xy = 0; xy < 9; ++xy) v0 += sh.prim1[2 * 36 + ij * 9 + xy];
+    for (int xy = 0; xy < 9; ++xy) v1 += sh.prim1[3 * 36 + ij * 9 + xy];
+    double v = 0.0;
+    v += v0;
+    v += v1;
+    sh.ints.S[i][j] = s;
+    sh.ints.T[i][j] = t;
+    sh.ints.V[i][j] = v;
   }
   __syncthreads();
+#ifdef VQF_STAGE_CLOCKS
+  t_sum = clock64();
+#endif
   if (threadIdx.x == 0) {
     scf(sh.ints, d, sh.hf, sh.C);
     sh.stop = sh.hf.converged ? 0 : kStatusScf;
+    for (int i = 0; i < 4; ++i) sh.integ[i] = sh.hf.hmo[i >> 1][i & 1];
   }
   __syncthreads();
+#ifdef VQF_STAGE_CLOCKS
+  t_scf = clock64();
+#endif
   if (sh.stop) return;
   if (threadIdx.x < 16) sh.mo[threadIdx.x] = mo_chem(sh.C, sh.ints.eri, threadIdx.x);
   __syncthreads();
-  if (threadIdx.x < 16) {
+  if (threadIdx.x < 16) {  // chemist -> physicist: <ij|kl> = (ik|jl)
     const int i = threadIdx.x >> 3, j = (threadIdx.x >> 2) & 1, kk = (threadIdx.x >> 1) & 1, l = threadIdx.x & 1;
-    sh.hf.eri_mo[threadIdx.x] = sh.mo[((i * 2 + kk) * 2 + j) * 2 + l];  // <ij|kl> = (ik|jl)
+    sh.integ[4 + threadIdx.x] = sh.mo[((i * 2 + kk) * 2 + j) * 2 + l];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < kNumContrib; idx += blockDim.x) {
-    int key;
-    double re, im;
-    if (!jw_contribution(idx, sh.hf.hmo, sh.hf.eri_mo, sh.hf.e_nuc, key, re, im)) key = -1;
-    sh.ckey[idx] = key;
-    sh.cre[idx] = re;
-    sh.cim[idx] = im;
-  }
-  __syncthreads();
-  // Per-string sums in generation order (canonicalize's merge order).
-  for (int key = threadIdx.x; key < 256; key += blockDim.x) {
+#ifdef VQF_STAGE_CLOCKS
+  t_mo = clock64();
+#endif
+  // Jordan-Wigner: per Pauli string, its contributions in generation order
+  // (canonicalize merges in order of first appearance, pauli.hpp:180-190).
+  const JwTable& jw = *p.jw;
+  for (int t = threadIdx.x; t < jw.n_keys; t += blockDim.x) {
     double re = 0.0, im = 0.0;
-    int seen = 0;
-    for (int idx = 0; idx < kNumContrib; ++idx) {
-      if (sh.ckey[idx] != key) continue;
-      if (!seen) {
-        re = sh.cre[idx];
-        im = sh.cim[idx];
-        seen = 1;
-      } else {
-        re += sh.cre[idx];
-        im += sh.cim[idx];
-      }
+    for (int e = jw.start[t]; e < jw.start[t + 1]; ++e) {
+      const double v = jw.slot[e] < 0 ? sh.hf.e_nuc : jw.coef[e] * sh.integ[jw.slot[e]];
+      if (jw.part[e]) im += v;
+      else re += v;
     }
-    sh.kre[key] = re;
-    sh.kim[key] = im;
-    sh.kseen[key] = seen;
+    sh.kre[t] = re;
+    sh.kim[t] = im;
+    // canonicalize drop (|c| < 1e-12) and check_hermitian_coefficients
+    // (pauli.hpp:195-214), decided per string in parallel
+    sh.kflag[t] = hypot(re, im) < 1e-12 ? 0 : (fabs(im) >= 1e-10 ? 2 : 1);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    // drop |c| < 1e-12, canonical sort, Hermiticity check (pauli.hpp:195-214)
-    int* keys = sh.keys;
-    int nk = 0;
-    for (int key = 0; key < 256; ++key)
-      if (sh.kseen[key] && hypot(sh.kre[key], sh.kim[key]) >= 1e-12) keys[nk++] = key;
-    for (int a = 1; a < nk; ++a) {
-      const int kk = keys[a];
-      const uint32_t ok = key_order(kk);
-      int b = a;
-      while (b > 0 && key_order(keys[b - 1]) > ok) {
-        keys[b] = keys[b - 1];
-        --b;
-      }
-      keys[b] = kk;
-    }
-    sh.n_terms = 0;
-    for (int a = 0; a < nk; ++a) {
-      const int key = keys[a];
-      if (fabs(sh.kim[key]) >= 1e-10) {
+    // compaction in canonical order (the table order); the first
+    // non-Hermitian survivor raises, as the reference's check loop does
+    int nt = 0;
+    for (int t = 0; t < jw.n_keys; ++t) {
+      if (sh.kflag[t] == 0) continue;
+      if (sh.kflag[t] == 2) {
         sh.stop = kStatusHermitian;
-        p.err_val[prob] = sh.kim[key];
+        p.err_val[prob] = sh.kim[t];
         break;
       }
-      const int x = key & 15, z = key >> 4;
-      // MSB-first masks: qubit q -> bit (3 - q)
-      uint64_t flip = 0, yz = 0;
+      const int key = jw.keys[t], x = key & 15, z = key >> 4;
+      uint64_t flip = 0, yz = 0;  // MSB-first: qubit q -> bit (3 - q)
       for (int q = 0; q < 4; ++q) {
         if ((x >> q) & 1) flip |= uint64_t{1} << (3 - q);
         if ((z >> q) & 1) yz |= uint64_t{1} << (3 - q);
       }
-      const int n_y = __popc(x & z);
-      const double c = sh.kre[key];  // imaginary part discarded (chem.hpp:465)
-      MaskTerm t{flip, yz, 0.0, 0.0};
-      switch (n_y & 3) {
-        case 0: t.cb_re = c; break;
-        case 1: t.cb_im = -c; break;
-        case 2: t.cb_re = -c; break;
-        default: t.cb_im = c; break;
+      const double c = sh.kre[t];  // imaginary part discarded (chem.hpp:465)
+      MaskTerm mt{flip, yz, 0.0, 0.0};
+      switch (__popc(x & z) & 3) {  // c * (-i)^{n_y}
+        case 0: mt.cb_re = c; break;
+        case 1: mt.cb_im = -c; break;
+        case 2: mt.cb_re = -c; break;
+        default: mt.cb_im = c; break;
       }
-      sh.terms[sh.n_terms++] = t;
-      if (p.ham_keys != nullptr) {
-        p.ham_keys[prob * 16 + a] = key;
-        p.ham_coeffs[prob * 16 + a] = c;
+      if (p.ham_keys != nullptr && nt < 16) {
+        p.ham_keys[prob * 16 + nt] = key;
+        p.ham_coeffs[prob * 16 + nt] = c;
       }
+      sh.terms[nt++] = mt;
     }
-    if (p.ham_count != nullptr) p.ham_count[prob] = sh.stop ? 0 : sh.n_terms;
+    sh.n_terms = nt;
+#ifdef VQF_STAGE_CLOCKS
+    t_jw = clock64();
+    if (prob == 0)
+      printf("PROLOGUE pair=%lld prims=%lld sums=%lld scf=%lld mo=%lld jw=%lld total=%lld (scf iters %d)\n",
+             t_pf - t_start, t_prim - t_pf, t_sum - t_prim, t_scf - t_sum, t_mo - t_scf, t_jw - t_mo,
+             t_jw - t_start, sh.hf.scf_iterations);
+#endif
+    if (p.ham_count != nullptr) p.ham_count[prob] = sh.stop ? 0 : nt;
     if (p.hf_out != nullptr) {
       p.hf_out[4 * prob + 0] = sh.hf.hf_energy;
       p.hf_out[4 * prob + 1] = sh.hf.e_elec;
@@ -272,158 +386,416 @@ __device__ void build_h2_device(Shared& sh, const chem::ChemConsts& k, double bo
   __syncthreads();
 }
 
+// Common kernel prologue: bias tables to smem, the problem's Hamiltonian as
+// mask terms (built on device in PES mode), then the lane tables.  Returns
+// false for threads that take no part in the optimisation (warps 1..3 of a
+// PES CTA, or a problem that already failed).
 template <bool PES>
-__global__ void __launch_bounds__(PES ? 256 : 1024) k_vqe_small(SmallParams p) {
+__device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int prob, double* bc, int D) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) sh.stop = 0;
+  for (int t = threadIdx.x; t < p.max_iterations; t += blockDim.x) {
+    bc[2 * t] = p.bc1[t];
+    bc[2 * t + 1] = p.bc2[t];
+  }
+  __syncthreads();
+  if (PES) {
+    if (p.status[prob] != 0) return false;  // rejected on the host (bond out of range)
+    build_h2_device(sh, p, prob);
+    if (sh.stop) {
+      if (threadIdx.x == 0) p.status[prob] = sh.stop;
+      return false;
+    }
+    if (threadIdx.x >= 32) return false;  // warp 0 runs the optimisation
+  } else {
+    const uint32_t t0 = p.term_off[prob], t1 = p.term_off[prob + 1];
+    for (uint32_t t = t0 + lane; t < t1; t += 32) sh.terms[t - t0] = p.terms[t];
+    if (lane == 0) sh.n_terms = static_cast<int>(t1 - t0);
+    __syncwarp();
+  }
+  build_tables(sh, D, lane);
+  return true;
+}
+
+// H2 fast path (n = 4, one parameter, 3 circuits): lanes 8c..8c+7 hold
+// circuit c with amplitude indices {sl, 8 + sl} (sl = lane & 7).  Every lane
+// carries theta / m / v and runs Adam itself (identical values in all lanes,
+// no broadcast), and computes the (cos, sin) of its own circuit's angle.
+// Exchanges per iteration: one DoubleExcitation shuffle, one shuffle per flip
+// group, a 3-level reduction and 3 energy shuffles.
+template <bool PES>
+__global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+  double* bc = reinterpret_cast<double*>(smem_raw + sizeof(Shared));
+  const int prob = blockIdx.x;
+  if (!prologue<PES>(sh, p, prob, bc, 16)) return;
+  const int lane = threadIdx.x & 31, seg = lane >> 3, sl = lane & 7;
+  const int circ = seg < 3 ? seg : 0;
+  const int G = sh.n_groups;
+  // this lane's Hamiltonian table entries, in registers for G <= 4
+  constexpr int kRegG = 4;
+  int fl_r[kRegG], fs_r[kRegG];
+  double2 o0_r[kRegG], o1_r[kRegG];
+#pragma unroll
+  for (int g = 0; g < kRegG; ++g) {
+    const bool on = g < G;
+    const int f = on ? sh.flip[g] : 0;
+    fl_r[g] = f & 7;
+    fs_r[g] = f & 8;
+    o0_r[g] = on ? sh.tab[g * 16 + sl] : make_double2(0.0, 0.0);
+    o1_r[g] = on ? sh.tab[g * 16 + 8 + sl] : make_double2(0.0, 0.0);
+  }
+  double* traj = p.traj + (size_t)prob * p.traj_stride;
+  double th = p.init_theta ? p.init_theta[prob] : 0.0, m = 0.0, v = 0.0;
+  int iters = 0, converged = 0;
+#ifdef VQF_STAGE_CLOCKS
+  long long stamps[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define STAMP(i) if (iter == 100) stamps[i] = clock64();
+#else
+#define STAMP(i)
+#endif
+  for (int iter = 0; iter <= p.max_iterations; ++iter) {
+    const bool final_eval = (iter == p.max_iterations);
+    STAMP(0)
+    // gradient(): shifted[k] = theta[k] +- pi/2 (vqe.hpp:119-121)
+    double t = th;
+    if (circ == 1) t = th + kShift;
+    if (circ == 2) t = th - kShift;
+    double sn, cs;
+    sincos(0.5 * t, &sn, &cs);
+    STAMP(1)
+    // basis_state(4, {1,1,0,0}): index 12 = slot 1 of sl 4
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(sl == 4 ? 1.0 : 0.0, 0.0);
+    // DoubleExcitation(0,1,2,3): partner of index i is i ^ 15
+    const double2 q0 = shfl_xor2(a1, 7, 8), q1 = shfl_xor2(a0, 7, 8);
+    if (sl == 4) a1 = rot_lo(cs, sn, a1, q1);  // index 12 (|1100>)
+    if (sl == 3) a0 = rot_hi(cs, sn, q0, a0);  // index 3  (|0011>)
+    STAMP(2)
+    // expectation: sum_g O_g(i) conj(psi_i) psi_{i ^ f_g}, group terms
+    // formed independently, then added in group order
+    double2 acc = make_double2(0.0, 0.0);
+    if (G <= kRegG) {
+      double2 term[kRegG];
+#pragma unroll
+      for (int g = 0; g < kRegG; ++g) {
+        double2 r0 = fs_r[g] ? a1 : a0, r1 = fs_r[g] ? a0 : a1;
+        if (fl_r[g]) {  // warp-uniform
+          r0 = shfl_xor2(r0, fl_r[g], 8);
+          r1 = shfl_xor2(r1, fl_r[g], 8);
+        }
+        const double v0r = a0.x * r0.x + a0.y * r0.y, v0i = a0.x * r0.y - a0.y * r0.x;
+        const double v1r = a1.x * r1.x + a1.y * r1.y, v1i = a1.x * r1.y - a1.y * r1.x;
+        term[g].x = (o0_r[g].x * v0r - o0_r[g].y * v0i) + (o1_r[g].x * v1r - o1_r[g].y * v1i);
+        term[g].y = (o0_r[g].x * v0i + o0_r[g].y * v0r) + (o1_r[g].x * v1i + o1_r[g].y * v1r);
+      }
+#pragma unroll
+      for (int g = 0; g < kRegG; ++g) {
+        acc.x += term[g].x;
+        acc.y += term[g].y;
+      }
+    } else {
+      for (int g = 0; g < G; ++g) {
+        const int f = sh.flip[g], fl = f & 7;
+        double2 r0 = (f & 8) ? a1 : a0, r1 = (f & 8) ? a0 : a1;
+        if (fl) {
+          r0 = shfl_xor2(r0, fl, 8);
+          r1 = shfl_xor2(r1, fl, 8);
+        }
+        const double2 o0 = sh.tab[g * 16 + sl], o1 = sh.tab[g * 16 + 8 + sl];
+        const double v0r = a0.x * r0.x + a0.y * r0.y, v0i = a0.x * r0.y - a0.y * r0.x;
+        const double v1r = a1.x * r1.x + a1.y * r1.y, v1i = a1.x * r1.y - a1.y * r1.x;
+        acc.x += (o0.x * v0r - o0.y * v0i) + (o1.x * v1r - o1.y * v1i);
+        acc.y += (o0.x * v0i + o0.y * v0r) + (o1.x * v1i + o1.y * v1r);
+      }
+    }
+    STAMP(3)
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, 8);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, 8);
+    }
+    const double2 e0 = shfl2(acc, 0), ep = shfl2(acc, 8), em = shfl2(acc, 16);
+    STAMP(4)
+    // checked_energy, then the gradient's two expectations (vqe.hpp:227-229);
+    // one predicate on the common path, the exact failure decoded after
+    const bool bad = fabs(e0.y) >= 1e-10 || !isfinite(e0.x) ||
+                     (!final_eval && (fabs(ep.y) >= 1e-10 || fabs(em.y) >= 1e-10));
+    if (bad) {
+      if (lane == 0) {
+        int st;
+        double val = 0.0;
+        if (fabs(e0.y) >= 1e-10) {
+          st = kStatusImag;
+          val = e0.y;
+        } else if (!isfinite(e0.x)) {
+          st = kStatusNonFinite;
+        } else {
+          st = kStatusImag;
+          val = fabs(ep.y) >= 1e-10 ? ep.y : em.y;
+        }
+        p.status[prob] = st;
+        p.err_val[prob] = val;
+        p.err_iter[prob] = iter;
+        p.err_theta[prob] = th;
+      }
+      return;
+    }
+    traj[iter] = e0.x;  // every lane stores the same value (one transaction)
+    if (final_eval) break;
+    const double g = 0.5 * (ep.x - em.x);
+    if (p.has_tol && fabs(g) < p.tol) {
+      converged = 1;
+      break;
+    }
+    STAMP(5)
+    // adam_step (vqe.hpp:152-174), t = iter + 1; the bias corrections are
+    // applied as host-computed reciprocals 1 / (1 - beta^t)
+    const double mk = p.beta1 * m + (1.0 - p.beta1) * g;
+    const double vk = p.beta2 * v + (1.0 - p.beta2) * g * g;
+    const double m_hat = mk * bc[2 * iter];
+    const double v_hat = vk * bc[2 * iter + 1];
+    th = th - p.lr * m_hat / (sqrt(v_hat) + p.eps);
+    m = mk;
+    v = vk;
+    iters = iter + 1;
+    STAMP(6)
+  }
+#ifdef VQF_STAGE_CLOCKS
+  if (prob == 0 && lane == 0)
+    printf("STAGES angle=%lld de=%lld groups=%lld reduce+bcast=%lld checks+grad=%lld adam=%lld total=%lld\n",
+           stamps[1] - stamps[0], stamps[2] - stamps[1], stamps[3] - stamps[2], stamps[4] - stamps[3],
+           stamps[5] - stamps[4], stamps[6] - stamps[5], stamps[6] - stamps[0]);
+#endif
+  if (lane == 0) {
+    p.iters[prob] = iters;
+    p.converged[prob] = converged;
+    p.energy[prob] = traj[converged ? iters : p.max_iterations];
+    p.theta_out[prob] = th;
+  }
+  const int len = converged ? iters + 1 : p.max_iterations + 1;
+  for (int k = len + lane; k < p.traj_stride; k += 32) traj[k] = __longlong_as_double(-1LL);
+}
+
+template <int A, bool PES, bool H2>
+__global__ void __launch_bounds__(PES ? kPesThreads : 32) k_vqe_warp(SmallParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
   const int prob = blockIdx.x;
   const int n = p.n_qubits, D = 1 << n, P = p.n_params, NC = 2 * P + 1;
-  const int slot = threadIdx.x / D, lane = threadIdx.x % D, slots = blockDim.x / D;
+  const int L = D / A;
+  const int lgL = __ffs(L) - 1;
+  const int lane = threadIdx.x & 31;
+  double* bc = reinterpret_cast<double*>(smem_raw + sizeof(Shared));  // [2][T]
 
-  if (threadIdx.x == 0) {
-    sh.stop = 0;
-    sh.converged = 0;
-    sh.iters = 0;
+  if (!prologue<PES>(sh, p, prob, bc, D)) return;
+  int basis = 12;
+  if (!H2) {
+    if (lane == 0) basis = build_program(sh, p.ansatz_kind, n, p.layers);
+    basis = __shfl_sync(0xffffffffu, basis, 0);
   }
-  __syncthreads();
-  if (PES) {
-    if (p.status[prob] != 0) return;  // rejected on the host (bond out of range)
-    build_h2_device(sh, p.chem, p.bonds[prob], p, prob);
-    if (sh.stop) {
-      if (threadIdx.x == 0) p.status[prob] = sh.stop;
+  // lane k owns parameter k (and k + 32): theta, m, v in registers
+  double th_reg[2], m_reg[2] = {0.0, 0.0}, v_reg[2] = {0.0, 0.0};
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int k = lane + 32 * r;
+    th_reg[r] = (k < P && p.init_theta) ? p.init_theta[(size_t)prob * P + k] : 0.0;
+    if (k < P) sh.theta[k] = th_reg[r];
+  }
+  __syncwarp();
+
+  double* traj = p.traj + (size_t)prob * p.traj_stride;
+  const int seg = lane / L, segs = 32 / L, sl = lane % L;
+  int iters = 0, converged = 0, status = 0;
+  double err_val = 0.0;
+
+  for (int iter = 0; iter <= p.max_iterations; ++iter) {
+    const bool final_eval = (iter == p.max_iterations);  // vqe.hpp:244-247
+    // (1) angles: (cos, sin)(0.5 * (theta_k + {0, +pi/2, -pi/2}))
+    for (int idx = lane; idx < 3 * P; idx += 32) {
+      const int k = idx / 3, j = idx - 3 * k;
+      double t = sh.theta[k];
+      if (j == 1) t = t + kShift;
+      if (j == 2) t = t - kShift;
+      double s, c;
+      sincos(0.5 * t, &s, &c);
+      sh.cs[k][j] = make_double2(c, s);
+    }
+    __syncwarp();
+    // (2) circuits, segs at a time; energies exchanged by shuffles when one
+    //     round covers every circuit (the common case), else via smem
+    const int nc = final_eval ? 1 : NC;
+    double2 e_own = make_double2(0.0, 0.0);
+    for (int c0 = 0; c0 < nc; c0 += segs) {
+      const int c = c0 + seg;
+      double2 amp[A];
+      run_circuit<A, H2>(sh, amp, c < nc ? c : 0, sl, L, lgL, basis);
+      const double2 e = circuit_energy<A>(sh, amp, sl, L, lgL, D);
+      if (nc <= segs) e_own = e;
+      else if (sl == 0 && c < nc) sh.energy[c] = e;
+    }
+    if (nc > segs) __syncwarp();
+    auto energy_of = [&](int c) -> double2 {  // warp-uniform c
+      return nc <= segs ? shfl2(e_own, c * L) : sh.energy[c];
+    };
+    // (3) checked_energy + gradient checks in the reference's order
+    //     (vqe.hpp:227-238), evaluated redundantly by every lane
+    {
+      const double2 e0 = energy_of(0);
+      if (fabs(e0.y) >= 1e-10) {
+        status = kStatusImag;
+        err_val = e0.y;
+      } else if (!isfinite(e0.x)) {
+        status = kStatusNonFinite;
+      } else {
+        for (int c = 1; c < nc; ++c) {
+          const double im = energy_of(c).y;
+          if (!status && fabs(im) >= 1e-10) {
+            status = kStatusImag;
+            err_val = im;
+          }
+        }
+      }
+      if (status) {
+        if (lane == 0) {
+          p.status[prob] = status;
+          p.err_val[prob] = err_val;
+          p.err_iter[prob] = iter;
+          for (int k = 0; k < P; ++k) p.err_theta[(size_t)prob * P + k] = sh.theta[k];
+        }
+        break;
+      }
+      if (lane == 0) traj[iter] = e0.x;
+    }
+    if (final_eval) break;
+    // gradient (vqe.hpp:118-124) in the lane that owns the parameter
+    double g_reg[2] = {0.0, 0.0};
+    double g_inf = 0.0;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (32 * r >= P) break;
+      const int k = lane + 32 * r;
+      double ep, em;
+      if (nc <= segs) {
+        const int kk = k < P ? k : 0;
+        ep = __shfl_sync(0xffffffffu, e_own.x, ((2 * kk + 1) * L) & 31);
+        em = __shfl_sync(0xffffffffu, e_own.x, ((2 * kk + 2) * L) & 31);
+      } else {
+        ep = k < P ? sh.energy[2 * k + 1].x : 0.0;
+        em = k < P ? sh.energy[2 * k + 2].x : 0.0;
+      }
+      g_reg[r] = 0.5 * (ep - em);
+      if (k < P) g_inf = fmax(g_inf, fabs(g_reg[r]));
+    }
+    for (int o = 1; o < P && o < 32; o <<= 1) g_inf = fmax(g_inf, __shfl_xor_sync(0xffffffffu, g_inf, o));
+    g_inf = __shfl_sync(0xffffffffu, g_inf, 0);  // warp-uniform stop decision
+    if (p.has_tol && g_inf < p.tol) {
+      converged = 1;
+      break;
+    }
+    // (4) adam_step (vqe.hpp:152-174), t = iter + 1, in the owning lane
+    const double b1 = bc[2 * iter], b2 = bc[2 * iter + 1];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int k = lane + 32 * r;
+      if (k < P) {
+        const double g = g_reg[r];
+        const double mk = p.beta1 * m_reg[r] + (1.0 - p.beta1) * g;
+        const double vk = p.beta2 * v_reg[r] + (1.0 - p.beta2) * g * g;
+        const double m_hat = mk * b1;  // b1, b2 = 1 / (1 - beta^t)
+        const double v_hat = vk * b2;
+        th_reg[r] = th_reg[r] - p.lr * m_hat / (sqrt(v_hat) + p.eps);
+        m_reg[r] = mk;
+        v_reg[r] = vk;
+        sh.theta[k] = th_reg[r];
+      }
+    }
+    iters = iter + 1;
+    __syncwarp();
+  }
+  if (status) return;
+  if (lane == 0) {
+    p.iters[prob] = iters;
+    p.converged[prob] = converged;
+    p.energy[prob] = traj[converged ? iters : p.max_iterations];
+  }
+  for (int k = lane; k < P; k += 32) p.theta_out[(size_t)prob * P + k] = sh.theta[k];
+  // NaN-pad the unused tail of a converged run's trajectory row
+  const int len = converged ? iters + 1 : p.max_iterations + 1;
+  for (int t = len + lane; t < p.traj_stride; t += 32) traj[t] = __longlong_as_double(-1LL);
+}
+
+size_t smem_for(const SmallParams& p) {
+  const size_t smem = sizeof(Shared) + 2 * sizeof(double) * (size_t)std::max(p.max_iterations, 1);
+  if (smem > 227 * 1024) throw_invalid("small engine: max_iterations too large for the on-chip bias tables");
+  return smem;
+}
+
+// Raises a kernel's dynamic shared memory limit once per process (the
+// attribute is per function, and the driver call costs microseconds on the
+// launch path otherwise).
+void opt_in_smem(void (*kernel)(SmallParams)) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, const void*>> done;  // (device, kernel)
+  int dev = 0;
+  VQF_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first == dev && d.second == reinterpret_cast<const void*>(kernel)) return;
+  VQF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  done.emplace_back(dev, reinterpret_cast<const void*>(kernel));
+}
+
+template <int A, bool PES, bool H2>
+void launch_k(const SmallParams& p, uint32_t batch, cudaStream_t stream) {
+  const size_t smem = smem_for(p);
+  opt_in_smem(k_vqe_warp<A, PES, H2>);
+  k_vqe_warp<A, PES, H2><<<batch, PES ? kPesThreads : 32, smem, stream>>>(p);
+}
+
+template <bool PES>
+void launch_h2(const SmallParams& p, uint32_t batch, cudaStream_t stream) {
+  const size_t smem = smem_for(p);
+  opt_in_smem(k_h2<PES>);
+  k_h2<PES><<<batch, PES ? kPesThreads : 32, smem, stream>>>(p);
+}
+
+template <int A>
+void launch_a(const SmallParams& p, uint32_t batch, bool pes, cudaStream_t stream) {
+  if constexpr (A == 2) {  // the H2 ansatz always lands here (D = 16, NC = 3)
+    if (p.ansatz_kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION) {
+      if (pes) launch_h2<true>(p, batch, stream);
+      else launch_h2<false>(p, batch, stream);
       return;
     }
-  } else {
-    const uint32_t t0 = p.term_off[prob], t1 = p.term_off[prob + 1];
-    for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) sh.terms[t - t0] = p.terms[t];
-    if (threadIdx.x == 0) sh.n_terms = static_cast<int>(t1 - t0);
-    __syncthreads();
   }
-  build_tables(sh, n);
-  for (int k = threadIdx.x; k < P; k += blockDim.x) {
-    sh.theta[k] = p.init_theta ? p.init_theta[(size_t)prob * P + k] : 0.0;
-    sh.m[k] = 0.0;
-    sh.v[k] = 0.0;
-  }
-  __syncthreads();
-  double* traj = p.traj + (size_t)prob * p.traj_stride;
-
-  // Warps whose first circuit slot is past the last circuit skip the round
-  // (warp-uniform, so the shuffles of active warps stay convergent).
-  const int warp_first_slot = (threadIdx.x & ~31) / D;
-  for (int iter = 0; iter < p.max_iterations; ++iter) {
-    for (int c0 = 0; c0 < NC; c0 += slots) {
-      if (c0 + warp_first_slot >= NC) continue;
-      const int c = c0 + slot;
-      const double2 amp = run_ansatz(p.ansatz_kind, n, p.layers, sh.theta, c < NC ? c : 0, lane);
-      const double2 e = lane_energy(sh, amp, lane, D);
-      if (lane == 0 && c < NC) sh.energy[c] = e;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      // checked_energy + gradient, in the reference's order (vqe.hpp:227-238)
-      const double2 e = sh.energy[0];
-      int st = 0;
-      double val = 0.0;
-      if (fabs(e.y) >= 1e-10) {
-        st = kStatusImag;
-        val = e.y;
-      } else if (!isfinite(e.x)) {
-        st = kStatusNonFinite;
-      } else {
-        for (int c = 1; c < NC && !st; ++c)
-          if (fabs(sh.energy[c].y) >= 1e-10) {
-            st = kStatusImag;
-            val = sh.energy[c].y;
-          }
-      }
-      if (st) {
-        sh.stop = st;
-        p.status[prob] = st;
-        p.err_val[prob] = val;
-        p.err_iter[prob] = iter;
-        for (int k = 0; k < P; ++k) p.err_theta[(size_t)prob * P + k] = sh.theta[k];
-      } else {
-        traj[iter] = e.x;
-        double g_inf = 0.0;
-        for (int k = 0; k < P; ++k) {
-          sh.grad[k] = 0.5 * (sh.energy[2 * k + 1].x - sh.energy[2 * k + 2].x);
-          g_inf = fmax(g_inf, fabs(sh.grad[k]));
-        }
-        if (p.has_tol && g_inf < p.tol) {
-          sh.stop = 1;
-          sh.converged = 1;
-        }
-      }
-    }
-    __syncthreads();
-    if (sh.stop) break;
-    // adam_step (vqe.hpp:152-174) with t = iter + 1
-    for (int k = threadIdx.x; k < P; k += blockDim.x) {
-      const double g = sh.grad[k];
-      const double mk = p.beta1 * sh.m[k] + (1.0 - p.beta1) * g;
-      const double vk = p.beta2 * sh.v[k] + (1.0 - p.beta2) * g * g;
-      const double m_hat = mk / p.bc1[iter];
-      const double v_hat = vk / p.bc2[iter];
-      sh.theta[k] = sh.theta[k] - p.lr * m_hat / (sqrt(v_hat) + p.eps);
-      sh.m[k] = mk;
-      sh.v[k] = vk;
-    }
-    if (threadIdx.x == 0) sh.iters = iter + 1;
-    __syncthreads();
-  }
-
-  if (sh.stop > 1) return;  // error recorded
-  if (!sh.converged) {
-    // final checked_energy (vqe.hpp:244-247)
-    if (threadIdx.x < 32) {  // warp 0; every slot in it runs circuit 0
-      const double2 amp = run_ansatz(p.ansatz_kind, n, p.layers, sh.theta, 0, lane);
-      const double2 e = lane_energy(sh, amp, lane, D);
-      if (threadIdx.x == 0) sh.energy[0] = e;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double2 e = sh.energy[0];
-      if (fabs(e.y) >= 1e-10) {
-        p.status[prob] = kStatusImag;
-        p.err_val[prob] = e.y;
-        p.err_iter[prob] = p.max_iterations;
-      } else if (!isfinite(e.x)) {
-        p.status[prob] = kStatusNonFinite;
-        p.err_iter[prob] = p.max_iterations;
-        for (int k = 0; k < P; ++k) p.err_theta[(size_t)prob * P + k] = sh.theta[k];
-      } else {
-        traj[p.max_iterations] = e.x;
-      }
-    }
-  }
-  if (threadIdx.x == 0 && p.status[prob] == 0) {
-    p.iters[prob] = sh.iters;
-    p.converged[prob] = sh.converged;
-    p.energy[prob] = traj[sh.converged ? sh.iters : p.max_iterations];
-  }
-  for (int k = threadIdx.x; k < P; k += blockDim.x) p.theta_out[(size_t)prob * P + k] = sh.theta[k];
-  // NaN-pad the unused tail of a converged run's trajectory row
-  const int len = sh.converged ? sh.iters + 1 : p.max_iterations + 1;
-  for (int t = len + threadIdx.x; t < p.traj_stride; t += blockDim.x) traj[t] = __longlong_as_double(-1LL);
+  if (pes) launch_k<A, true, false>(p, batch, stream);
+  else launch_k<A, false, false>(p, batch, stream);
 }
 
 }  // namespace
 
 size_t small_smem_bytes() { return sizeof(Shared); }
 
+// Lanes per circuit L: the largest power of two with NC * L <= 32 and
+// L <= D (one circuit round per iteration when it fits); amplitudes per
+// lane A = D / L.
+int small_amps_per_lane(int n_qubits, int n_params) {
+  const int D = 1 << n_qubits, NC = 2 * n_params + 1;
+  int L = 1;
+  while (L * 2 <= D && NC * L * 2 <= 32) L *= 2;
+  return D / L;
+}
+
 void launch_vqe_small(const SmallParams& p, uint32_t batch, bool pes, cudaStream_t stream) {
-  const int D = 1 << p.n_qubits, NC = 2 * p.n_params + 1;
-  int threads = ((NC * D + 31) / 32) * 32;
-  if (threads > 1024) threads = 1024;
-  if (pes) threads = 256;  // chemistry prologue uses 256; H2 needs 3 x 16 lanes
-  const size_t smem = sizeof(Shared);
-  if (pes) {
-    VQF_CUDA(cudaFuncSetAttribute(k_vqe_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_vqe_small<true><<<batch, threads, smem, stream>>>(p);
-  } else {
-    VQF_CUDA(cudaFuncSetAttribute(k_vqe_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_vqe_small<false><<<batch, threads, smem, stream>>>(p);
+  switch (small_amps_per_lane(p.n_qubits, p.n_params)) {
+    case 1: launch_a<1>(p, batch, pes, stream); break;
+    case 2: launch_a<2>(p, batch, pes, stream); break;
+    case 4: launch_a<4>(p, batch, pes, stream); break;
+    case 8: launch_a<8>(p, batch, pes, stream); break;
+    case 16: launch_a<16>(p, batch, pes, stream); break;
+    case 32: launch_a<32>(p, batch, pes, stream); break;
+    default: throw Error(VQF_LOGIC_ERROR, "small engine: unsupported register size");
   }
   VQF_LAUNCHED();
   VQF_CUDA(cudaGetLastError());

@@ -35,6 +35,7 @@ struct SmallParams {
   // PES mode
   const double* bonds;
   chem::ChemConsts chem;
+  const chem::JwTable* jw;
   const double* init_theta;  // batch * P, or null (theta0 = 0)
   // outputs
   double* energy;
@@ -55,6 +56,7 @@ struct SmallParams {
 };
 
 size_t small_smem_bytes();
+int small_amps_per_lane(int n_qubits, int n_params);
 void launch_vqe_small(const SmallParams& p, uint32_t batch, bool pes, cudaStream_t stream);
 
 }  // namespace vqf

@@ -1,0 +1,42 @@
+"""Small, deterministic workloads for ncu captures (run under gpurun).
+
+  python scripts/prof_targets.py pes        # fused PES kernel, 3 launches
+  python scripts/prof_targets.py gates N    # RY / CNOT / DE on an N-qubit fp64 state
+  python scripts/prof_targets.py expect N   # TFIM expectation (diag + N flip groups)
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2601_09951_b200 import vqeforge as V  # noqa: E402
+
+
+def main():
+    what = sys.argv[1]
+    V.init(0)
+    if what == "pes":
+        plan = V.PesPlan(V.SweepConfig())
+        for _ in range(3):
+            plan.launch()
+        rep = plan.read()
+        assert rep.all_ok
+    elif what == "gates":
+        n = int(sys.argv[2])
+        psi = V.StateVector(n)
+        V.apply_circuit(psi, [V.Gate.ry(0.3, q) for q in (0, 1, n // 2, n - 2, n - 1)])
+        V.apply_circuit(psi, [V.Gate.cnot(0, 1), V.Gate.cnot(n - 2, n - 1), V.Gate.double_excitation(0.4, 0, 1, 2, 3)])
+    elif what == "expect":
+        n = int(sys.argv[2])
+        psi = V.StateVector(n)
+        V.apply_circuit(psi, [V.Gate.ry(0.3, q) for q in range(n)])
+        print(V.expectation(psi, V.build_tfim(n, 1.0, 1.0)))
+    else:
+        raise SystemExit(f"unknown target {what}")
+
+
+if __name__ == "__main__":
+    main()
