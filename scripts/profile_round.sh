@@ -1,0 +1,16 @@
+#!/bin/bash
+# ncu evidence for profiles/ (run under gpurun, one GPU):
+#   1. launch list of the bench command (per-launch device time)
+#   2. --set full captures of the top kernels
+set -x
+OUT=gpurun_out
+mkdir -p $OUT
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_bench.csv \
+    python bench.py --steps 3 --warmup 1 --no-cpu-baseline > $OUT/bench_under_ncu.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_gate1 -s 3 -c 2 -o $OUT/full_ry30 \
+    python scripts/prof_targets.py gates 30 > $OUT/full_ry30.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_h2 -c 1 -o $OUT/full_pes \
+    python scripts/prof_targets.py pes > $OUT/full_pes.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_expect -c 3 -o $OUT/full_expect28 \
+    python scripts/prof_targets.py expect 28 > $OUT/full_expect28.log 2>&1
+ls -la $OUT
