@@ -207,6 +207,7 @@ def gate_roofline(V, torch, device, n, steps, warmup):
 def run_ours(args, rank, world, local_rank):
     import torch
 
+    from paper_2601_09951_b200 import dist as D
     from paper_2601_09951_b200 import vqeforge as V
 
     dist = None
@@ -224,11 +225,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(local_rank)
 
     def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return D.max_over_ranks(x, dist, f"cuda:{local_rank}")
 
     clocks = ClockSampler(local_rank)
     cfg = V.SweepConfig(chunk_index=rank, n_chunks=world)
@@ -276,11 +273,8 @@ def run_ours(args, rank, world, local_rank):
     # ---- gather results, check parity against the reference's fixture
     pts = [(p.bond_angstrom, p.energy_hartree, p.iterations, p.ok) for p in rep.points]
     e2e_pts = [(p.bond_angstrom, p.energy_hartree, p.iterations, p.ok) for p in e2e_rep.points]
-    if dist is not None:
-        allp = [None] * world
-        dist.all_gather_object(allp, (pts, e2e_pts))
-        pts = [x for r in allp for x in r[0]]
-        e2e_pts = [x for r in allp for x in r[1]]
+    pts = D.gather_points(pts, dist)
+    e2e_pts = D.gather_points(e2e_pts, dist)
     if rank != 0:
         return
     with open(os.path.join(ROOT, "tests", "golden", "pes_default.json")) as f:
