@@ -21,6 +21,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;
+constexpr int kExpU = 8;  // loads in flight per thread in the expectation passes
 constexpr int kRedBlocks = 4 * 148;  // reduction grid: 4 CTAs per SM (148 SMs)
 
 template <typename T>
@@ -243,6 +244,80 @@ __global__ void __launch_bounds__(kThreads) k_expect_diag(const typename V2<T>::
   }
 }
 
+// Diagonal group, tiled: the index splits as i = (hi << B) | lo over tiles of
+// 2^B contiguous amplitudes, and every Z-string sign factorises as
+// (-1)^popc(i & yz) = (-1)^popc(lo & yz_lo) * (-1)^popc(hi & yz_hi).
+//   * terms with yz_hi = 0 fold into a per-CTA table L[lo] (built once);
+//   * terms with yz_lo = 0 fold into one scalar per tile;
+//   * mixed terms stay a per-amplitude loop.
+// Per amplitude: one L lookup (shared memory), two adds, |psi|^2 * D, with
+// kExpU loads in flight per thread — the pass is HBM-bound instead of
+// looping over every Z term per amplitude.
+// grid = (blocks, batch); dynamic smem = 2^B double2.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_expect_diag_tiled(
+    const typename V2<T>::type* __restrict__ a, uint32_t n, uint32_t B, const MaskTerm* __restrict__ lo_t,
+    uint32_t n_lo, const MaskTerm* __restrict__ hi_t, uint32_t n_hi, const MaskTerm* __restrict__ mx_t,
+    uint32_t n_mx, double* __restrict__ partials, uint32_t G) {
+  extern __shared__ double2 Ltab[];
+  __shared__ MaskTerm mx[64];
+  const uint32_t b = blockIdx.y;
+  const uint32_t tile_amps = 1u << B;
+  const uint64_t n_tiles = uint64_t{1} << (n - B);
+  const typename V2<T>::type* s = a + ((uint64_t)b << n);
+  for (uint32_t lo = threadIdx.x; lo < tile_amps; lo += kThreads) {
+    double re = 0.0, im = 0.0;
+    for (uint32_t t = 0; t < n_lo; ++t) {
+      const double sg = parity_sign(lo & lo_t[t].yz);
+      re += sg * lo_t[t].cb_re;
+      im += sg * lo_t[t].cb_im;
+    }
+    Ltab[lo] = make_double2(re, im);
+  }
+  if (threadIdx.x < n_mx) mx[threadIdx.x] = mx_t[threadIdx.x];
+  __syncthreads();
+  double2 acc = make_double2(0.0, 0.0);
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    double hre = 0.0, him = 0.0;  // warp-uniform per tile
+    for (uint32_t t = 0; t < n_hi; ++t) {
+      const double sg = parity_sign(tile & (hi_t[t].yz >> B));
+      hre += sg * hi_t[t].cb_re;
+      him += sg * hi_t[t].cb_im;
+    }
+    const uint64_t base = tile << B;
+    for (uint32_t lo0 = threadIdx.x; lo0 < tile_amps; lo0 += kThreads * kExpU) {
+      typename V2<T>::type x[kExpU];
+#pragma unroll
+      for (int u = 0; u < kExpU; ++u) {
+        const uint32_t lo = lo0 + u * kThreads;
+        if (lo < tile_amps) x[u] = s[base | lo];
+      }
+#pragma unroll
+      for (int u = 0; u < kExpU; ++u) {
+        const uint32_t lo = lo0 + u * kThreads;
+        if (lo >= tile_amps) break;
+        const uint64_t i = base | lo;
+        const double p = (double)x[u].x * (double)x[u].x + (double)x[u].y * (double)x[u].y;
+        const double2 l = Ltab[lo];
+        double dre = l.x + hre, dim = l.y + him;
+        for (uint32_t t = 0; t < n_mx; ++t) {
+          const double sg = parity_sign(i & mx[t].yz);
+          dre += sg * mx[t].cb_re;
+          dim += sg * mx[t].cb_im;
+        }
+        acc.x += p * dre;
+        acc.y += p * dim;
+      }
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) {
+    const size_t o = ((size_t)b * G + 0) * gridDim.x + blockIdx.x;
+    partials[2 * o] = acc.x;
+    partials[2 * o + 1] = acc.y;
+  }
+}
+
 // Off-diagonal group with flip mask f (statevector.hpp:235-241): each pair
 // (i, j = i ^ f), i with f's top bit clear, is read once.  With
 // v = conj(psi_i) psi_j and sigma_t = (-1)^popc(f & yz_t), the two
@@ -267,26 +342,41 @@ __global__ void __launch_bounds__(kThreads) k_expect_flip(const typename V2<T>::
       sig[threadIdx.x] = parity_sign(flip & st[threadIdx.x].yz);
     }
     __syncthreads();
-    for (uint64_t k = (uint64_t)blockIdx.x * kThreads + threadIdx.x; k < half; k += (uint64_t)gridDim.x * kThreads) {
-      const uint64_t i = insert_zero(k, hb);
-      const typename V2<T>::type x = s[i], y = s[i ^ flip];
-      // v = conj(x) * y
-      const double vr = (double)x.x * (double)y.x + (double)x.y * (double)y.y;
-      const double vi = (double)x.x * (double)y.y - (double)x.y * (double)y.x;
-      double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
-      for (uint32_t t = 0; t < cnt; ++t) {
-        const double sg = parity_sign(i & st[t].yz);
-        if (sig[t] > 0.0) {
-          ar += sg * st[t].cb_re;
-          ai += sg * st[t].cb_im;
-        } else {
-          br += sg * st[t].cb_re;
-          bi += sg * st[t].cb_im;
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t k0 = (uint64_t)blockIdx.x * kThreads + threadIdx.x; k0 < half; k0 += stride * kExpU) {
+      typename V2<T>::type x[kExpU], y[kExpU];
+      uint64_t idx[kExpU];
+#pragma unroll
+      for (int u = 0; u < kExpU; ++u) {  // pairs in flight before arithmetic
+        const uint64_t k = k0 + u * stride;
+        idx[u] = insert_zero(k, hb);
+        if (k < half) {
+          x[u] = s[idx[u]];
+          y[u] = s[idx[u] ^ flip];
         }
       }
-      // A * (2 vr) + B * (2i vi)
-      acc.x += 2.0 * (ar * vr - bi * vi);
-      acc.y += 2.0 * (ai * vr + br * vi);
+#pragma unroll
+      for (int u = 0; u < kExpU; ++u) {
+        if (k0 + u * stride >= half) break;
+        const uint64_t i = idx[u];
+        // v = conj(x) * y
+        const double vr = (double)x[u].x * (double)y[u].x + (double)x[u].y * (double)y[u].y;
+        const double vi = (double)x[u].x * (double)y[u].y - (double)x[u].y * (double)y[u].x;
+        double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+        for (uint32_t t = 0; t < cnt; ++t) {
+          const double sg = parity_sign(i & st[t].yz);
+          if (sig[t] > 0.0) {
+            ar += sg * st[t].cb_re;
+            ai += sg * st[t].cb_im;
+          } else {
+            br += sg * st[t].cb_re;
+            bi += sg * st[t].cb_im;
+          }
+        }
+        // A * (2 vr) + B * (2i vi)
+        acc.x += 2.0 * (ar * vr - bi * vi);
+        acc.y += 2.0 * (ai * vr + br * vi);
+      }
     }
   }
   acc = block_sum(acc);
@@ -400,16 +490,37 @@ void expectation_t(vqf_statevector* sv, const CompiledHam& h, double* dev_out) {
   const uint32_t nb = std::max(nb_diag, nb_flip);
   ensure_partials(sv, 2 * (size_t)sv->batch * G * nb);
   VQF_CUDA(cudaMemsetAsync(sv->partials, 0, 2 * sizeof(double) * sv->batch * G * nb, sv->stream));
-  const size_t tbytes = std::max<size_t>(1, h.terms.size()) * sizeof(MaskTerm);
-  ensure_terms(sv, tbytes);
-  if (!h.terms.empty())
-    VQF_CUDA(cudaMemcpyAsync(sv->terms_dev, h.terms.data(), h.terms.size() * sizeof(MaskTerm),
-                             cudaMemcpyHostToDevice, sv->stream));
+  // Diagonal group split for the tiled kernel (k_expect_diag_tiled): terms
+  // whose Z/Y support is all below / all above the tile width, and mixed.
+  const uint32_t B = std::min<uint32_t>(n, 11);  // 2048-amplitude tiles, 32 KB table
+  const uint64_t lo_mask = (uint64_t{1} << B) - 1;
+  std::vector<MaskTerm> all = h.terms, lo, hi, mx;
+  for (uint32_t t = h.group_offset[0]; t < h.group_offset[1]; ++t) {
+    const MaskTerm& m = h.terms[t];
+    if ((m.yz & ~lo_mask) == 0) lo.push_back(m);
+    else if ((m.yz & lo_mask) == 0) hi.push_back(m);
+    else mx.push_back(m);
+  }
+  const bool tiled = mx.size() <= 64;
+  const uint32_t o_lo = static_cast<uint32_t>(all.size());
+  all.insert(all.end(), lo.begin(), lo.end());
+  const uint32_t o_hi = static_cast<uint32_t>(all.size());
+  all.insert(all.end(), hi.begin(), hi.end());
+  const uint32_t o_mx = static_cast<uint32_t>(all.size());
+  all.insert(all.end(), mx.begin(), mx.end());
+  ensure_terms(sv, std::max<size_t>(1, all.size()) * sizeof(MaskTerm));
+  if (!all.empty())
+    VQF_CUDA(cudaMemcpyAsync(sv->terms_dev, all.data(), all.size() * sizeof(MaskTerm), cudaMemcpyHostToDevice,
+                             sv->stream));
   const MaskTerm* td = static_cast<const MaskTerm*>(sv->terms_dev);
   for (uint32_t g = 0; g < G; ++g) {
     const uint32_t t0 = h.group_offset[g], cnt = h.group_offset[g + 1] - t0;
     if (cnt == 0) continue;
-    if (g == 0) {
+    if (g == 0 && tiled) {
+      k_expect_diag_tiled<T><<<dim3(nb, sv->batch), kThreads, sizeof(double2) << B, sv->stream>>>(
+          a, n, B, td + o_lo, static_cast<uint32_t>(lo.size()), td + o_hi, static_cast<uint32_t>(hi.size()),
+          td + o_mx, static_cast<uint32_t>(mx.size()), sv->partials, G);
+    } else if (g == 0) {
       k_expect_diag<T><<<dim3(nb, sv->batch), kThreads, 0, sv->stream>>>(a, n, td + t0, cnt, sv->partials, G, 0);
     } else {
       const uint64_t f = h.group_flip[g];
