@@ -1,0 +1,435 @@
+// Adjoint-differentiation gradient for the HBM engine (wide registers).
+//
+// The reference differentiates with the two-term parameter shift
+// (vqe.hpp:112-127): 2P extra circuits per iteration.  For the
+// hardware-efficient ansatz at 26 qubits that is 105 full circuits per
+// iteration.  The adjoint method gets the same gradient (analytically equal
+// for these single-frequency gates; numerically equal to ~1e-15) from:
+//   forward   psi = U_L ... U_1 |init>                     (existing kernels)
+//   k_apply_ham  lambda = H psi, E = <psi|lambda>          (one tiled pass)
+//   backward  for k = L..1:  psi <- U_k^dag psi;
+//             if U_k has parameter j:  g_j = 2 Re <lambda| dU_k/dtheta |psi>;
+//             lambda <- U_k^dag lambda
+// Each parameterised backward step is ONE kernel (k_adj_givens): it reads and
+// writes both vectors once (4S) and reduces the derivative inner product
+// deterministically into per-block partials.
+#include <algorithm>
+#include <cstring>
+
+#include "adjoint.cuh"
+
+namespace vqf {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kU = 4;
+constexpr int kBlocks = 4 * 148;
+constexpr uint32_t kTileBits = 11;
+constexpr int kMaxGroups = 256;
+constexpr int kMaxTerms = 1024;
+
+template <typename T>
+struct V2;
+template <>
+struct V2<double> {
+  using type = double2;
+};
+template <>
+struct V2<float> {
+  using type = float2;
+};
+
+__device__ __forceinline__ uint64_t insert_zero(uint64_t k, uint32_t bit) {
+  const uint64_t low = k & ((uint64_t{1} << bit) - 1);
+  return ((k >> bit) << (bit + 1)) | low;
+}
+
+__device__ __forceinline__ double parity_sign(uint64_t x) { return (__popcll(x) & 1) ? -1.0 : 1.0; }
+
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+__device__ __forceinline__ double2 block_sum(double2 v) {
+  __shared__ double2 sh[kThreads / 32];
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < kThreads / 32 ? sh[l] : make_double2(0.0, 0.0);
+    v = warp_sum(v);
+  }
+  __syncthreads();
+  return v;
+}
+
+// lambda = H psi and <psi|lambda>, one pass over 2^B-amplitude tiles.
+// Per amplitude i: lambda_i = D(i) psi_i + sum_g O_g(i) psi_{i ^ f_g}, with
+// D from the tiled diagonal split and O_g(i) = sum_t cb_t (-1)^popc(i & yz_t).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_apply_ham(const typename V2<T>::type* __restrict__ psi,
+                                                        typename V2<T>::type* __restrict__ lam, uint32_t n,
+                                                        uint32_t B, HamDevC h, double* __restrict__ partials) {
+  using A = typename V2<T>::type;
+  extern __shared__ double2 Ltab[];
+  __shared__ MaskTerm mx[64];
+  const uint32_t tile_amps = 1u << B;
+  const uint64_t n_tiles = uint64_t{1} << (n - B);
+  for (uint32_t lo = threadIdx.x; lo < tile_amps; lo += kThreads) {
+    double re = 0.0, im = 0.0;
+    for (uint32_t t = 0; t < h.n_lo; ++t) {
+      const double sg = parity_sign(lo & h.lo_t[t].yz);
+      re += sg * h.lo_t[t].cb_re;
+      im += sg * h.lo_t[t].cb_im;
+    }
+    Ltab[lo] = make_double2(re, im);
+  }
+  if (threadIdx.x < h.n_mx) mx[threadIdx.x] = h.mx_t[threadIdx.x];
+  __syncthreads();
+  double2 acc = make_double2(0.0, 0.0);
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    double hre = 0.0, him = 0.0;
+    for (uint32_t t = 0; t < h.n_hi; ++t) {
+      const double sg = parity_sign(tile & (h.hi_t[t].yz >> B));
+      hre += sg * h.hi_t[t].cb_re;
+      him += sg * h.hi_t[t].cb_im;
+    }
+    const uint64_t base = tile << B;
+    for (uint32_t lo0 = threadIdx.x; lo0 < tile_amps; lo0 += kThreads * kU) {
+      A x[kU];
+      double2 l[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t lo = lo0 + u * kThreads;
+        if (lo < tile_amps) x[u] = psi[base | lo];
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t lo = lo0 + u * kThreads;
+        const uint64_t i = base | lo;
+        double dre = 0.0, dim = 0.0;
+        if (lo < tile_amps) {
+          const double2 lt = Ltab[lo];
+          dre = lt.x + hre;
+          dim = lt.y + him;
+          for (uint32_t t = 0; t < h.n_mx; ++t) {
+            const double sg = parity_sign(i & mx[t].yz);
+            dre += sg * mx[t].cb_re;
+            dim += sg * mx[t].cb_im;
+          }
+        }
+        l[u] = make_double2(dre * (double)x[u].x - dim * (double)x[u].y, dre * (double)x[u].y + dim * (double)x[u].x);
+      }
+      for (uint32_t g = 0; g < h.n_groups; ++g) {
+        const uint64_t f = h.flips[g];
+        A y[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t lo = lo0 + u * kThreads;
+          if (lo < tile_amps) y[u] = psi[(base | lo) ^ f];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint64_t i = base | (lo0 + u * kThreads);
+          double ore = 0.0, oim = 0.0;
+          for (uint32_t t = h.group_off[g]; t < h.group_off[g + 1]; ++t) {
+            const double sg = parity_sign(i & h.terms[t].yz);
+            ore += sg * h.terms[t].cb_re;
+            oim += sg * h.terms[t].cb_im;
+          }
+          l[u].x += ore * (double)y[u].x - oim * (double)y[u].y;
+          l[u].y += ore * (double)y[u].y + oim * (double)y[u].x;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t lo = lo0 + u * kThreads;
+        if (lo >= tile_amps) break;
+        A out;
+        out.x = static_cast<T>(l[u].x);
+        out.y = static_cast<T>(l[u].y);
+        lam[base | lo] = out;
+        // <psi|lambda> += conj(psi_i) lambda_i
+        acc.x += (double)x[u].x * l[u].x + (double)x[u].y * l[u].y;
+        acc.y += (double)x[u].x * l[u].y - (double)x[u].y * l[u].x;
+      }
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = acc.x;
+    partials[2 * blockIdx.x + 1] = acc.y;
+  }
+}
+
+// One backward step of a Givens-type parameterised gate G(theta) =
+// [[c, -s], [s, c]] on amplitude pairs (r | pat_a, r | pat_b), r = index with
+// M zero bits inserted at pos[] (RY: M = 1, pat_a = 0, pat_b = bit;
+// DoubleExcitation: M = 4, |1100> / |0011>; SingleExcitation: M = 2).
+//   psi'  = G^dag psi                       (psi_{k-1})
+//   g    += Re( conj(l_a) mu_a + conj(l_b) mu_b ),  mu = (dG/dtheta) psi'
+//   lam'  = G^dag lam
+// dG/dtheta = 1/2 [[-s, -c], [c, -s]].  Per-block partials of g.
+template <typename T, int M>
+__global__ void __launch_bounds__(kThreads) k_adj_givens(typename V2<T>::type* __restrict__ psi,
+                                                         typename V2<T>::type* __restrict__ lam, uint32_t n,
+                                                         uint64_t pat_a, uint64_t pat_b, uint64_t total, uint32_t p0,
+                                                         uint32_t p1, uint32_t p2, uint32_t p3, double c, double s,
+                                                         double* __restrict__ partials) {
+  using A = typename V2<T>::type;
+  const uint32_t pos[4] = {p0, p1, p2, p3};
+  const T ct = static_cast<T>(c), st = static_cast<T>(s);
+  double acc = 0.0;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t k0 = (uint64_t)blockIdx.x * kThreads + threadIdx.x; k0 < total; k0 += stride * kU) {
+    A a[kU], b[kU], la[kU], lb[kU];
+    uint64_t r[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t k = k0 + u * stride;
+      uint64_t x = k;
+#pragma unroll
+      for (int m = 0; m < M; ++m) x = insert_zero(x, pos[m]);
+      r[u] = x;
+      if (k < total) {
+        a[u] = psi[x | pat_a];
+        b[u] = psi[x | pat_b];
+        la[u] = lam[x | pat_a];
+        lb[u] = lam[x | pat_b];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (k0 + u * stride >= total) break;
+      // psi' = G^dag psi: a' = c a + s b, b' = -s a + c b
+      A pa, pb;
+      pa.x = ct * a[u].x + st * b[u].x;
+      pa.y = ct * a[u].y + st * b[u].y;
+      pb.x = ct * b[u].x - st * a[u].x;
+      pb.y = ct * b[u].y - st * a[u].y;
+      // mu = dG psi' = 1/2 (-s a' - c b', c a' - s b')
+      const double mar = 0.5 * (-s * (double)pa.x - c * (double)pb.x), mai = 0.5 * (-s * (double)pa.y - c * (double)pb.y);
+      const double mbr = 0.5 * (c * (double)pa.x - s * (double)pb.x), mbi = 0.5 * (c * (double)pa.y - s * (double)pb.y);
+      acc += (double)la[u].x * mar + (double)la[u].y * mai + (double)lb[u].x * mbr + (double)lb[u].y * mbi;
+      A qa, qb;
+      qa.x = ct * la[u].x + st * lb[u].x;
+      qa.y = ct * la[u].y + st * lb[u].y;
+      qb.x = ct * lb[u].x - st * la[u].x;
+      qb.y = ct * lb[u].y - st * la[u].y;
+      psi[r[u] | pat_a] = pa;
+      psi[r[u] | pat_b] = pb;
+      lam[r[u] | pat_a] = qa;
+      lam[r[u] | pat_b] = qb;
+    }
+  }
+  const double2 t = block_sum(make_double2(acc, 0.0));
+  if (threadIdx.x == 0) partials[blockIdx.x] = t.x;
+}
+
+// Self-inverse CNOT on both vectors in one pass.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_adj_cnot(typename V2<T>::type* __restrict__ psi,
+                                                       typename V2<T>::type* __restrict__ lam, uint32_t n,
+                                                       uint32_t pos_lo, uint32_t pos_hi, uint64_t cbit, uint64_t tbit,
+                                                       uint64_t total) {
+  using A = typename V2<T>::type;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t k0 = (uint64_t)blockIdx.x * kThreads + threadIdx.x; k0 < total; k0 += stride * kU) {
+    A a[kU], b[kU], la[kU], lb[kU];
+    uint64_t r[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t k = k0 + u * stride;
+      r[u] = insert_zero(insert_zero(k, pos_lo), pos_hi) | cbit;
+      if (k < total) {
+        a[u] = psi[r[u]];
+        b[u] = psi[r[u] | tbit];
+        la[u] = lam[r[u]];
+        lb[u] = lam[r[u] | tbit];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (k0 + u * stride >= total) break;
+      psi[r[u]] = b[u];
+      psi[r[u] | tbit] = a[u];
+      lam[r[u]] = lb[u];
+      lam[r[u] | tbit] = la[u];
+    }
+  }
+}
+
+// Fixed-order sums of per-block partials: out[j] = sum_b partials[j * nb + b]
+// for the P gradient rows (scaled by 2) and the energy row (complex).
+__global__ void k_adj_finish(const double* __restrict__ gpart, uint32_t P, uint32_t nb,
+                             const double* __restrict__ epart, uint32_t ne, double* __restrict__ out) {
+  const uint32_t j = blockIdx.x;
+  double2 acc = make_double2(0.0, 0.0);
+  if (j < P) {
+    for (uint32_t b = threadIdx.x; b < nb; b += kThreads) acc.x += gpart[(size_t)j * nb + b];
+  } else {
+    for (uint32_t b = threadIdx.x; b < ne; b += kThreads) {
+      acc.x += epart[2 * b];
+      acc.y += epart[2 * b + 1];
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) {
+    if (j < P) out[j] = 2.0 * acc.x;
+    else {
+      out[P] = acc.x;
+      out[P + 1] = acc.y;
+    }
+  }
+}
+
+template <typename T>
+void run_t(AdjointPlan& pl, const std::vector<AdjGate>& prog, const std::vector<double>& theta, double* e_out,
+           double* grad_out) {
+  using A = typename V2<T>::type;
+  vqf_statevector* sv = pl.psi;
+  A* psi = static_cast<A*>(pl.psi->amps);
+  A* lam = static_cast<A*>(pl.lam->amps);
+  const uint32_t n = sv->n_qubits;
+  cudaStream_t st = sv->stream;
+  const auto grid_for = [](uint64_t items) {
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((items + kThreads * kU - 1) / (kThreads * kU), kBlocks)));
+  };
+  // lambda = H psi, E = <psi|lambda>
+  const uint32_t B = pl.tile_bits;
+  k_apply_ham<T><<<pl.nb_ham, kThreads, sizeof(double2) << B, st>>>(psi, lam, n, B, pl.hd, pl.epart);
+  VQF_LAUNCHED();
+  // backward sweep
+  for (size_t gi = prog.size(); gi-- > 0;) {
+    const AdjGate& g = prog[gi];
+    const auto bit_of = [n](uint32_t w) { return n - 1 - w; };
+    if (g.kind == VQF_GATE_CNOT) {
+      const uint32_t bc = bit_of(g.wires[0]), bt = bit_of(g.wires[1]);
+      const uint64_t total = uint64_t{1} << (n - 2);
+      k_adj_cnot<T><<<grid_for(total), kThreads, 0, st>>>(psi, lam, n, std::min(bc, bt), std::max(bc, bt),
+                                                           uint64_t{1} << bc, uint64_t{1} << bt, total);
+    } else {
+      const double th = theta[g.param];
+      const double c = std::cos(0.5 * th), s = std::sin(0.5 * th);
+      double* gp = pl.gpart + (size_t)g.param * pl.nb;
+      if (g.kind == VQF_GATE_RY) {
+        const uint32_t b = bit_of(g.wires[0]);
+        const uint64_t total = uint64_t{1} << (n - 1);
+        k_adj_givens<T, 1><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, 0, uint64_t{1} << b, total, b, 0, 0, 0, c, s, gp);
+      } else if (g.kind == VQF_GATE_DOUBLE_EXCITATION) {
+        uint32_t pos[4];
+        uint64_t m[4];
+        for (int i = 0; i < 4; ++i) {
+          pos[i] = bit_of(g.wires[i]);
+          m[i] = uint64_t{1} << pos[i];
+        }
+        std::sort(pos, pos + 4);
+        const uint64_t total = uint64_t{1} << (n - 4);
+        k_adj_givens<T, 4><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, m[0] | m[1], m[2] | m[3], total, pos[0], pos[1],
+                                                       pos[2], pos[3], c, s, gp);
+      } else {  // SingleExcitation
+        uint32_t pos[2] = {bit_of(g.wires[0]), bit_of(g.wires[1])};
+        const uint64_t m0 = uint64_t{1} << pos[0], m1 = uint64_t{1} << pos[1];
+        std::sort(pos, pos + 2);
+        const uint64_t total = uint64_t{1} << (n - 2);
+        k_adj_givens<T, 2><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, m0, m1, total, pos[0], pos[1], 0, 0, c, s, gp);
+      }
+    }
+    VQF_LAUNCHED();
+  }
+  const uint32_t P = pl.P;
+  k_adj_finish<<<P + 1, kThreads, 0, st>>>(pl.gpart, P, pl.nb, pl.epart, pl.nb_ham, pl.dout);
+  VQF_LAUNCHED();
+  VQF_CUDA(cudaMemcpyAsync(pl.hout, pl.dout, (P + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  VQF_CUDA(cudaStreamSynchronize(st));
+  VQF_CUDA(cudaGetLastError());
+  std::memcpy(grad_out, pl.hout, P * sizeof(double));
+  e_out[0] = pl.hout[P];
+  e_out[1] = pl.hout[P + 1];
+}
+
+}  // namespace
+
+void AdjointPlan::init(vqf_statevector* psi_, vqf_statevector* lam_, const CompiledHam& h, uint32_t n_params) {
+  psi = psi_;
+  lam = lam_;
+  P = n_params;
+  const uint32_t n = psi->n_qubits;
+  tile_bits = std::min<uint32_t>(n, kTileBits);
+  nb = kBlocks;
+  nb_ham = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t{1} << (n - tile_bits), kBlocks)));
+  // Hamiltonian tables: diagonal split + off-diagonal groups
+  const uint64_t lo_mask = (uint64_t{1} << tile_bits) - 1;
+  std::vector<MaskTerm> lo, hi, mx, off;
+  std::vector<uint64_t> flips;
+  std::vector<uint32_t> goff{0};
+  for (uint32_t t = h.group_offset[0]; t < h.group_offset[1]; ++t) {
+    const MaskTerm& m = h.terms[t];
+    if ((m.yz & ~lo_mask) == 0) lo.push_back(m);
+    else if ((m.yz & lo_mask) == 0) hi.push_back(m);
+    else mx.push_back(m);
+  }
+  if (mx.size() > 64) throw_invalid("adjoint gradient: more than 64 diagonal terms straddle the tile boundary");
+  for (size_t g = 1; g + 1 < h.group_offset.size(); ++g) {
+    flips.push_back(h.group_flip[g]);
+    for (uint32_t t = h.group_offset[g]; t < h.group_offset[g + 1]; ++t) off.push_back(h.terms[t]);
+    goff.push_back(static_cast<uint32_t>(off.size()));
+  }
+  if (flips.size() > kMaxGroups || off.size() > kMaxTerms) throw_invalid("adjoint gradient: Hamiltonian too large");
+  std::vector<unsigned char> blob;
+  auto put = [&](const void* p, size_t bytes) {
+    const size_t at = (blob.size() + 15) & ~size_t{15};
+    blob.resize(at + std::max<size_t>(bytes, 16));
+    if (bytes) std::memcpy(blob.data() + at, p, bytes);
+    return at;
+  };
+  const size_t o_lo = put(lo.data(), lo.size() * sizeof(MaskTerm));
+  const size_t o_hi = put(hi.data(), hi.size() * sizeof(MaskTerm));
+  const size_t o_mx = put(mx.data(), mx.size() * sizeof(MaskTerm));
+  const size_t o_fl = put(flips.data(), flips.size() * sizeof(uint64_t));
+  const size_t o_go = put(goff.data(), goff.size() * sizeof(uint32_t));
+  const size_t o_te = put(off.data(), off.size() * sizeof(MaskTerm));
+  const size_t o_gp = put(nullptr, 0);
+  blob.resize(o_gp);
+  const size_t bytes = o_gp + sizeof(double) * ((size_t)P * nb + 2 * (size_t)nb_ham + P + 2);
+  VQF_CUDA(cudaSetDevice(psi->device));
+  VQF_CUDA(cudaMalloc(&dev, bytes));
+  VQF_CUDA(cudaMemcpy(dev, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+  VQF_CUDA(cudaMallocHost(&hout, sizeof(double) * (P + 2)));
+  auto* d = static_cast<unsigned char*>(dev);
+  hd = HamDevC{reinterpret_cast<const MaskTerm*>(d + o_lo), reinterpret_cast<const MaskTerm*>(d + o_hi),
+               reinterpret_cast<const MaskTerm*>(d + o_mx), static_cast<uint32_t>(lo.size()),
+               static_cast<uint32_t>(hi.size()), static_cast<uint32_t>(mx.size()),
+               reinterpret_cast<const uint64_t*>(d + o_fl), reinterpret_cast<const uint32_t*>(d + o_go),
+               reinterpret_cast<const MaskTerm*>(d + o_te), static_cast<uint32_t>(flips.size())};
+  gpart = reinterpret_cast<double*>(d + o_gp);
+  epart = gpart + (size_t)P * nb;
+  dout = epart + 2 * (size_t)nb_ham;
+  const int smem = static_cast<int>(sizeof(double2) << tile_bits);
+  VQF_CUDA(cudaFuncSetAttribute(k_apply_ham<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  VQF_CUDA(cudaFuncSetAttribute(k_apply_ham<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  VQF_CUDA(cudaMemsetAsync(gpart, 0, sizeof(double) * (size_t)P * nb, psi->stream));
+}
+
+AdjointPlan::~AdjointPlan() {
+  if (dev) cudaFree(dev);
+  if (hout) cudaFreeHost(hout);
+}
+
+void AdjointPlan::run(const std::vector<AdjGate>& prog, const std::vector<double>& theta, double* e_out,
+                      double* grad_out) {
+  VQF_CUDA(cudaSetDevice(psi->device));
+  if (psi->dtype == VQF_F64)
+    run_t<double>(*this, prog, theta, e_out, grad_out);
+  else
+    run_t<float>(*this, prog, theta, e_out, grad_out);
+}
+
+}  // namespace vqf

@@ -13,6 +13,7 @@
 #include <memory>
 #include <thread>
 
+#include "adjoint.cuh"
 #include "chem_host.h"
 #include "pauli_host.h"
 #include "sv.cuh"
@@ -417,12 +418,50 @@ struct ShiftEvaluator {
   }
 };
 
+// prepare_ansatz (vqe.hpp:65-96) as a gate list for the adjoint sweep.
+std::vector<AdjGate> ansatz_program(int32_t kind, uint32_t layers, uint32_t n) {
+  std::vector<AdjGate> prog;
+  if (kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION) {
+    prog.push_back(AdjGate{VQF_GATE_DOUBLE_EXCITATION, {0, 1, 2, 3}, 0});
+    return prog;
+  }
+  int32_t k = 0;
+  for (uint32_t layer = 0; layer < layers; ++layer) {
+    for (uint32_t q = 0; q < n; ++q) prog.push_back(AdjGate{VQF_GATE_RY, {q, 0, 0, 0}, k++});
+    for (uint32_t q = 0; q + 1 < n; ++q) prog.push_back(AdjGate{VQF_GATE_CNOT, {q, q + 1, 0, 0}, -1});
+  }
+  return prog;
+}
+
+// Forward state + lambda vector + adjoint plan for one register.
+struct AdjointRunner {
+  HbmEngine eng;
+  vqf_statevector* lam = nullptr;
+  AdjointPlan plan;
+  std::vector<AdjGate> prog;
+  AdjointRunner(uint32_t n, int32_t kind, uint32_t layers, int device, const CompiledHam& ch)
+      : eng(n, kind, layers, 1, device), prog(ansatz_program(kind, layers, n)) {
+    if (vqf_sv_create(n, 1, VQF_F64, device, &lam) != VQF_OK) throw Error(VQF_CUDA_ERROR, vqf_last_error());
+    plan.init(eng.sv, lam, ch, eng.P);
+  }
+  ~AdjointRunner() { vqf_sv_destroy(lam); }
+  // E(theta) (complex) and dE/dtheta.
+  void run(const std::vector<double>& theta, double* e, double* grad) {
+    eng.prepare([&](uint32_t j, uint32_t) { return theta[j]; });
+    plan.run(prog, theta, e, grad);
+  }
+};
+
 void run_vqe_hbm(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const vqf_adam_config& cfg,
-                 const std::vector<double>& init, int device, vqf_vqe_result* r) {
+                 const std::vector<double>& init, int32_t method, int device, vqf_vqe_result* r) {
   const uint32_t n = h->n_qubits;
   const CompiledHam ch = compile_hamiltonian(h);
-  ShiftEvaluator ev(n, kind, layers, device);
-  const uint32_t P = ev.P;
+  const bool adjoint = method == VQF_GRAD_ADJOINT;
+  std::unique_ptr<ShiftEvaluator> evp;
+  std::unique_ptr<AdjointRunner> adj;
+  if (adjoint) adj = std::make_unique<AdjointRunner>(n, kind, layers, device, ch);
+  else evp = std::make_unique<ShiftEvaluator>(n, kind, layers, device);
+  const uint32_t P = ansatz_params(kind, layers, n);
   std::vector<double> theta = init.empty() ? std::vector<double>(P, 0.0) : init;
   std::vector<double> m(P, 0.0), v(P, 0.0), grad(P), tn(P), mn(P), vn(P), E;
   int64_t step = 0;
@@ -439,16 +478,25 @@ void run_vqe_hbm(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const 
   };
   double last = 0.0;
   for (int iter = 0; iter < cfg.max_iterations; ++iter) {
-    ev.run(theta, ch, static_cast<int>(ev.NC), E);
+    if (adjoint) {
+      // one forward + one backward sweep; circuit_evaluations counts the
+      // forward circuits actually executed
+      E.assign(2, 0.0);
+      adj->run(theta, E.data(), grad.data());
+    } else {
+      evp->run(theta, ch, static_cast<int>(evp->NC), E);
+    }
     if (std::abs(E[1]) >= 1e-10) throw_runtime(imag_msg(E[1]));
     ++r->circuit_evaluations;
     if (!std::isfinite(E[0])) throw_runtime(nonfinite_msg(iter, theta.data(), P));
     push(E[0]);
     last = E[0];
-    for (uint32_t c = 1; c < ev.NC; ++c)
-      if (std::abs(E[2 * c + 1]) >= 1e-10) throw_runtime(imag_msg(E[2 * c + 1]));
-    for (uint32_t k = 0; k < P; ++k) grad[k] = 0.5 * (E[2 * (2 * k + 1)] - E[2 * (2 * k + 2)]);
-    r->circuit_evaluations += 2 * (uint64_t)P;
+    if (!adjoint) {
+      for (uint32_t c = 1; c < evp->NC; ++c)
+        if (std::abs(E[2 * c + 1]) >= 1e-10) throw_runtime(imag_msg(E[2 * c + 1]));
+      for (uint32_t k = 0; k < P; ++k) grad[k] = 0.5 * (E[2 * (2 * k + 1)] - E[2 * (2 * k + 2)]);
+      r->circuit_evaluations += 2 * (uint64_t)P;
+    }
     if (cfg.has_gradient_tolerance) {
       double g_inf = 0.0;
       for (double g : grad) g_inf = std::max(g_inf, std::abs(g));
@@ -465,7 +513,13 @@ void run_vqe_hbm(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const 
     r->iterations_run = iter + 1;
   }
   if (!converged) {
-    ev.run(theta, ch, 1, E);
+    if (adjoint) {
+      adj->eng.prepare([&](uint32_t j, uint32_t) { return theta[j]; });
+      E.assign(2, 0.0);
+      sv_expectation(adj->eng.sv, ch, E.data());
+    } else {
+      evp->run(theta, ch, 1, E);
+    }
     if (std::abs(E[1]) >= 1e-10) throw_runtime(imag_msg(E[1]));
     ++r->circuit_evaluations;
     if (!std::isfinite(E[0])) throw_runtime(nonfinite_msg(cfg.max_iterations, theta.data(), P));
@@ -490,7 +544,7 @@ void run_vqe_impl(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const
   check_ansatz_register(kind, n);
   if (method != VQF_GRAD_PARAMETER_SHIFT && method != VQF_GRAD_ADJOINT) throw_invalid("unknown gradient method");
   std::vector<double> init_v(init, init + n_init);
-  if (small_ok(n, P)) {
+  if (small_ok(n, P) && method == VQF_GRAD_PARAMETER_SHIFT) {
     SmallJob j;
     j.batch = 1;
     j.n_qubits = static_cast<int32_t>(n);
@@ -506,7 +560,7 @@ void run_vqe_impl(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const
     if (j.status[0] != kStatusOk) throw_runtime(small_error(j, 0, 0.0));
     fill_result(j, 0, r);
   } else {
-    run_vqe_hbm(h, kind, layers, *cfg, init_v, device, r);
+    run_vqe_hbm(h, kind, layers, *cfg, init_v, method, device, r);
   }
   r->wall_seconds = seconds_since(t0);
 }
@@ -695,8 +749,14 @@ int vqf_gradient(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h
     check_ansatz_register(kind, h->n_qubits);
     if (method != VQF_GRAD_PARAMETER_SHIFT && method != VQF_GRAD_ADJOINT) throw_invalid("unknown gradient method");
     const CompiledHam ch = compile_hamiltonian(h);
-    ShiftEvaluator ev(h->n_qubits, kind, layers, device);
     std::vector<double> th(theta, theta + n_theta), E;
+    if (method == VQF_GRAD_ADJOINT) {
+      AdjointRunner adj(h->n_qubits, kind, layers, device, ch);
+      double e[2];
+      adj.run(th, e, grad_out);
+      return;
+    }
+    ShiftEvaluator ev(h->n_qubits, kind, layers, device);
     ev.run(th, ch, static_cast<int>(ev.NC), E);
     for (uint32_t c = 1; c < ev.NC; ++c)
       if (std::abs(E[2 * c + 1]) >= 1e-10) throw_runtime(imag_msg(E[2 * c + 1]));

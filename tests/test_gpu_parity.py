@@ -390,3 +390,45 @@ def test_large_register_properties(gpu):
     V.apply_circuit(psi, [V.Gate.ry(-0.3, q) for q in range(n)])
     z = V.expectation(psi, V.build_z_sum(n))
     assert abs(z - n) < 1e-9
+
+
+# ------------------------------------------------------- adjoint gradient
+@pytest.mark.parametrize("n", [4, 7, 10])
+def test_adjoint_gradient_matches_parameter_shift_oracle(gpu, orc, n):
+    """Adjoint (one forward + one backward sweep) vs the reference's
+    parameter-shift rule (vqe.hpp:112-127) on the oracle."""
+    V = gpu
+    rng = np.random.default_rng(40 + n)
+    hea = V.AnsatzSpec.hardware_efficient(2)
+    for h in [orc.build_tfim(n, 1.0, 0.8), orc.canonicalize(random_hamiltonian(random.Random(n), n, 20))]:
+        th = rng.uniform(-2, 2, 2 * n)
+        g = V.gradient(th, to_v(V, h), hea, method="adjoint")
+        assert np.max(np.abs(g - orc.gradient(1, 2, th, h))) < E_TOL
+    h2 = orc.build_h2_hamiltonian(0.9)
+    g = V.gradient([0.4], to_v(V, h2), V.AnsatzSpec.h2_double_excitation(), method="adjoint")
+    assert abs(g[0] - orc.gradient(0, 0, [0.4], h2)[0]) < E_TOL
+
+
+def test_adjoint_run_vqe_matches_golden(gpu, golden):
+    V = gpu
+    for key in ["tfim6", "tfim8"]:
+        g = golden("vqe_runs.json")["hea"][key]
+        n = g["hamiltonian"]["n_qubits"]
+        h, _ = ham_from_text(V, n, g["hamiltonian"]["text"])
+        r = V.run_vqe(h, V.AnsatzSpec.hardware_efficient(g["layers"]),
+                      V.AdamConfig(learning_rate=g["lr"], max_iterations=g["max_iterations"]), [g["theta_init"]] * (2 * n),
+                      method="adjoint")
+        assert np.max(np.abs(np.array(r.trajectory) - g["trajectory"])) < E_TOL
+        assert np.max(np.abs(np.array(r.theta) - g["theta"])) < 1e-9
+
+
+def test_adjoint_equals_shift_at_width_20(gpu):
+    """Both engines of ours at a width the oracle would take minutes on."""
+    V = gpu
+    n = 20
+    h = V.build_tfim(n, 1.0, 1.0)
+    th = np.random.default_rng(7).uniform(-1, 1, 2 * n)
+    hea = V.AnsatzSpec.hardware_efficient(2)
+    ga = V.gradient(th, h, hea, method="adjoint")
+    gs = V.gradient(th, h, hea, method="shift")
+    assert np.max(np.abs(ga - gs)) < 1e-10
