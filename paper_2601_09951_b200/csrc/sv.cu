@@ -12,6 +12,7 @@
 //   expectation, per flip group             : S    (read once)
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 
 #include "sv.cuh"
 
@@ -602,6 +603,18 @@ void sv_norms(vqf_statevector* sv, double* out) {
   for (uint32_t b = 0; b < sv->batch; ++b) out[b] = std::sqrt(tmp[2 * b]);
 }
 
+void retain_pool(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (std::find(done.begin(), done.end(), device) != done.end()) return;
+  cudaMemPool_t pool;
+  VQF_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t threshold = UINT64_MAX;
+  VQF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  done.push_back(device);
+}
+
 void sv_ensure_cs(vqf_statevector* sv, size_t n_doubles) {
   if (sv->cs_cap >= n_doubles) return;
   if (sv->cs_dev) VQF_CUDA(cudaFree(sv->cs_dev));
@@ -630,7 +643,12 @@ int vqf_sv_create(uint32_t n_qubits, uint32_t batch, int32_t dtype, int32_t devi
       VQF_CUDA(cudaSetDevice(device));
       VQF_CUDA(cudaStreamCreateWithFlags(&sv->own_stream, cudaStreamNonBlocking));
       sv->stream = sv->own_stream;
-      VQF_CUDA(cudaMalloc(&sv->amps, sv->amp_bytes() * sv->dim() * batch));
+      // stream-ordered allocation from the device pool, whose release
+      // threshold is raised once per device so freed states stay mapped and
+      // repeated calls (VQE iterations, scaling widths) reuse HBM instead of
+      // paying cudaMalloc page-mapping costs
+      retain_pool(device);
+      VQF_CUDA(cudaMallocAsync(&sv->amps, sv->amp_bytes() * sv->dim() * batch, sv->stream));
       VQF_CUDA(cudaMallocHost(&sv->host_out, 2 * sizeof(double) * batch));
       VQF_CUDA(cudaMalloc(&sv->dev_out, 2 * sizeof(double) * batch));
       sv_reset(sv, 0);
@@ -649,7 +667,10 @@ int vqf_sv_destroy(vqf_sv sv) {
     cudaSetDevice(sv->device);
     if (sv->stream) cudaStreamSynchronize(sv->stream);
     if (sv->own_stream && sv->own_stream != sv->stream) cudaStreamSynchronize(sv->own_stream);
-    if (sv->amps) cudaFree(sv->amps);
+    if (sv->amps) {  // freed on the handle's own stream (a caller stream may be gone)
+      cudaFreeAsync(sv->amps, sv->own_stream);
+      cudaStreamSynchronize(sv->own_stream);
+    }
     if (sv->partials) cudaFree(sv->partials);
     if (sv->terms_dev) cudaFree(sv->terms_dev);
     if (sv->cs_dev) cudaFree(sv->cs_dev);

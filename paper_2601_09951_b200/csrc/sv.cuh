@@ -52,5 +52,7 @@ void sv_expectation(vqf_statevector* sv, const CompiledHam& h, double* out);
 void sv_expectation_async(vqf_statevector* sv, const CompiledHam& h, double* dev_out);
 void sv_norms(vqf_statevector* sv, double* out);
 void sv_ensure_cs(vqf_statevector* sv, size_t n_doubles);
+// Keeps freed stream-ordered allocations of `device` cached in its pool.
+void retain_pool(int device);
 
 }  // namespace vqf
