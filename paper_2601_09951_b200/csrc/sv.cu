@@ -15,6 +15,7 @@
 #include <mutex>
 
 #include "sv.cuh"
+#include "tile.cuh"
 
 namespace vqf {
 
@@ -770,12 +771,20 @@ int vqf_apply_circuit(vqf_sv sv, const vqf_gate* gates, uint32_t n_gates) {
   return guarded([&] {
     if (sv == nullptr) throw_invalid("null state vector");
     VQF_CUDA(cudaSetDevice(sv->device));
-    for (uint32_t i = 0; i < n_gates; ++i) {
-      const vqf_gate& g = gates[i];
-      sv_check_gate(sv, g);
+    for (uint32_t i = 0; i < n_gates; ++i) sv_check_gate(sv, gates[i]);  // all-or-nothing validation
+    if (n_gates == 1) {
+      const vqf_gate& g = gates[0];
       GateArgs a{g.kind, g.n_wires, {g.wires[0], g.wires[1], g.wires[2], g.wires[3]}, std::cos(0.5 * g.angle),
                  std::sin(0.5 * g.angle), nullptr};
       sv_apply(sv, a);
+    } else {  // fused shared-memory tile passes (tile.cu)
+      std::vector<TGate> tg(n_gates);
+      for (uint32_t i = 0; i < n_gates; ++i) {
+        const vqf_gate& g = gates[i];
+        tg[i] = TGate{g.kind, g.n_wires, {g.wires[0], g.wires[1], g.wires[2], g.wires[3]}, -1,
+                      std::cos(0.5 * g.angle), std::sin(0.5 * g.angle)};
+      }
+      run_circuit_tiled(sv, tg, nullptr);
     }
     VQF_CUDA(cudaStreamSynchronize(sv->stream));
   });

@@ -17,6 +17,7 @@
 #include "chem_host.h"
 #include "pauli_host.h"
 #include "sv.cuh"
+#include "tile.cuh"
 #include "vqe_small.cuh"
 
 namespace vqf {
@@ -316,6 +317,22 @@ void fill_result(const SmallJob& j, uint32_t b, vqf_vqe_result* r) {
   r->circuit_evaluations = grads * (1 + 2 * (uint64_t)j.P) + (conv ? 0 : 1);
 }
 
+// prepare_ansatz (vqe.hpp:65-96) as a fusable gate list; parameterised gates
+// take their (cos, sin) from the engine's per-entry table.
+std::vector<TGate> ansatz_tgates(int32_t kind, uint32_t layers, uint32_t n) {
+  std::vector<TGate> g;
+  if (kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION) {
+    g.push_back(TGate{VQF_GATE_DOUBLE_EXCITATION, 4, {0, 1, 2, 3}, 0, 0.0, 0.0});
+    return g;
+  }
+  int32_t k = 0;
+  for (uint32_t layer = 0; layer < layers; ++layer) {
+    for (uint32_t q = 0; q < n; ++q) g.push_back(TGate{VQF_GATE_RY, 1, {q, 0, 0, 0}, k++, 0.0, 0.0});
+    for (uint32_t q = 0; q + 1 < n; ++q) g.push_back(TGate{VQF_GATE_CNOT, 2, {q, q + 1, 0, 0}, -1, 0.0, 0.0});
+  }
+  return g;
+}
+
 // ------------------------------------------------------------------------
 // HBM engine: prepare every circuit of `thetas` (NC rows of P angles) into
 // an NC-entry batch and evaluate <H>.  Angles go through the host libm
@@ -347,25 +364,8 @@ struct HbmEngine {
     sv_ensure_cs(sv, cs.size());
     VQF_CUDA(cudaMemcpyAsync(sv->cs_dev, cs.data(), cs.size() * sizeof(double), cudaMemcpyHostToDevice,
                              sv->stream));
-    const double* csd = sv->cs_dev;
-    if (kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION) {
-      sv_reset(sv, 12);  // basis_state(4, {1,1,0,0})
-      GateArgs g{VQF_GATE_DOUBLE_EXCITATION, 4, {0, 1, 2, 3}, 0, 0, csd};
-      sv_apply(sv, g);
-      return;
-    }
-    sv_reset(sv, 0);
-    uint32_t k = 0;
-    for (uint32_t layer = 0; layer < layers; ++layer) {
-      for (uint32_t q = 0; q < n; ++q, ++k) {
-        GateArgs g{VQF_GATE_RY, 1, {q, 0, 0, 0}, 0, 0, csd + 2 * (size_t)k * B};
-        sv_apply(sv, g);
-      }
-      for (uint32_t q = 0; q + 1 < n; ++q) {
-        GateArgs g{VQF_GATE_CNOT, 2, {q, q + 1, 0, 0}, 0, 0, nullptr};
-        sv_apply(sv, g);
-      }
-    }
+    sv_reset(sv, kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION ? 12 : 0);  // basis_state(4, {1,1,0,0}) / |0..0>
+    run_circuit_tiled(sv, ansatz_tgates(kind, layers, n), sv->cs_dev);
   }
 };
 
@@ -706,18 +706,14 @@ int vqf_prepare_ansatz(int32_t kind, uint32_t layers, const double* theta, uint3
       sv_apply(sv, g);
     } else {
       sv_reset(sv, 0);
-      const uint32_t n = sv->n_qubits;
-      uint32_t k = 0;
-      for (uint32_t layer = 0; layer < layers; ++layer) {
-        for (uint32_t q = 0; q < n; ++q, ++k) {
-          GateArgs g{VQF_GATE_RY, 1, {q, 0, 0, 0}, std::cos(0.5 * theta[k]), std::sin(0.5 * theta[k]), nullptr};
-          sv_apply(sv, g);
+      std::vector<TGate> g = ansatz_tgates(kind, layers, sv->n_qubits);
+      for (auto& t : g)
+        if (t.param >= 0) {
+          t.c = std::cos(0.5 * theta[t.param]);
+          t.s = std::sin(0.5 * theta[t.param]);
+          t.param = -1;
         }
-        for (uint32_t q = 0; q + 1 < n; ++q) {
-          GateArgs g{VQF_GATE_CNOT, 2, {q, q + 1, 0, 0}, 0, 0, nullptr};
-          sv_apply(sv, g);
-        }
-      }
+      run_circuit_tiled(sv, g, nullptr);
     }
     VQF_CUDA(cudaStreamSynchronize(sv->stream));
   });
