@@ -267,6 +267,17 @@ int vqf_apply_circuit(vqf_sv sv, const vqf_gate* gates, uint32_t n_gates);
 /* expectation (statevector.hpp:217-249) per batch entry; throws (returns
  * VQF_RUNTIME_ERROR) on an imaginary residue >= 1e-10 in any entry. */
 int vqf_expectation(vqf_sv sv, const vqf_hamiltonian* h, double* out);
+/* Same sum without the residue check, as interleaved (re, im) per entry:
+ * the per-shard partial of a distributed expectation (the check applies to
+ * the all-reduced total). */
+int vqf_expectation_complex(vqf_sv sv, const vqf_hamiltonian* h, double* out);
+/* sum_t c_t (-i)^{n_y} sum_i (-1)^popc(i & yz_t) conj(a_i) b_{i ^ flip_t} for
+ * two states of one register (batch entry 0), as (re, im): the shard-pair
+ * term of a distributed expectation whose Pauli string flips global wires. */
+int vqf_cross_expectation(vqf_sv a, vqf_sv b, const vqf_hamiltonian* h, double* out);
+/* Raw device address and byte size of the amplitudes (for exchanging
+ * shards with NCCL / peer copies; the handle keeps ownership). */
+int vqf_sv_device_ptr(vqf_sv sv, void** ptr, uint64_t* bytes);
 
 /* ---------------------------------------------------------------- VQE */
 /* prepare_ansatz (vqe.hpp:65-96) into every batch entry of sv. */

@@ -119,6 +119,9 @@ SIGNATURES = [
     ("vqf_apply_gate", C.c_int, [SV, C.POINTER(Gate)]),
     ("vqf_apply_circuit", C.c_int, [SV, C.POINTER(Gate), C.c_uint32]),
     ("vqf_expectation", C.c_int, [SV, C.POINTER(Hamiltonian), dp]),
+    ("vqf_expectation_complex", C.c_int, [SV, C.POINTER(Hamiltonian), dp]),
+    ("vqf_sv_device_ptr", C.c_int, [SV, C.POINTER(C.c_void_p), u64p]),
+    ("vqf_cross_expectation", C.c_int, [SV, SV, C.POINTER(Hamiltonian), dp]),
     ("vqf_prepare_ansatz", C.c_int, [C.c_int32, C.c_uint32, dp, C.c_uint32, SV]),
     ("vqf_energy", C.c_int, [dp, C.c_uint32, C.POINTER(Hamiltonian), C.c_int32, C.c_uint32, C.c_int32, dp]),
     ("vqf_gradient", C.c_int, [dp, C.c_uint32, C.POINTER(Hamiltonian), C.c_int32, C.c_uint32, C.c_int32, C.c_int32,

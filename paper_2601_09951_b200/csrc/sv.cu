@@ -320,6 +320,43 @@ __global__ void __launch_bounds__(kThreads) k_expect_diag_tiled(
   }
 }
 
+// Cross term between two states a, b of one register:
+//   sum_t cb_t sum_i (-1)^popc(i & yz_t) conj(a_i) b_{i ^ flip_t}
+// (the shard-pair contribution of a Pauli term that flips global wires of a
+// distributed state, paper_2601_09951_b200/dsv.py).  Terms in shared memory,
+// per-block partials, fixed-order final sum.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_expect_cross(const typename V2<T>::type* __restrict__ a,
+                                                           const typename V2<T>::type* __restrict__ bvec, uint32_t n,
+                                                           const MaskTerm* __restrict__ terms, uint32_t n_terms,
+                                                           double* __restrict__ partials) {
+  __shared__ MaskTerm st[64];
+  const uint64_t D = uint64_t{1} << n;
+  double2 acc = make_double2(0.0, 0.0);
+  for (uint32_t t0 = 0; t0 < n_terms; t0 += 64) {
+    const uint32_t cnt = min(64u, n_terms - t0);
+    __syncthreads();
+    if (threadIdx.x < cnt) st[threadIdx.x] = terms[t0 + threadIdx.x];
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < D; i += (uint64_t)gridDim.x * kThreads) {
+      const typename V2<T>::type x = a[i];
+      for (uint32_t t = 0; t < cnt; ++t) {
+        const typename V2<T>::type y = bvec[i ^ st[t].flip];
+        const double vr = (double)x.x * (double)y.x + (double)x.y * (double)y.y;
+        const double vi = (double)x.x * (double)y.y - (double)x.y * (double)y.x;
+        const double sg = parity_sign(i & st[t].yz);
+        acc.x += sg * (st[t].cb_re * vr - st[t].cb_im * vi);
+        acc.y += sg * (st[t].cb_re * vi + st[t].cb_im * vr);
+      }
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = acc.x;
+    partials[2 * blockIdx.x + 1] = acc.y;
+  }
+}
+
 // Off-diagonal group with flip mask f (statevector.hpp:235-241): each pair
 // (i, j = i ^ f), i with f's top bit clear, is read once.  With
 // v = conj(psi_i) psi_j and sigma_t = (-1)^popc(f & yz_t), the two
@@ -787,6 +824,61 @@ int vqf_apply_circuit(vqf_sv sv, const vqf_gate* gates, uint32_t n_gates) {
       run_circuit_tiled(sv, tg, nullptr);
     }
     VQF_CUDA(cudaStreamSynchronize(sv->stream));
+  });
+}
+
+int vqf_expectation_complex(vqf_sv sv, const vqf_hamiltonian* h, double* out) {
+  return guarded([&] {
+    if (sv == nullptr) throw_invalid("null state vector");
+    if (h == nullptr) throw_invalid("null hamiltonian");
+    if (h->n_qubits != sv->n_qubits) throw_invalid("expectation: qubit count mismatch");
+    const CompiledHam c = compile_hamiltonian(h);
+    VQF_CUDA(cudaSetDevice(sv->device));
+    sv_expectation(sv, c, out);
+  });
+}
+
+int vqf_sv_device_ptr(vqf_sv sv, void** ptr, uint64_t* bytes) {
+  return guarded([&] {
+    if (sv == nullptr) throw_invalid("null state vector");
+    VQF_CUDA(cudaStreamSynchronize(sv->stream));
+    *ptr = sv->amps;
+    *bytes = sv->amp_bytes() * sv->dim() * sv->batch;
+  });
+}
+
+int vqf_cross_expectation(vqf_sv a, vqf_sv b, const vqf_hamiltonian* h, double* out) {
+  return guarded([&] {
+    if (a == nullptr || b == nullptr || h == nullptr) throw_invalid("null argument");
+    if (a->n_qubits != b->n_qubits || h->n_qubits != a->n_qubits || a->dtype != b->dtype || a->device != b->device)
+      throw_invalid("cross expectation: states must share register, dtype and device");
+    const CompiledHam c = compile_hamiltonian(h);
+    VQF_CUDA(cudaSetDevice(a->device));
+    VQF_CUDA(cudaStreamSynchronize(b->stream));
+    const uint32_t nb = red_blocks(a->dim());
+    ensure_partials(a, 2 * (size_t)nb);
+    const size_t tb = std::max<size_t>(1, c.terms.size()) * sizeof(MaskTerm);
+    ensure_terms(a, tb);
+    if (!c.terms.empty())
+      VQF_CUDA(cudaMemcpyAsync(a->terms_dev, c.terms.data(), c.terms.size() * sizeof(MaskTerm),
+                               cudaMemcpyHostToDevice, a->stream));
+    const MaskTerm* td = static_cast<const MaskTerm*>(a->terms_dev);
+    const uint32_t nt = static_cast<uint32_t>(c.terms.size());
+    if (a->dtype == VQF_F64)
+      k_expect_cross<double><<<nb, kThreads, 0, a->stream>>>(static_cast<const double2*>(a->amps),
+                                                            static_cast<const double2*>(b->amps), a->n_qubits, td, nt,
+                                                            a->partials);
+    else
+      k_expect_cross<float><<<nb, kThreads, 0, a->stream>>>(static_cast<const float2*>(a->amps),
+                                                           static_cast<const float2*>(b->amps), a->n_qubits, td, nt,
+                                                           a->partials);
+    VQF_LAUNCHED();
+    k_final_sum<<<1, kThreads, 0, a->stream>>>(a->partials, nb, a->dev_out);
+    VQF_LAUNCHED();
+    VQF_CUDA(cudaMemcpyAsync(a->host_out, a->dev_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, a->stream));
+    VQF_CUDA(cudaStreamSynchronize(a->stream));
+    out[0] = a->host_out[0];
+    out[1] = a->host_out[1];
   });
 }
 
