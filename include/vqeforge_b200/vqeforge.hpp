@@ -151,6 +151,100 @@ inline QubitHamiltonian canonicalize(const QubitHamiltonian& h) {
   return buf.result(h.n_qubits);
 }
 
+inline char axis_char(PauliAxis a) {
+  switch (a) {
+    case PauliAxis::I: return 'I';
+    case PauliAxis::X: return 'X';
+    case PauliAxis::Y: return 'Y';
+    case PauliAxis::Z: return 'Z';
+  }
+  return '?';
+}
+
+// pauli.hpp:294-309: one term per line, "%.17g %.17g <axis><index>...".
+inline std::string to_text(const QubitHamiltonian& h) {
+  std::string out;
+  char buf[64];
+  for (const auto& t : h.terms) {
+    std::snprintf(buf, sizeof buf, "%.17g", t.coefficient.real());
+    out += buf;
+    std::snprintf(buf, sizeof buf, "%.17g", t.coefficient.imag());
+    out += ' ';
+    out += buf;
+    if (!t.axes.empty()) {
+      out += ' ';
+      for (const auto& [q, a] : t.axes) out += axis_char(a) + std::to_string(q);
+    }
+    out += '\n';
+  }
+  return out;
+}
+
+inline constexpr std::uint32_t kDenseOracleMaxQubits = 12;  // pauli.hpp:51
+
+struct TooManyQubits : std::domain_error {  // pauli.hpp:53-58
+  explicit TooManyQubits(std::uint32_t n)
+      : std::domain_error("dense oracle limited to " + std::to_string(kDenseOracleMaxQubits) + " qubits, got " +
+                          std::to_string(n)) {}
+};
+
+// pauli.hpp:278-285 exact_ground_energy: lowest eigenvalue of the dense
+// realisation (host; the n x n Hermitian matrix is embedded as the 2n x 2n
+// real symmetric [[A, -B], [B, A]] and diagonalised by cyclic Jacobi — the
+// oracle used by the reference's variational-bound checks, not a hot path).
+inline double exact_ground_energy(const QubitHamiltonian& h) {
+  if (h.n_qubits > kDenseOracleMaxQubits) throw TooManyQubits(h.n_qubits);
+  const std::size_t D = std::size_t{1} << h.n_qubits, M = 2 * D;
+  std::vector<double> a(M * M, 0.0);
+  for (const auto& t : h.terms) {
+    std::uint64_t flip = 0, yz = 0;
+    unsigned ny = 0;
+    for (const auto& [q, ax] : t.axes) {
+      const std::uint64_t bit = std::uint64_t{1} << (h.n_qubits - 1 - q);
+      if (ax == PauliAxis::X || ax == PauliAxis::Y) flip |= bit;
+      if (ax == PauliAxis::Y || ax == PauliAxis::Z) yz |= bit;
+      if (ax == PauliAxis::Y) ++ny;
+    }
+    static const std::complex<double> base_tab[4] = {{1, 0}, {0, -1}, {-1, 0}, {0, 1}};
+    const std::complex<double> cb = t.coefficient * base_tab[ny % 4];
+    for (std::size_t i = 0; i < D; ++i) {
+      const std::complex<double> v = (__builtin_popcountll(i & yz) & 1) ? -cb : cb;
+      const std::size_t j = i ^ flip;
+      a[i * M + j] += v.real();
+      a[(i + D) * M + (j + D)] += v.real();
+      a[i * M + (j + D)] -= v.imag();
+      a[(i + D) * M + j] += v.imag();
+    }
+  }
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (std::size_t i = 0; i < M; ++i)
+      for (std::size_t j = i + 1; j < M; ++j) off += a[i * M + j] * a[i * M + j];
+    if (off < 1e-30) break;
+    for (std::size_t p = 0; p < M; ++p)
+      for (std::size_t q = p + 1; q < M; ++q) {
+        const double apq = a[p * M + q];
+        if (std::abs(apq) < 1e-300) continue;
+        const double theta = (a[q * M + q] - a[p * M + p]) / (2.0 * apq);
+        const double tt = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(tt * tt + 1.0), s = tt * c;
+        for (std::size_t k = 0; k < M; ++k) {
+          const double akp = a[k * M + p], akq = a[k * M + q];
+          a[k * M + p] = c * akp - s * akq;
+          a[k * M + q] = s * akp + c * akq;
+        }
+        for (std::size_t k = 0; k < M; ++k) {
+          const double apk = a[p * M + k], aqk = a[q * M + k];
+          a[p * M + k] = c * apk - s * aqk;
+          a[q * M + k] = s * apk + c * aqk;
+        }
+      }
+  }
+  double e0 = a[0];
+  for (std::size_t i = 1; i < M; ++i) e0 = std::min(e0, a[i * M + i]);
+  return e0;
+}
+
 // ------------------------------------------------------------ statevector
 // statevector.hpp:33-51 (host value type, as in the reference)
 struct StateVector {
@@ -519,6 +613,8 @@ struct ScalingConfig {  // sweep.hpp:237-249
   bool z_sum_mode = false;
   double theta_init = 0.1;
   bool force = false;
+  bool adjoint = false;  // extension: adjoint gradients instead of parameter shift
+  int device = 0;
 };
 
 struct ScalingRecord {  // sweep.hpp:251-257
@@ -534,7 +630,7 @@ inline std::vector<ScalingRecord> run_scaling_study(const ScalingConfig& config)
   vqf_scaling_config c{config.qubits.data(), static_cast<std::uint32_t>(config.qubits.size()), config.layers,
                        config.iterations, config.learning_rate, config.coupling, config.field,
                        config.z_sum_mode ? 1 : 0, config.theta_init, config.force ? 1 : 0,
-                       VQF_GRAD_PARAMETER_SHIFT, 0};
+                       config.adjoint ? VQF_GRAD_ADJOINT : VQF_GRAD_PARAMETER_SHIFT, config.device};
   std::vector<vqf_scaling_record> recs(config.qubits.size());
   detail::check(vqf_run_scaling_study(&c, recs.data()));
   std::vector<ScalingRecord> out;
