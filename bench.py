@@ -254,7 +254,7 @@ def run_ours(args, rank, world, local_rank):
     rep = plan.read()
 
     # ---- e2e: public C ABI with host buffers (H2D + kernel + D2H per step)
-    buf = V.SweepBuffers(V.SweepConfig(chunk_index=rank, n_chunks=world), trajectories=True)
+    buf = V.SweepBuffers(V.SweepConfig(chunk_index=rank, n_chunks=world), trajectories=False)
     for _ in range(max(args.warmup, 3)):
         buf.run()
     barrier()

@@ -152,6 +152,42 @@ __host__ __device__ inline double one_e_term_pf(const ChemConsts& k, const PairF
   return k.coef[x] * k.coef[y] * prim;
 }
 
+// Distinct pair factors: pair_factor(ij, xy) depends on (ij, x, y) only
+// through operands that are exactly symmetric under a -> b, so same-centre
+// pairs (ij = 00, 11) with swapped primitives and the two orientations of the
+// mixed pair (01 xy == 10 yx) are the same value: 6 + 6 + 9 = 21 distinct.
+__host__ __device__ inline int pf_uid(int ij, int x, int y) {
+  if (ij == 0 || ij == 3) {
+    const int a = x < y ? x : y, b = x < y ? y : x;
+    return (ij ? 6 : 0) + a * (5 - a) / 2 + b;
+  }
+  return 12 + (ij == 1 ? x * 3 + y : y * 3 + x);
+}
+// Index of the unordered pair (u <= v) of distinct pair factors, 0..230.
+__host__ __device__ inline int pf_pair(int u, int v) { return u * 21 - u * (u - 1) / 2 + (v - u); }
+
+// eri_prim's prefactor (chem.hpp:177): symmetric in (p, q) bitwise.
+__host__ __device__ inline double eri_pref(const ChemConsts& k, double p, double q) {
+  return 2.0 * k.pow_pi_25 / (p * q * sqrt(p + q));
+}
+// eri_term_pf with the prefactor and Boys value looked up (same operation
+// order from there on).
+__host__ __device__ inline double eri_term_tab(const ChemConsts& k, const PairFactor& bra, const PairFactor& ket,
+                                               double pref, double boys, int x, int y, int z, int w) {
+  const double prim = pref * bra.E * ket.E * boys;
+  return k.coef[x] * k.coef[y] * k.coef[z] * k.coef[w] * prim;
+}
+// one_e_term_pf with the nuclear-attraction Boys value looked up.
+__host__ __device__ inline double one_e_term_tab(const ChemConsts& k, const PairFactor& f, int xy, int which,
+                                                 double boys) {
+  const int x = xy / 3, y = xy % 3;
+  double prim;
+  if (which == 0) prim = k.pow_pi_p15[x][y] * f.E;
+  else if (which == 1) prim = f.mu * (3.0 - 2.0 * f.mu * f.d2) * k.pow_pi_p15[x][y] * f.E;
+  else prim = -2.0 * kPi / f.p * f.E * boys;
+  return k.coef[x] * k.coef[y] * prim;
+}
+
 struct AoInts {
   double S[2][2], T[2][2], V[2][2], eri[16];
 };

@@ -10,7 +10,9 @@
 #include <chrono>
 #include <cstring>
 #include <iostream>
+#include <limits>
 #include <memory>
+#include <mutex>
 #include <thread>
 
 #include "adjoint.cuh"
@@ -129,6 +131,11 @@ struct SmallJob {
   // inputs
   std::vector<double> bonds;          // PES
   std::vector<int32_t> status_in;     // PES: kStatusBond pre-marked
+  // PES grid mode: bonds [grid_first, grid_first + batch) of
+  // bond_grid(grid_min, grid_max, grid_n) are generated and range-checked on
+  // the device, Adam tables come from the device cache: no H2D copy at all
+  int32_t grid_n = 0, grid_first = 0;
+  double grid_min = 0.0, grid_max = 0.0;
   std::vector<MaskTerm> terms;        // generic
   std::vector<uint32_t> term_off;     // generic
   std::vector<double> init_theta;     // optional, batch * P
@@ -138,6 +145,81 @@ struct SmallJob {
   std::vector<int32_t> iters, converged, status, err_iter, ham_keys, ham_count;
   double device_seconds = 0.0;
 };
+
+// -DVQF_HOST_TIMING: host-side checkpoints of the run_sweep path (scripts/host_timing.sh)
+#ifdef VQF_HOST_TIMING
+struct HostMarks {
+  std::chrono::steady_clock::time_point t[16];
+  const char* name[16];
+  int n = 0;
+  void mark(const char* what) {
+    if (n < 16) {
+      t[n] = std::chrono::steady_clock::now();
+      name[n++] = what;
+    }
+  }
+  void dump() {
+    for (int i = 1; i < n; ++i)
+      std::fprintf(stderr, "HOST %-14s %8.2f us\n", name[i],
+                   std::chrono::duration<double, std::micro>(t[i] - t[i - 1]).count());
+    n = 0;
+  }
+};
+static HostMarks g_marks;
+#define HMARK(x) g_marks.mark(x)
+#define HDUMP() g_marks.dump()
+#else
+#define HMARK(x)
+#define HDUMP()
+#endif
+
+// Adam bias-correction tables (2T std::pow calls, ~20 us for T = 200) are a
+// function of (beta1, beta2, T) only: computed once per distinct triple.
+void cached_bias_tables(const vqf_adam_config& c, int32_t T, std::vector<double>& bc1, std::vector<double>& bc2) {
+  struct Entry {
+    double b1, b2;
+    int32_t T;
+    std::vector<double> bc1, bc2;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Entry& e : cache)
+    if (e.b1 == c.beta1 && e.b2 == c.beta2 && e.T == T) {
+      bc1 = e.bc1;
+      bc2 = e.bc2;
+      return;
+    }
+  host::bias_tables(c, T, bc1, bc2);
+  if (cache.size() >= 8) cache.erase(cache.begin());
+  cache.push_back(Entry{c.beta1, c.beta2, T, bc1, bc2});
+}
+
+// Device-resident copy of the bias tables per (device, beta1, beta2, T),
+// uploaded once; null when the cache is full (the caller stages them).
+const double* device_bias_tables(int device, const vqf_adam_config& c, int32_t T) {
+  struct Entry {
+    int device;
+    double b1, b2;
+    int32_t T;
+    double* ptr;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Entry& e : cache)
+    if (e.device == device && e.b1 == c.beta1 && e.b2 == c.beta2 && e.T == T) return e.ptr;
+  if (cache.size() >= 64) return nullptr;
+  std::vector<double> bc1, bc2;
+  cached_bias_tables(c, T, bc1, bc2);
+  const size_t n = bc1.size();
+  double* d = nullptr;
+  VQF_CUDA(cudaMalloc(&d, 2 * n * sizeof(double)));
+  VQF_CUDA(cudaMemcpy(d, bc1.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  VQF_CUDA(cudaMemcpy(d + n, bc2.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  cache.push_back(Entry{device, c.beta1, c.beta2, T, d});
+  return d;
+}
 
 // Device layout of one small-engine job: inputs, then fixed-size outputs,
 // then the trajectories (last, so a caller that does not want them skips
@@ -152,7 +234,7 @@ struct SmallStage {
     const uint32_t B = j.batch, P = j.P;
     const int32_t T = j.adam.max_iterations;
     stride = static_cast<uint32_t>(std::max(T, 0)) + 1;
-    host::bias_tables(j.adam, T, bc1, bc2);
+    cached_bias_tables(j.adam, T, bc1, bc2);
     Carver c;
     o_bc1 = c.take<double>(bc1.size());
     o_bc2 = c.take<double>(bc2.size());
@@ -193,7 +275,11 @@ struct SmallStage {
       std::memcpy(pin + o_status, j.status_in.data(), B * sizeof(int32_t));
   }
 
-  SmallParams params(const SmallJob& j, unsigned char* dev, int device) const {
+  // out_host: when set, the fixed-size outputs (status .. hf) are written by
+  // the kernel straight into this mapped pinned buffer (zero-copy; no D2H
+  // copy and its DMA latency); trajectories stay in device memory.
+  SmallParams params(const SmallJob& j, unsigned char* dev, int device, unsigned char* out_host = nullptr) const {
+    unsigned char* out = out_host ? out_host : dev;
     SmallParams p{};
     p.n_qubits = j.n_qubits;
     p.ansatz_kind = j.kind;
@@ -209,26 +295,37 @@ struct SmallStage {
     p.bc1 = reinterpret_cast<const double*>(dev + o_bc1);
     p.bc2 = reinterpret_cast<const double*>(dev + o_bc2);
     p.bonds = reinterpret_cast<const double*>(dev + o_bonds);
+    if (j.grid_n > 0) {
+      const double* tab = device_bias_tables(device, j.adam, j.adam.max_iterations);
+      if (tab != nullptr) {
+        p.bc1 = tab;
+        p.bc2 = tab + bc1.size();
+        p.grid_n = j.grid_n;
+        p.grid_first = j.grid_first;
+        p.grid_min = j.grid_min;
+        p.grid_max = j.grid_max;
+      }
+    }
     p.chem = chem::consts();
     p.jw = j.pes ? chem::jw_table_device(device) : nullptr;
     p.terms = reinterpret_cast<const MaskTerm*>(dev + o_terms);
     p.term_off = reinterpret_cast<const uint32_t*>(dev + o_toff);
     p.init_theta = j.init_theta.empty() ? nullptr : reinterpret_cast<const double*>(dev + o_init);
-    p.energy = reinterpret_cast<double*>(dev + o_energy);
-    p.theta_out = reinterpret_cast<double*>(dev + o_theta);
+    p.energy = reinterpret_cast<double*>(out + o_energy);
+    p.theta_out = reinterpret_cast<double*>(out + o_theta);
     p.traj = reinterpret_cast<double*>(dev + o_traj);
     p.traj_stride = static_cast<int32_t>(stride);
-    p.iters = reinterpret_cast<int32_t*>(dev + o_iters);
-    p.converged = reinterpret_cast<int32_t*>(dev + o_conv);
-    p.status = reinterpret_cast<int32_t*>(dev + o_status);
-    p.err_val = reinterpret_cast<double*>(dev + o_errv);
-    p.err_iter = reinterpret_cast<int32_t*>(dev + o_erri);
-    p.err_theta = reinterpret_cast<double*>(dev + o_errt);
+    p.iters = reinterpret_cast<int32_t*>(out + o_iters);
+    p.converged = reinterpret_cast<int32_t*>(out + o_conv);
+    p.status = reinterpret_cast<int32_t*>(out + o_status);
+    p.err_val = reinterpret_cast<double*>(out + o_errv);
+    p.err_iter = reinterpret_cast<int32_t*>(out + o_erri);
+    p.err_theta = reinterpret_cast<double*>(out + o_errt);
     if (j.want_ham) {
-      p.ham_keys = reinterpret_cast<int32_t*>(dev + o_hk);
-      p.ham_coeffs = reinterpret_cast<double*>(dev + o_hc);
-      p.ham_count = reinterpret_cast<int32_t*>(dev + o_hn);
-      p.hf_out = reinterpret_cast<double*>(dev + o_hf);
+      p.ham_keys = reinterpret_cast<int32_t*>(out + o_hk);
+      p.ham_coeffs = reinterpret_cast<double*>(out + o_hc);
+      p.ham_count = reinterpret_cast<int32_t*>(out + o_hn);
+      p.hf_out = reinterpret_cast<double*>(out + o_hf);
     }
     return p;
   }
@@ -266,24 +363,32 @@ struct SmallStage {
 void run_small(SmallJob& j, int device, bool want_traj = true, size_t* h2d = nullptr, size_t* d2h = nullptr) {
   Workspace& ws = workspace(device);
   VQF_CUDA(cudaSetDevice(device));
+  HMARK("setdevice");
   const SmallStage st(j);
   ws.reserve(st.total, st.total);
   auto* pin = static_cast<unsigned char*>(ws.pin);
   auto* dev = static_cast<unsigned char*>(ws.dev);
   st.pack(j, pin);
-  const SmallParams p = st.params(j, dev, device);
-  VQF_CUDA(cudaMemcpyAsync(dev, pin, st.in_end, cudaMemcpyHostToDevice, ws.stream));
+  const SmallParams p = st.params(j, dev, device, pin);
+  const bool staged = p.grid_n == 0;  // grid mode needs no inputs from the host
+  HMARK("stage+params");
+  if (staged) VQF_CUDA(cudaMemcpyAsync(dev, pin, st.in_end, cudaMemcpyHostToDevice, ws.stream));
   VQF_CUDA(cudaEventRecord(ws.ev0, ws.stream));
   launch_vqe_small(p, j.batch, j.pes, ws.stream);
   VQF_CUDA(cudaEventRecord(ws.ev1, ws.stream));
-  VQF_CUDA(cudaMemcpyAsync(pin + st.o_status, dev + st.o_status, st.d2h_bytes(want_traj), cudaMemcpyDeviceToHost,
-                           ws.stream));
+  HMARK("launch");
+  if (want_traj)  // outputs arrive zero-copy; only trajectories need a copy
+    VQF_CUDA(cudaMemcpyAsync(pin + st.o_traj, dev + st.o_traj, st.total - st.o_traj, cudaMemcpyDeviceToHost,
+                             ws.stream));
+  HMARK("d2h issue");
   VQF_CUDA(cudaStreamSynchronize(ws.stream));
+  HMARK("sync");
   float ms = 0.f;
   VQF_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
   j.device_seconds = ms * 1e-3;
   st.unpack(j, pin, want_traj);
-  if (h2d) *h2d = st.in_end;
+  HMARK("unpack");
+  if (h2d) *h2d = staged ? st.in_end : 0;
   if (d2h) *d2h = st.d2h_bytes(want_traj);
 }
 
@@ -637,8 +742,8 @@ void pes_fill(const SmallJob& j, const vqf_sweep_config& cfg, const std::vector<
   for (uint64_t i = b0; i < b1; ++i) {
     const uint32_t b = static_cast<uint32_t>(i - b0);
     rep->bond_angstrom[i] = grid[i];
-    rep->energy_hartree[i] = std::nan("");
-    rep->theta_star[i] = std::nan("");
+    rep->energy_hartree[i] = std::numeric_limits<double>::quiet_NaN();
+    rep->theta_star[i] = std::numeric_limits<double>::quiet_NaN();
     rep->iterations[i] = 0;
     rep->ok[i] = 0;
     if (rep->wall_seconds) rep->wall_seconds[i] = j.device_seconds;
@@ -811,6 +916,7 @@ int vqf_run_sweep(const vqf_sweep_config* cfg, vqf_sweep_report* rep) {
     if (cfg == nullptr || rep == nullptr) throw_invalid("null argument");
     if (cfg->workers < 1) throw_invalid("workers must be >= 1");  // sweep.hpp:129
     const auto start = Clock::now();
+    HMARK("enter");
     const SweepSlice sl = sweep_slice(*cfg);
     const int W = cfg->workers;
     std::vector<uint64_t> wbe(2 * (size_t)W);
@@ -826,6 +932,10 @@ int vqf_run_sweep(const vqf_sweep_config* cfg, vqf_sweep_report* rep) {
         const auto tw = Clock::now();
         const uint64_t b0 = sl.lo + wbe[2 * w], b1 = sl.lo + wbe[2 * w + 1];
         SmallJob j = pes_job(*cfg, sl.grid, b0, b1, errors);
+        j.grid_n = cfg->n_points;  // bonds generated on the device (grid mode)
+        j.grid_first = static_cast<int32_t>(b0);
+        j.grid_min = cfg->d_min;
+        j.grid_max = cfg->d_max;
         if (j.batch > 0) {
           run_small(j, devices[w % devices.size()], rep->trajectories != nullptr, &h2d[w], &d2h[w]);
           dev_secs[w] = j.device_seconds;
@@ -846,7 +956,10 @@ int vqf_run_sweep(const vqf_sweep_config* cfg, vqf_sweep_report* rep) {
     }
     for (auto& f : fails)
       if (f) std::rethrow_exception(f);
+    HMARK("fill");
     pes_finish(sl, errors, rep);
+    HMARK("finish");
+    HDUMP();
     rep->device_seconds = *std::max_element(dev_secs.begin(), dev_secs.end());
     rep->h2d_bytes = 0;
     rep->d2h_bytes = 0;

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "chem.cuh"
+#include "fastmath.cuh"
 #include "vqe_small.cuh"
 
 namespace vqf {
@@ -63,6 +64,9 @@ struct Shared {
   int stop;
   // PES prologue scratch
   chem::PairFactor pf[36];
+  int pf_rep[21];                     // a pair-factor index per distinct pair factor
+  double eri_pref[231], eri_boys[231];  // per unordered pair of distinct pair factors
+  double nuc_boys[42];                // per distinct pair factor x nucleus
   double prim[1296];
   double prim1[144];
   chem::AoInts ints;
@@ -72,7 +76,17 @@ struct Shared {
   double integ[20];  // hmo (4) then physicist eri_mo (16)
   double kre[256], kim[256];
   int kflag[256];
+  int wlive[8], wbad[8];  // per-warp survivor counts / first non-Hermitian key
+  unsigned char cpart[chem::kNumContrib];  // Jordan-Wigner contribution part (0 re, 1 im)
 };
+
+#ifdef VQF_STAGE_CLOCKS
+__device__ __forceinline__ unsigned __mysmid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#endif
 
 __device__ __forceinline__ double2 shfl_xor2(double2 v, int m, int width) {
   v.x = __shfl_xor_sync(0xffffffffu, v.x, m, width);
@@ -243,6 +257,16 @@ __device__ int build_program(Shared& sh, int kind, int n, int layers) {
   return 0;
 }
 
+// Bond length of problem `prob`: staged, or bond_grid's own arithmetic.
+__device__ __forceinline__ double pes_bond(const SmallParams& p, int prob) {
+  if (p.grid_n <= 0) return p.bonds[prob];
+  const int i = p.grid_first + prob;
+  if (p.grid_n == 1) return p.grid_min;
+  if (i == p.grid_n - 1) return p.grid_max;
+  const double span = p.grid_max - p.grid_min;
+  return p.grid_min + span * static_cast<double>(i) / static_cast<double>(p.grid_n - 1);
+}
+
 // PES prologue: this CTA's H2 Hamiltonian as mask terms in smem (all
 // kPesThreads threads).  Sets sh.stop to kStatusScf / kStatusHermitian.
 //   1. 36 pair factors (one exp each) shared by every primitive;
@@ -253,24 +277,70 @@ __device__ int build_program(Shared& sh, int kind, int n, int layers) {
 __device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
   using namespace chem;
   const ChemConsts& k = p.chem;
-  const double d = p.bonds[prob] * kAngstromToBohr;
+  const double d = pes_bond(p, prob) * kAngstromToBohr;
 #ifdef VQF_STAGE_CLOCKS
   long long t_start = clock64(), t_pf, t_prim, t_sum, t_scf, t_mo, t_jw;
 #endif
-  for (int idx = threadIdx.x; idx < 36; idx += blockDim.x) sh.pf[idx] = pair_factor(k, d, idx / 9, idx % 9);
+  // The Jordan-Wigner contribution map is bond-independent: issue its loads
+  // now so their latency hides under the integral work.
+  const JwTable& jw = *p.jw;
+  constexpr int kContribPerThread = (kNumContrib + kPesThreads - 1) / kPesThreads;
+  int c_slot[kContribPerThread], c_part[kContribPerThread];
+  double c_coef[kContribPerThread];
+#pragma unroll
+  for (int u = 0; u < kContribPerThread; ++u) {
+    const int e = threadIdx.x + u * kPesThreads;
+    const bool in = e < kNumContrib;
+    c_slot[u] = in ? jw.slot[e] : 0;
+    c_part[u] = in ? jw.part[e] : 0;
+    c_coef[u] = in ? jw.coef[e] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < 36; idx += blockDim.x) {
+    const int ij = idx / 9, x = (idx % 9) / 3, y = idx % 3;
+    sh.pf[idx] = pair_factor(k, d, ij, idx % 9);
+    if (ij == 1 || ((ij == 0 || ij == 3) && x <= y)) sh.pf_rep[pf_uid(ij, x, y)] = idx;
+  }
   __syncthreads();
 #ifdef VQF_STAGE_CLOCKS
   t_pf = clock64();
 #endif
+  // The transcendental part of every primitive (Boys function, ERI
+  // prefactor) depends on its pair factors only through values that are
+  // exactly symmetric under bra <-> ket and under swapping the two
+  // primitives of a same-centre pair, so it is evaluated once per unordered
+  // pair of the 21 distinct pair factors (231 + 42 nuclear instead of
+  // 1296 + 72) - bitwise the values eri_prim / nuclear_prim compute.
+  for (int idx = threadIdx.x; idx < 441 + 42; idx += blockDim.x) {
+    if (idx < 441) {
+      const int u = idx / 21, v = idx % 21;
+      if (u <= v) {
+        const PairFactor& a = sh.pf[sh.pf_rep[u]];
+        const PairFactor& b = sh.pf[sh.pf_rep[v]];
+        const int pi = pf_pair(u, v);
+        sh.eri_pref[pi] = eri_pref(k, a.p, b.p);
+        sh.eri_boys[pi] = boys_f0(a.p * b.p / (a.p + b.p) * d2z(a.P, b.P));
+      }
+    } else {
+      const int o = idx - 441, u = o >> 1;
+      const PairFactor& f = sh.pf[sh.pf_rep[u]];
+      sh.nuc_boys[o] = boys_f0(f.p * d2z(f.P, (o & 1) ? d : 0.0));
+    }
+  }
+  __syncthreads();
   constexpr int kOne = 36 * 4;  // S, T, V(nucleus 0), V(nucleus 1) per (ij, xy)
   for (int idx = threadIdx.x; idx < 1296 + kOne; idx += blockDim.x) {
     if (idx < 1296) {
       const int ijkl = idx / 81, r = idx % 81;
       const int x = r / 27, y = (r / 9) % 3, z = (r / 3) % 3, w = r % 3;
-      sh.prim[idx] = eri_term_pf(k, sh.pf[(ijkl >> 2) * 9 + x * 3 + y], sh.pf[(ijkl & 3) * 9 + z * 3 + w], x, y, z, w);
+      const int bra = (ijkl >> 2) * 9 + x * 3 + y, ket = (ijkl & 3) * 9 + z * 3 + w;
+      const int u = pf_uid(ijkl >> 2, x, y), v = pf_uid(ijkl & 3, z, w);
+      const int pi = u <= v ? pf_pair(u, v) : pf_pair(v, u);
+      sh.prim[idx] = eri_term_tab(k, sh.pf[bra], sh.pf[ket], sh.eri_pref[pi], sh.eri_boys[pi], x, y, z, w);
     } else {
       const int o = idx - 1296, which = o / 36, e = o % 36;
-      sh.prim1[o] = one_e_term_pf(k, sh.pf[e], e % 9, which < 2 ? which : 2, which == 3 ? d : 0.0);
+      const int ij = e / 9, x = (e % 9) / 3, y = e % 3;
+      const double nb = which >= 2 ? sh.nuc_boys[2 * pf_uid(ij, x, y) + (which - 2)] : 0.0;
+      sh.prim1[o] = one_e_term_tab(k, sh.pf[e], e % 9, which < 2 ? which : 2, nb);
     }
   }
   __syncthreads();
@@ -321,12 +391,40 @@ __device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
 #endif
   // Jordan-Wigner: per Pauli string, its contributions in generation order
   // (canonicalize merges in order of first appearance, pauli.hpp:180-190).
-  const JwTable& jw = *p.jw;
+  // contribution values, block-parallel, staged in smem (sh.prim is free
+  // again); then each string sums its own run sequentially, in generation
+  // order, from smem
+  static_assert(kNumContrib <= 1296, "contribution values reuse sh.prim");
+#pragma unroll
+  for (int u = 0; u < kContribPerThread; ++u) {
+    const int e = threadIdx.x + u * kPesThreads;
+    if (e < kNumContrib) {
+      sh.prim[e] = c_slot[u] < 0 ? sh.hf.e_nuc : c_coef[u] * sh.integ[c_slot[u]];
+      sh.cpart[e] = static_cast<unsigned char>(c_part[u]);
+    }
+  }
+  __syncthreads();
   for (int t = threadIdx.x; t < jw.n_keys; t += blockDim.x) {
     double re = 0.0, im = 0.0;
-    for (int e = jw.start[t]; e < jw.start[t + 1]; ++e) {
-      const double v = jw.slot[e] < 0 ? sh.hf.e_nuc : jw.coef[e] * sh.integ[jw.slot[e]];
-      if (jw.part[e]) im += v;
+    const int e1 = jw.start[t + 1];
+    int e = jw.start[t];
+    for (; e + 4 <= e1; e += 4) {  // loads batched ahead of the ordered adds
+      double v[4];
+      unsigned char pt[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        v[u] = sh.prim[e + u];
+        pt[u] = sh.cpart[e + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (pt[u]) im += v[u];
+        else re += v[u];
+      }
+    }
+    for (; e < e1; ++e) {
+      const double v = sh.prim[e];
+      if (sh.cpart[e]) im += v;
       else re += v;
     }
     sh.kre[t] = re;
@@ -336,17 +434,35 @@ __device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
     sh.kflag[t] = hypot(re, im) < 1e-12 ? 0 : (fabs(im) >= 1e-10 ? 2 : 1);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    // compaction in canonical order (the table order); the first
-    // non-Hermitian survivor raises, as the reference's check loop does
-    int nt = 0;
-    for (int t = 0; t < jw.n_keys; ++t) {
-      if (sh.kflag[t] == 0) continue;
-      if (sh.kflag[t] == 2) {
+  // Compaction in canonical order (the table order), block-parallel: a
+  // survivor's slot is the number of survivors before it (warp ballots +
+  // per-warp counts).  The first non-Hermitian survivor raises, as the
+  // reference's check loop does (pauli.hpp:207-214).
+  static_assert(kPesThreads >= 256, "one thread per Jordan-Wigner key");
+  {
+    const int t = threadIdx.x, w = t >> 5, ln = t & 31;
+    const int flag = t < jw.n_keys ? sh.kflag[t] : 0;
+    const unsigned live = __ballot_sync(0xffffffffu, flag == 1), bad = __ballot_sync(0xffffffffu, flag == 2);
+    if (w < 8 && ln == 0) {
+      sh.wlive[w] = __popc(live);
+      sh.wbad[w] = bad ? w * 32 + __ffs(bad) - 1 : 1 << 30;
+    }
+    __syncthreads();
+    int base = 0, total = 0, first_bad = 1 << 30;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      base += u < w ? sh.wlive[u] : 0;
+      total += sh.wlive[u];
+      first_bad = min(first_bad, sh.wbad[u]);
+    }
+    if (first_bad < (1 << 30)) {
+      if (t == 0) {
         sh.stop = kStatusHermitian;
-        p.err_val[prob] = sh.kim[t];
-        break;
+        p.err_val[prob] = sh.kim[first_bad];
+        sh.n_terms = 0;
       }
+    } else if (flag == 1) {
+      const int nt = base + __popc(live & ((1u << ln) - 1u));
       const int key = jw.keys[t], x = key & 15, z = key >> 4;
       uint64_t flip = 0, yz = 0;  // MSB-first: qubit q -> bit (3 - q)
       for (int q = 0; q < 4; ++q) {
@@ -365,9 +481,13 @@ __device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
         p.ham_keys[prob * 16 + nt] = key;
         p.ham_coeffs[prob * 16 + nt] = c;
       }
-      sh.terms[nt++] = mt;
+      sh.terms[nt] = mt;
     }
-    sh.n_terms = nt;
+    if (t == 0 && first_bad >= (1 << 30)) sh.n_terms = total;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nt = sh.n_terms;
 #ifdef VQF_STAGE_CLOCKS
     t_jw = clock64();
     if (prob == 0)
@@ -400,7 +520,14 @@ __device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int p
   }
   __syncthreads();
   if (PES) {
-    if (p.status[prob] != 0) return false;  // rejected on the host (bond out of range)
+    if (p.grid_n > 0) {  // grid mode: the range check (chem.hpp:33-34) is ours
+      const double b = pes_bond(p, prob);
+      const int32_t st = (b >= chem::kMinBond && b <= chem::kMaxBond) ? 0 : kStatusBond;
+      if (threadIdx.x == 0) p.status[prob] = st;
+      if (st != 0) return false;
+    } else if (p.status[prob] != 0) {
+      return false;  // rejected on the host (bond out of range)
+    }
     build_h2_device(sh, p, prob);
     if (sh.stop) {
       if (threadIdx.x == 0) p.status[prob] = sh.stop;
@@ -429,7 +556,15 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
   Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
   double* bc = reinterpret_cast<double*>(smem_raw + sizeof(Shared));
   const int prob = blockIdx.x;
+#ifdef VQF_STAGE_CLOCKS
+  unsigned long long g_entry;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
+#endif
   if (!prologue<PES>(sh, p, prob, bc, 16)) return;
+#ifdef VQF_STAGE_CLOCKS
+  unsigned long long g_loop;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_loop));
+#endif
   const int lane = threadIdx.x & 31, seg = lane >> 3, sl = lane & 7;
   const int circ = seg < 3 ? seg : 0;
   const int G = sh.n_groups;
@@ -449,6 +584,11 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
   double* traj = p.traj + (size_t)prob * p.traj_stride;
   double th = p.init_theta ? p.init_theta[prob] : 0.0, m = 0.0, v = 0.0;
   int iters = 0, converged = 0;
+  // basis_state(4, {1,1,0,0}) (index 12 = slot 1 of sl 4) and its
+  // DoubleExcitation partners (index i <-> i ^ 15) are loop-invariant: the
+  // exchange happens once, each iteration only rotates.
+  const double2 in0 = make_double2(0.0, 0.0), in1 = make_double2(sl == 4 ? 1.0 : 0.0, 0.0);
+  const double2 q0 = shfl_xor2(in1, 7, 8), q1 = shfl_xor2(in0, 7, 8);
 #ifdef VQF_STAGE_CLOCKS
   long long stamps[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #define STAMP(i) if (iter == 100) stamps[i] = clock64();
@@ -457,43 +597,49 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
 #endif
   for (int iter = 0; iter <= p.max_iterations; ++iter) {
     const bool final_eval = (iter == p.max_iterations);
+#ifdef VQF_STAGE_CLOCKS
+    if (iter == 101) stamps[7] = clock64();
+#endif
     STAMP(0)
     // gradient(): shifted[k] = theta[k] +- pi/2 (vqe.hpp:119-121)
     double t = th;
     if (circ == 1) t = th + kShift;
     if (circ == 2) t = th - kShift;
     double sn, cs;
-    sincos(0.5 * t, &sn, &cs);
+    sincos_short(0.5 * t, &sn, &cs);
     STAMP(1)
-    // basis_state(4, {1,1,0,0}): index 12 = slot 1 of sl 4
-    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(sl == 4 ? 1.0 : 0.0, 0.0);
-    // DoubleExcitation(0,1,2,3): partner of index i is i ^ 15
-    const double2 q0 = shfl_xor2(a1, 7, 8), q1 = shfl_xor2(a0, 7, 8);
-    if (sl == 4) a1 = rot_lo(cs, sn, a1, q1);  // index 12 (|1100>)
-    if (sl == 3) a0 = rot_hi(cs, sn, q0, a0);  // index 3  (|0011>)
+    // DoubleExcitation(0,1,2,3) on |1100>: rotate indices 12 and 3
+    const double2 r12 = make_double2(fma(cs, in1.x, -sn * q1.x), fma(cs, in1.y, -sn * q1.y));
+    const double2 r3 = make_double2(fma(sn, q0.x, cs * in0.x), fma(sn, q0.y, cs * in0.y));
+    const double2 a1 = sl == 4 ? r12 : in1, a0 = sl == 3 ? r3 : in0;
     STAMP(2)
-    // expectation: sum_g O_g(i) conj(psi_i) psi_{i ^ f_g}, group terms
-    // formed independently, then added in group order
+    // expectation: sum_g O_g(i) conj(psi_i) psi_{i ^ f_g}.  Group 0 is the
+    // diagonal (flip 0, build_tables puts it first): O_0(i) |psi_i|^2 with no
+    // exchange; the flip groups exchange partners by shuffle.  Group terms
+    // are formed independently, then added in group order.
     double2 acc = make_double2(0.0, 0.0);
     if (G <= kRegG) {
       double2 term[kRegG];
+      {
+        const double n0 = fma(a0.x, a0.x, a0.y * a0.y), n1 = fma(a1.x, a1.x, a1.y * a1.y);
+        term[0] = make_double2(fma(o0_r[0].x, n0, o1_r[0].x * n1), fma(o0_r[0].y, n0, o1_r[0].y * n1));
+      }
 #pragma unroll
-      for (int g = 0; g < kRegG; ++g) {
+      for (int g = 1; g < kRegG; ++g) {
+        term[g] = make_double2(0.0, 0.0);
+        if (g >= G) continue;  // warp-uniform
         double2 r0 = fs_r[g] ? a1 : a0, r1 = fs_r[g] ? a0 : a1;
         if (fl_r[g]) {  // warp-uniform
           r0 = shfl_xor2(r0, fl_r[g], 8);
           r1 = shfl_xor2(r1, fl_r[g], 8);
         }
-        const double v0r = a0.x * r0.x + a0.y * r0.y, v0i = a0.x * r0.y - a0.y * r0.x;
-        const double v1r = a1.x * r1.x + a1.y * r1.y, v1i = a1.x * r1.y - a1.y * r1.x;
-        term[g].x = (o0_r[g].x * v0r - o0_r[g].y * v0i) + (o1_r[g].x * v1r - o1_r[g].y * v1i);
-        term[g].y = (o0_r[g].x * v0i + o0_r[g].y * v0r) + (o1_r[g].x * v1i + o1_r[g].y * v1r);
+        const double v0r = fma(a0.x, r0.x, a0.y * r0.y), v0i = fma(a0.x, r0.y, -a0.y * r0.x);
+        const double v1r = fma(a1.x, r1.x, a1.y * r1.y), v1i = fma(a1.x, r1.y, -a1.y * r1.x);
+        term[g].x = fma(o0_r[g].x, v0r, fma(-o0_r[g].y, v0i, fma(o1_r[g].x, v1r, -o1_r[g].y * v1i)));
+        term[g].y = fma(o0_r[g].x, v0i, fma(o0_r[g].y, v0r, fma(o1_r[g].x, v1i, o1_r[g].y * v1r)));
       }
-#pragma unroll
-      for (int g = 0; g < kRegG; ++g) {
-        acc.x += term[g].x;
-        acc.y += term[g].y;
-      }
+      acc.x = (term[0].x + term[1].x) + (term[2].x + term[3].x);
+      acc.y = (term[0].y + term[1].y) + (term[2].y + term[3].y);
     } else {
       for (int g = 0; g < G; ++g) {
         const int f = sh.flip[g], fl = f & 7;
@@ -555,7 +701,7 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
     const double vk = p.beta2 * v + (1.0 - p.beta2) * g * g;
     const double m_hat = mk * bc[2 * iter];
     const double v_hat = vk * bc[2 * iter + 1];
-    th = th - p.lr * m_hat / (sqrt(v_hat) + p.eps);
+    th = th - adam_delta(p.lr, m_hat, v_hat, p.eps);
     m = mk;
     v = vk;
     iters = iter + 1;
@@ -563,9 +709,16 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
   }
 #ifdef VQF_STAGE_CLOCKS
   if (prob == 0 && lane == 0)
-    printf("STAGES angle=%lld de=%lld groups=%lld reduce+bcast=%lld checks+grad=%lld adam=%lld total=%lld\n",
+    printf("STAGES angle=%lld de=%lld groups=%lld reduce+bcast=%lld checks+grad=%lld adam=%lld total=%lld "
+           "iteration=%lld\n",
            stamps[1] - stamps[0], stamps[2] - stamps[1], stamps[3] - stamps[2], stamps[4] - stamps[3],
-           stamps[5] - stamps[4], stamps[6] - stamps[5], stamps[6] - stamps[0]);
+           stamps[5] - stamps[4], stamps[6] - stamps[5], stamps[6] - stamps[0], stamps[7] - stamps[0]);
+  if (lane == 0) {
+    unsigned long long g_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+    printf("TIMELINE bond %d sm %u entry %llu prologue_ns %llu loop_ns %llu end %llu\n", prob,
+           static_cast<unsigned>(__mysmid()), g_entry, g_loop - g_entry, g_end - g_loop, g_end);
+  }
 #endif
   if (lane == 0) {
     p.iters[prob] = iters;
@@ -618,7 +771,7 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_vqe_warp(SmallParams
       if (j == 1) t = t + kShift;
       if (j == 2) t = t - kShift;
       double s, c;
-      sincos(0.5 * t, &s, &c);
+      sincos_short(0.5 * t, &s, &c);
       sh.cs[k][j] = make_double2(c, s);
     }
     __syncwarp();
@@ -704,7 +857,7 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_vqe_warp(SmallParams
         const double vk = p.beta2 * v_reg[r] + (1.0 - p.beta2) * g * g;
         const double m_hat = mk * b1;  // b1, b2 = 1 / (1 - beta^t)
         const double v_hat = vk * b2;
-        th_reg[r] = th_reg[r] - p.lr * m_hat / (sqrt(v_hat) + p.eps);
+        th_reg[r] = th_reg[r] - adam_delta(p.lr, m_hat, v_hat, p.eps);
         m_reg[r] = mk;
         v_reg[r] = vk;
         sh.theta[k] = th_reg[r];

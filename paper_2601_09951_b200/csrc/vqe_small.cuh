@@ -32,8 +32,12 @@ struct SmallParams {
   // generic mode: grouped-by-problem mask terms
   const MaskTerm* terms;
   const uint32_t* term_off;  // batch + 1
-  // PES mode
+  // PES mode: bonds[] (staged), or, when grid_n > 0, bond grid_first + b of
+  // bond_grid(grid_min, grid_max, grid_n) computed on device (sweep.hpp:68-85
+  // arithmetic, bitwise) with the range check done there too (no H2D copy)
   const double* bonds;
+  double grid_min, grid_max;
+  int32_t grid_n, grid_first;
   chem::ChemConsts chem;
   const chem::JwTable* jw;
   const double* init_theta;  // batch * P, or null (theta0 = 0)
@@ -44,7 +48,7 @@ struct SmallParams {
   int32_t traj_stride;
   int32_t* iters;
   int32_t* converged;
-  int32_t* status;  // in: 0 or kStatusBond (PES); out: status
+  int32_t* status;  // in: 0 or kStatusBond (staged PES); out: status
   double* err_val;
   int32_t* err_iter;
   double* err_theta;  // batch * P
