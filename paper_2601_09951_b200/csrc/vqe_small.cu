@@ -544,190 +544,253 @@ __device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int p
   return true;
 }
 
-// H2 fast path (n = 4, one parameter, 3 circuits): lanes 8c..8c+7 hold
-// circuit c with amplitude indices {sl, 8 + sl} (sl = lane & 7).  Every lane
-// carries theta / m / v and runs Adam itself (identical values in all lanes,
-// no broadcast), and computes the (cos, sin) of its own circuit's angle.
-// Exchanges per iteration: one DoubleExcitation shuffle, one shuffle per flip
-// group, a 3-level reduction and 3 energy shuffles.
-template <bool PES>
-__global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
-  double* bc = reinterpret_cast<double*>(smem_raw + sizeof(Shared));
-  const int prob = blockIdx.x;
-#ifdef VQF_STAGE_CLOCKS
-  unsigned long long g_entry;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
-#endif
-  if (!prologue<PES>(sh, p, prob, bc, 16)) return;
-#ifdef VQF_STAGE_CLOCKS
-  unsigned long long g_loop;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_loop));
-#endif
-  const int lane = threadIdx.x & 31, seg = lane >> 3, sl = lane & 7;
-  const int circ = seg < 3 ? seg : 0;
-  const int G = sh.n_groups;
-  // this lane's Hamiltonian table entries, in registers for G <= 4
-  constexpr int kRegG = 4;
-  int fl_r[kRegG], fs_r[kRegG];
-  double2 o0_r[kRegG], o1_r[kRegG];
-#pragma unroll
-  for (int g = 0; g < kRegG; ++g) {
-    const bool on = g < G;
-    const int f = on ? sh.flip[g] : 0;
-    fl_r[g] = f & 7;
-    fs_r[g] = f & 8;
-    o0_r[g] = on ? sh.tab[g * 16 + sl] : make_double2(0.0, 0.0);
-    o1_r[g] = on ? sh.tab[g * 16 + 8 + sl] : make_double2(0.0, 0.0);
+// Failure of checked_energy / gradient at iteration `iter` (vqe.hpp:213-229):
+// decoded off the hot path.
+__device__ __forceinline__ void h2_fail(const SmallParams& p, int prob, int iter, double th, double2 e0, double2 ep,
+                                     double2 em) {
+  int st;
+  double val = 0.0;
+  if (fabs(e0.y) >= 1e-10) {
+    st = kStatusImag;
+    val = e0.y;
+  } else if (!isfinite(e0.x)) {
+    st = kStatusNonFinite;
+  } else {
+    st = kStatusImag;
+    val = fabs(ep.y) >= 1e-10 ? ep.y : em.y;
   }
+  p.status[prob] = st;
+  p.err_val[prob] = val;
+  p.err_iter[prob] = iter;
+  p.err_theta[prob] = th;
+}
+
+// The three circuits of one H2 iteration, E(theta), E(theta + pi/2) and
+// E(theta - pi/2) (vqe.hpp:115-127), each complete on every lane.  Lanes
+// 8c..8c+7 hold circuit c with amplitude indices {sl, 8 + sl}.  REG: the
+// Hamiltonian's flip groups (<= 4) are in registers; else read from smem.
+struct H2Lane {
+  int sl, circ, G;
+  int fl[4], fs[4];
+  double2 o0[4], o1[4];
+  double2 in0, in1, q0, q1;  // |1100> and its DoubleExcitation partners
+};
+
+// own: this lane's circuit total (lane 0 holds E(theta)); ep / em: the two
+// shifted energies on every lane.
+template <bool REG, bool FAST>
+__device__ __forceinline__ void h2_energies(const Shared& sh, const H2Lane& L, double th, double2& own, double2& ep,
+                                            double2& em) {
+  // gradient(): shifted[k] = theta[k] +- pi/2 (vqe.hpp:119-121)
+  double t = th;
+  if (L.circ == 1) t = th + kShift;
+  if (L.circ == 2) t = th - kShift;
+  double sn, cs;
+  if (FAST) sincos_reduced(0.5 * t, &sn, &cs);
+  else sincos(0.5 * t, &sn, &cs);
+  // DoubleExcitation(0,1,2,3) on |1100>: rotate indices 12 and 3
+  const double2 r12 = make_double2(fma(cs, L.in1.x, -sn * L.q1.x), fma(cs, L.in1.y, -sn * L.q1.y));
+  const double2 r3 = make_double2(fma(sn, L.q0.x, cs * L.in0.x), fma(sn, L.q0.y, cs * L.in0.y));
+  const double2 a1 = L.sl == 4 ? r12 : L.in1, a0 = L.sl == 3 ? r3 : L.in0;
+  // expectation: sum_g O_g(i) conj(psi_i) psi_{i ^ f_g}.  Group 0 is the
+  // diagonal (flip 0, build_tables puts it first): O_0(i) |psi_i|^2 with no
+  // exchange; the flip groups exchange partners by shuffle.  Group terms
+  // are formed independently, then added in group order.
+  double2 acc;
+  if (REG) {
+    double2 term[4];
+    {
+      const double n0 = fma(a0.x, a0.x, a0.y * a0.y), n1 = fma(a1.x, a1.x, a1.y * a1.y);
+      term[0] = make_double2(fma(L.o0[0].x, n0, L.o1[0].x * n1), fma(L.o0[0].y, n0, L.o1[0].y * n1));
+    }
+#pragma unroll
+    for (int g = 1; g < 4; ++g) {
+      term[g] = make_double2(0.0, 0.0);
+      if (g >= L.G) continue;  // warp-uniform
+      double2 r0 = L.fs[g] ? a1 : a0, r1 = L.fs[g] ? a0 : a1;
+      if (L.fl[g]) {  // warp-uniform
+        r0 = shfl_xor2(r0, L.fl[g], 8);
+        r1 = shfl_xor2(r1, L.fl[g], 8);
+      }
+      const double v0r = fma(a0.x, r0.x, a0.y * r0.y), v0i = fma(a0.x, r0.y, -a0.y * r0.x);
+      const double v1r = fma(a1.x, r1.x, a1.y * r1.y), v1i = fma(a1.x, r1.y, -a1.y * r1.x);
+      term[g].x = fma(L.o0[g].x, v0r, fma(-L.o0[g].y, v0i, fma(L.o1[g].x, v1r, -L.o1[g].y * v1i)));
+      term[g].y = fma(L.o0[g].x, v0i, fma(L.o0[g].y, v0r, fma(L.o1[g].x, v1i, L.o1[g].y * v1r)));
+    }
+    acc.x = (term[0].x + term[1].x) + (term[2].x + term[3].x);
+    acc.y = (term[0].y + term[1].y) + (term[2].y + term[3].y);
+  } else {
+    acc = make_double2(0.0, 0.0);
+    for (int g = 0; g < L.G; ++g) {
+      const int f = sh.flip[g], fl = f & 7;
+      double2 r0 = (f & 8) ? a1 : a0, r1 = (f & 8) ? a0 : a1;
+      if (fl) {
+        r0 = shfl_xor2(r0, fl, 8);
+        r1 = shfl_xor2(r1, fl, 8);
+      }
+      const double2 o0 = sh.tab[g * 16 + L.sl], o1 = sh.tab[g * 16 + 8 + L.sl];
+      const double v0r = fma(a0.x, r0.x, a0.y * r0.y), v0i = fma(a0.x, r0.y, -a0.y * r0.x);
+      const double v1r = fma(a1.x, r1.x, a1.y * r1.y), v1i = fma(a1.x, r1.y, -a1.y * r1.x);
+      acc.x += fma(o0.x, v0r, fma(-o0.y, v0i, fma(o1.x, v1r, -o1.y * v1i)));
+      acc.y += fma(o0.x, v0i, fma(o0.y, v0r, fma(o1.x, v1i, o1.y * v1r)));
+    }
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, 8);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, 8);
+  }
+  own = acc;
+  ep = shfl2(acc, 8);
+  em = shfl2(acc, 16);
+}
+
+// One iteration of run_vqe's loop (vqe.hpp:225-243) on one warp: energies,
+// checks, trajectory, gradient, tolerance, Adam.  Every lane carries theta /
+// m / v and runs Adam itself (identical values in all lanes, no broadcast).
+// Returns 0 continue, 1 converged, 2 failed (status written), 3 theta left
+// the fast-trig range (FAST only; nothing written, redo with FAST = false).
+struct H2State {
+  double th, m, v;
+};
+
+template <bool REG, bool FAST>
+__device__ __forceinline__ int h2_step(const Shared& sh, const SmallParams& p, int prob, const double* bc,
+                                       const H2Lane& L, int iter, H2State& s, double tol, double* traj) {
+  const int lane = threadIdx.x & 31;
+  const bool range_bad = FAST && !(fabs(s.th) < kFastTrigTheta);  // warp-uniform
+  double2 own, ep, em;
+  h2_energies<REG, FAST>(sh, L, s.th, own, ep, em);
+  // checked_energy, then the gradient's two expectations (vqe.hpp:227-229):
+  // each lane checks its own circuit, one vote
+  const bool my_bad = range_bad || fabs(own.y) >= 1e-10 || (L.circ == 0 && !isfinite(own.x));
+  if (__any_sync(0xffffffffu, my_bad)) {
+    if (range_bad) return 3;
+    const double2 e0 = shfl2(own, 0);
+    if (lane == 0) h2_fail(p, prob, iter, s.th, e0, ep, em);
+    return 2;
+  }
+  if (lane == 0) traj[iter] = own.x;
+  const double g = 0.5 * (ep.x - em.x);
+  if (fabs(g) < tol) return 1;
+  // adam_step (vqe.hpp:152-174), t = iter + 1; the bias corrections are
+  // applied as host-computed reciprocals 1 / (1 - beta^t)
+  const double mk = p.beta1 * s.m + (1.0 - p.beta1) * g;
+  const double vk = p.beta2 * s.v + (1.0 - p.beta2) * g * g;
+  const double m_hat = mk * bc[2 * iter];
+  const double v_hat = vk * bc[2 * iter + 1];
+  s.th = s.th - adam_delta(p.lr, m_hat, v_hat, p.eps);
+  s.m = mk;
+  s.v = vk;
+  return 0;
+}
+
+// run_vqe's loop (vqe.hpp:225-247) for one bond: the fast-trig loop, and
+// the library-sincos continuation should theta ever leave its range.
+template <bool REG>
+__device__ __forceinline__ void h2_optimise(const Shared& sh, const SmallParams& p, int prob, const double* bc,
+                                            const H2Lane& L, unsigned long long g_entry, unsigned long long g_loop) {
+  const int lane = threadIdx.x & 31;
   double* traj = p.traj + (size_t)prob * p.traj_stride;
-  double th = p.init_theta ? p.init_theta[prob] : 0.0, m = 0.0, v = 0.0;
-  int iters = 0, converged = 0;
-  // basis_state(4, {1,1,0,0}) (index 12 = slot 1 of sl 4) and its
-  // DoubleExcitation partners (index i <-> i ^ 15) are loop-invariant: the
-  // exchange happens once, each iteration only rotates.
-  const double2 in0 = make_double2(0.0, 0.0), in1 = make_double2(sl == 4 ? 1.0 : 0.0, 0.0);
-  const double2 q0 = shfl_xor2(in1, 7, 8), q1 = shfl_xor2(in0, 7, 8);
+  H2State s{p.init_theta ? p.init_theta[prob] : 0.0, 0.0, 0.0};
+  const double tol = p.has_tol ? p.tol : -1.0;  // |g| < -1 never holds
+  const int T = p.max_iterations;
 #ifdef VQF_STAGE_CLOCKS
-  long long stamps[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#define STAMP(i) if (iter == 100) stamps[i] = clock64();
-#else
-#define STAMP(i)
+  long long c100 = 0, c101 = 0;
 #endif
-  for (int iter = 0; iter <= p.max_iterations; ++iter) {
-    const bool final_eval = (iter == p.max_iterations);
+  int iter = 0, rc = 0;
+  for (; iter < T; ++iter) {
 #ifdef VQF_STAGE_CLOCKS
-    if (iter == 101) stamps[7] = clock64();
+    if (iter == 100) c100 = clock64();
+    if (iter == 101) c101 = clock64();
 #endif
-    STAMP(0)
-    // gradient(): shifted[k] = theta[k] +- pi/2 (vqe.hpp:119-121)
-    double t = th;
-    if (circ == 1) t = th + kShift;
-    if (circ == 2) t = th - kShift;
-    double sn, cs;
-    sincos_short(0.5 * t, &sn, &cs);
-    STAMP(1)
-    // DoubleExcitation(0,1,2,3) on |1100>: rotate indices 12 and 3
-    const double2 r12 = make_double2(fma(cs, in1.x, -sn * q1.x), fma(cs, in1.y, -sn * q1.y));
-    const double2 r3 = make_double2(fma(sn, q0.x, cs * in0.x), fma(sn, q0.y, cs * in0.y));
-    const double2 a1 = sl == 4 ? r12 : in1, a0 = sl == 3 ? r3 : in0;
-    STAMP(2)
-    // expectation: sum_g O_g(i) conj(psi_i) psi_{i ^ f_g}.  Group 0 is the
-    // diagonal (flip 0, build_tables puts it first): O_0(i) |psi_i|^2 with no
-    // exchange; the flip groups exchange partners by shuffle.  Group terms
-    // are formed independently, then added in group order.
-    double2 acc = make_double2(0.0, 0.0);
-    if (G <= kRegG) {
-      double2 term[kRegG];
-      {
-        const double n0 = fma(a0.x, a0.x, a0.y * a0.y), n1 = fma(a1.x, a1.x, a1.y * a1.y);
-        term[0] = make_double2(fma(o0_r[0].x, n0, o1_r[0].x * n1), fma(o0_r[0].y, n0, o1_r[0].y * n1));
-      }
-#pragma unroll
-      for (int g = 1; g < kRegG; ++g) {
-        term[g] = make_double2(0.0, 0.0);
-        if (g >= G) continue;  // warp-uniform
-        double2 r0 = fs_r[g] ? a1 : a0, r1 = fs_r[g] ? a0 : a1;
-        if (fl_r[g]) {  // warp-uniform
-          r0 = shfl_xor2(r0, fl_r[g], 8);
-          r1 = shfl_xor2(r1, fl_r[g], 8);
-        }
-        const double v0r = fma(a0.x, r0.x, a0.y * r0.y), v0i = fma(a0.x, r0.y, -a0.y * r0.x);
-        const double v1r = fma(a1.x, r1.x, a1.y * r1.y), v1i = fma(a1.x, r1.y, -a1.y * r1.x);
-        term[g].x = fma(o0_r[g].x, v0r, fma(-o0_r[g].y, v0i, fma(o1_r[g].x, v1r, -o1_r[g].y * v1i)));
-        term[g].y = fma(o0_r[g].x, v0i, fma(o0_r[g].y, v0r, fma(o1_r[g].x, v1i, o1_r[g].y * v1r)));
-      }
-      acc.x = (term[0].x + term[1].x) + (term[2].x + term[3].x);
-      acc.y = (term[0].y + term[1].y) + (term[2].y + term[3].y);
-    } else {
-      for (int g = 0; g < G; ++g) {
-        const int f = sh.flip[g], fl = f & 7;
-        double2 r0 = (f & 8) ? a1 : a0, r1 = (f & 8) ? a0 : a1;
-        if (fl) {
-          r0 = shfl_xor2(r0, fl, 8);
-          r1 = shfl_xor2(r1, fl, 8);
-        }
-        const double2 o0 = sh.tab[g * 16 + sl], o1 = sh.tab[g * 16 + 8 + sl];
-        const double v0r = a0.x * r0.x + a0.y * r0.y, v0i = a0.x * r0.y - a0.y * r0.x;
-        const double v1r = a1.x * r1.x + a1.y * r1.y, v1i = a1.x * r1.y - a1.y * r1.x;
-        acc.x += (o0.x * v0r - o0.y * v0i) + (o1.x * v1r - o1.y * v1i);
-        acc.y += (o0.x * v0i + o0.y * v0r) + (o1.x * v1i + o1.y * v1r);
-      }
+    rc = h2_step<REG, true>(sh, p, prob, bc, L, iter, s, tol, traj);
+    if (rc != 0) break;
+  }
+  if (rc == 3) {
+    for (rc = 0; iter < T; ++iter) {
+      rc = h2_step<REG, false>(sh, p, prob, bc, L, iter, s, tol, traj);
+      if (rc != 0) break;
     }
-    STAMP(3)
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, 8);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, 8);
-    }
-    const double2 e0 = shfl2(acc, 0), ep = shfl2(acc, 8), em = shfl2(acc, 16);
-    STAMP(4)
-    // checked_energy, then the gradient's two expectations (vqe.hpp:227-229);
-    // one predicate on the common path, the exact failure decoded after
-    const bool bad = fabs(e0.y) >= 1e-10 || !isfinite(e0.x) ||
-                     (!final_eval && (fabs(ep.y) >= 1e-10 || fabs(em.y) >= 1e-10));
-    if (bad) {
-      if (lane == 0) {
-        int st;
-        double val = 0.0;
-        if (fabs(e0.y) >= 1e-10) {
-          st = kStatusImag;
-          val = e0.y;
-        } else if (!isfinite(e0.x)) {
-          st = kStatusNonFinite;
-        } else {
-          st = kStatusImag;
-          val = fabs(ep.y) >= 1e-10 ? ep.y : em.y;
-        }
-        p.status[prob] = st;
-        p.err_val[prob] = val;
-        p.err_iter[prob] = iter;
-        p.err_theta[prob] = th;
-      }
+  }
+  if (rc == 2) return;
+  const int converged = rc == 1, iters = iter;
+  double e_final;
+  if (converged) {
+    e_final = traj[iters];
+  } else {  // the final checked_energy (vqe.hpp:244-247)
+    double2 own, ep, em;
+    if (fabs(s.th) < kFastTrigTheta) h2_energies<REG, true>(sh, L, s.th, own, ep, em);
+    else h2_energies<REG, false>(sh, L, s.th, own, ep, em);
+    const double2 e0 = shfl2(own, 0);
+    if (fabs(e0.y) >= 1e-10 || !isfinite(e0.x)) {
+      if (lane == 0) h2_fail(p, prob, T, s.th, e0, make_double2(0.0, 0.0), make_double2(0.0, 0.0));
       return;
     }
-    traj[iter] = e0.x;  // every lane stores the same value (one transaction)
-    if (final_eval) break;
-    const double g = 0.5 * (ep.x - em.x);
-    if (p.has_tol && fabs(g) < p.tol) {
-      converged = 1;
-      break;
-    }
-    STAMP(5)
-    // adam_step (vqe.hpp:152-174), t = iter + 1; the bias corrections are
-    // applied as host-computed reciprocals 1 / (1 - beta^t)
-    const double mk = p.beta1 * m + (1.0 - p.beta1) * g;
-    const double vk = p.beta2 * v + (1.0 - p.beta2) * g * g;
-    const double m_hat = mk * bc[2 * iter];
-    const double v_hat = vk * bc[2 * iter + 1];
-    th = th - adam_delta(p.lr, m_hat, v_hat, p.eps);
-    m = mk;
-    v = vk;
-    iters = iter + 1;
-    STAMP(6)
+    if (lane == 0) traj[T] = e0.x;
+    e_final = e0.x;
   }
 #ifdef VQF_STAGE_CLOCKS
-  if (prob == 0 && lane == 0)
-    printf("STAGES angle=%lld de=%lld groups=%lld reduce+bcast=%lld checks+grad=%lld adam=%lld total=%lld "
-           "iteration=%lld\n",
-           stamps[1] - stamps[0], stamps[2] - stamps[1], stamps[3] - stamps[2], stamps[4] - stamps[3],
-           stamps[5] - stamps[4], stamps[6] - stamps[5], stamps[6] - stamps[0], stamps[7] - stamps[0]);
+  if (prob == 0 && lane == 0) printf("STAGES iteration=%lld\n", c101 - c100);
   if (lane == 0) {
     unsigned long long g_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
     printf("TIMELINE bond %d sm %u entry %llu prologue_ns %llu loop_ns %llu end %llu\n", prob,
            static_cast<unsigned>(__mysmid()), g_entry, g_loop - g_entry, g_end - g_loop, g_end);
   }
+#else
+  (void)g_entry;
+  (void)g_loop;
 #endif
   if (lane == 0) {
     p.iters[prob] = iters;
     p.converged[prob] = converged;
-    p.energy[prob] = traj[converged ? iters : p.max_iterations];
-    p.theta_out[prob] = th;
+    p.energy[prob] = e_final;
+    p.theta_out[prob] = s.th;
   }
-  const int len = converged ? iters + 1 : p.max_iterations + 1;
+  const int len = converged ? iters + 1 : T + 1;
   for (int k = len + lane; k < p.traj_stride; k += 32) traj[k] = __longlong_as_double(-1LL);
+}
+
+// H2 fast path (n = 4, one parameter, 3 circuits x 8 lanes x 2 amplitudes).
+// Exchanges per iteration: one shuffle per flip group, a 3-level reduction
+// and 3 energy shuffles; the DoubleExcitation partner exchange of the fixed
+// input state is done once.
+template <bool PES>
+__global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+  double* bc = reinterpret_cast<double*>(smem_raw + sizeof(Shared));
+  const int prob = blockIdx.x;
+  unsigned long long g_entry = 0, g_loop = 0;
+#ifdef VQF_STAGE_CLOCKS
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
+#endif
+  if (!prologue<PES>(sh, p, prob, bc, 16)) return;
+#ifdef VQF_STAGE_CLOCKS
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_loop));
+#endif
+  H2Lane L;
+  const int lane = threadIdx.x & 31, seg = lane >> 3;
+  L.sl = lane & 7;
+  L.circ = seg < 3 ? seg : 0;
+  L.G = sh.n_groups;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const bool on = g < L.G;
+    const int f = on ? sh.flip[g] : 0;
+    L.fl[g] = f & 7;
+    L.fs[g] = f & 8;
+    L.o0[g] = on ? sh.tab[g * 16 + L.sl] : make_double2(0.0, 0.0);
+    L.o1[g] = on ? sh.tab[g * 16 + 8 + L.sl] : make_double2(0.0, 0.0);
+  }
+  // basis_state(4, {1,1,0,0}): index 12 = slot 1 of sl 4; partner i ^ 15
+  L.in0 = make_double2(0.0, 0.0);
+  L.in1 = make_double2(L.sl == 4 ? 1.0 : 0.0, 0.0);
+  L.q0 = shfl_xor2(L.in1, 7, 8);
+  L.q1 = shfl_xor2(L.in0, 7, 8);
+  if (L.G <= 4) h2_optimise<true>(sh, p, prob, bc, L, g_entry, g_loop);
+  else h2_optimise<false>(sh, p, prob, bc, L, g_entry, g_loop);
 }
 
 template <int A, bool PES, bool H2>

@@ -270,6 +270,21 @@ def test_run_vqe_errors_and_init(gpu, ref):
     assert a.trajectory == b.trajectory and a.theta == b.theta  # test_vqe.cpp:216-226
 
 
+@pytest.mark.parametrize("theta0", [2.0 ** 28 - 0.015, -(2.0 ** 28) + 0.015, 3.0e8, 1.0e12])
+def test_run_vqe_h2_large_theta_trig_path(gpu, ref, theta0):
+    """The H2 loop's short-range sincos hands over to the library sincos
+    once |theta| >= 2^28 (fastmath.cuh): trajectories stay on the reference's,
+    including a run that crosses the threshold mid-optimisation."""
+    V = gpu
+    H2 = V.AnsatzSpec.h2_double_excitation()
+    h = ref.build_h2_hamiltonian(0.7414)
+    want = ref.run_vqe(h, max_iter=40, init=[theta0])
+    r = V.run_vqe(to_v(V, h), H2, V.AdamConfig(max_iterations=40), [theta0])
+    assert r.iterations_run == want["iterations_run"] == 40
+    assert np.max(np.abs(np.array(r.trajectory) - want["trajectory"])) < E_TOL
+    assert r.theta[0] == pytest.approx(want["theta"][0], rel=1e-15, abs=1e-9)
+
+
 @pytest.mark.parametrize("key", ["tfim4", "zsum5", "tfim6", "tfim8"])
 def test_run_vqe_hea_matches_golden(gpu, golden, key):
     V = gpu
