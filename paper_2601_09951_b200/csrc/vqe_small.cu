@@ -279,7 +279,7 @@ __device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
   const ChemConsts& k = p.chem;
   const double d = pes_bond(p, prob) * kAngstromToBohr;
 #ifdef VQF_STAGE_CLOCKS
-  long long t_start = clock64(), t_pf, t_prim, t_sum, t_scf, t_mo, t_jw;
+  long long t_start = clock64(), t_pf, t_boys, t_prim, t_sum, t_scf, t_mo, t_jw;
 #endif
   // The Jordan-Wigner contribution map is bond-independent: issue its loads
   // now so their latency hides under the integral work.
@@ -327,6 +327,9 @@ __device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
     }
   }
   __syncthreads();
+#ifdef VQF_STAGE_CLOCKS
+  t_boys = clock64();
+#endif
   constexpr int kOne = 36 * 4;  // S, T, V(nucleus 0), V(nucleus 1) per (ij, xy)
   for (int idx = threadIdx.x; idx < 1296 + kOne; idx += blockDim.x) {
     if (idx < 1296) {
@@ -491,8 +494,8 @@ __device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
 #ifdef VQF_STAGE_CLOCKS
     t_jw = clock64();
     if (prob == 0)
-      printf("PROLOGUE pair=%lld prims=%lld sums=%lld scf=%lld mo=%lld jw=%lld total=%lld (scf iters %d)\n",
-             t_pf - t_start, t_prim - t_pf, t_sum - t_prim, t_scf - t_sum, t_mo - t_scf, t_jw - t_mo,
+      printf("PROLOGUE pair=%lld boys=%lld prims=%lld sums=%lld scf=%lld mo=%lld jw=%lld total=%lld (scf iters %d)\n",
+             t_pf - t_start, t_boys - t_pf, t_prim - t_boys, t_sum - t_prim, t_scf - t_sum, t_mo - t_scf, t_jw - t_mo,
              t_jw - t_start, sh.hf.scf_iterations);
 #endif
     if (p.ham_count != nullptr) p.ham_count[prob] = sh.stop ? 0 : nt;
@@ -566,38 +569,40 @@ __device__ __forceinline__ void h2_fail(const SmallParams& p, int prob, int iter
 }
 
 // The three circuits of one H2 iteration, E(theta), E(theta + pi/2) and
-// E(theta - pi/2) (vqe.hpp:115-127), each complete on every lane.  Lanes
-// 8c..8c+7 hold circuit c with amplitude indices {sl, 8 + sl}.  REG: the
-// Hamiltonian's flip groups (<= 4) are in registers; else read from smem.
+// E(theta - pi/2) (vqe.hpp:115-127).  Lanes 8c..8c+7 hold circuit c with
+// amplitude indices {sl, 8 + sl} (lanes 24..31 repeat circuit 0).  G: the
+// number of flip groups, compile-time so the group loop has no branches
+// (1..4, tables in registers); 0 = any count, tables read from smem.
 struct H2Lane {
   int sl, circ, G;
+  double shift;  // 0, +pi/2, -pi/2 (theta + shift is the reference's sum)
   int fl[4], fs[4];
   double2 o0[4], o1[4];
   double2 in0, in1, q0, q1;  // |1100> and its DoubleExcitation partners
 };
 
-// own: this lane's circuit total (lane 0 holds E(theta)); ep / em: the two
-// shifted energies on every lane.
-template <bool REG, bool FAST>
-__device__ __forceinline__ void h2_energies(const Shared& sh, const H2Lane& L, double th, double2& own, double2& ep,
-                                            double2& em) {
+// own: this lane's circuit total (lane 0 holds E(theta)); ep_re / em_re:
+// the real parts of the two shifted energies on every lane.
+template <int G, bool FAST>
+__device__ __forceinline__ void h2_energies(const Shared& sh, const H2Lane& L, double th, double2& own,
+                                            double& ep_re, double& em_re) {
   // gradient(): shifted[k] = theta[k] +- pi/2 (vqe.hpp:119-121)
-  double t = th;
-  if (L.circ == 1) t = th + kShift;
-  if (L.circ == 2) t = th - kShift;
+  const double t = th + L.shift;
   double sn, cs;
   if (FAST) sincos_reduced(0.5 * t, &sn, &cs);
   else sincos(0.5 * t, &sn, &cs);
-  // DoubleExcitation(0,1,2,3) on |1100>: rotate indices 12 and 3
-  const double2 r12 = make_double2(fma(cs, L.in1.x, -sn * L.q1.x), fma(cs, L.in1.y, -sn * L.q1.y));
-  const double2 r3 = make_double2(fma(sn, L.q0.x, cs * L.in0.x), fma(sn, L.q0.y, cs * L.in0.y));
-  const double2 a1 = L.sl == 4 ? r12 : L.in1, a0 = L.sl == 3 ? r3 : L.in0;
+  // DoubleExcitation(0,1,2,3) on the fixed input |1100>: indices 12 and 3
+  // rotate; every other amplitude and its partner are zero, so the same
+  // rotation formula on all lanes leaves them zero (no per-lane select).
+  const double2 a1 = make_double2(fma(cs, L.in1.x, -sn * L.q1.x), fma(cs, L.in1.y, -sn * L.q1.y));
+  const double2 a0 = make_double2(fma(sn, L.q0.x, cs * L.in0.x), fma(sn, L.q0.y, cs * L.in0.y));
   // expectation: sum_g O_g(i) conj(psi_i) psi_{i ^ f_g}.  Group 0 is the
   // diagonal (flip 0, build_tables puts it first): O_0(i) |psi_i|^2 with no
-  // exchange; the flip groups exchange partners by shuffle.  Group terms
-  // are formed independently, then added in group order.
+  // exchange; the flip groups exchange partners by shuffle (xor 0 when a
+  // group flips only the slot bit).  Group terms are formed independently,
+  // then added in group order.
   double2 acc;
-  if (REG) {
+  if (G > 0) {
     double2 term[4];
     {
       const double n0 = fma(a0.x, a0.x, a0.y * a0.y), n1 = fma(a1.x, a1.x, a1.y * a1.y);
@@ -606,28 +611,28 @@ __device__ __forceinline__ void h2_energies(const Shared& sh, const H2Lane& L, d
 #pragma unroll
     for (int g = 1; g < 4; ++g) {
       term[g] = make_double2(0.0, 0.0);
-      if (g >= L.G) continue;  // warp-uniform
-      double2 r0 = L.fs[g] ? a1 : a0, r1 = L.fs[g] ? a0 : a1;
-      if (L.fl[g]) {  // warp-uniform
+      if (g < G) {
+        double2 r0 = L.fs[g] ? a1 : a0, r1 = L.fs[g] ? a0 : a1;
         r0 = shfl_xor2(r0, L.fl[g], 8);
         r1 = shfl_xor2(r1, L.fl[g], 8);
+        const double v0r = fma(a0.x, r0.x, a0.y * r0.y), v0i = fma(a0.x, r0.y, -a0.y * r0.x);
+        const double v1r = fma(a1.x, r1.x, a1.y * r1.y), v1i = fma(a1.x, r1.y, -a1.y * r1.x);
+        term[g].x = fma(L.o0[g].x, v0r, fma(-L.o0[g].y, v0i, fma(L.o1[g].x, v1r, -L.o1[g].y * v1i)));
+        term[g].y = fma(L.o0[g].x, v0i, fma(L.o0[g].y, v0r, fma(L.o1[g].x, v1i, L.o1[g].y * v1r)));
       }
-      const double v0r = fma(a0.x, r0.x, a0.y * r0.y), v0i = fma(a0.x, r0.y, -a0.y * r0.x);
-      const double v1r = fma(a1.x, r1.x, a1.y * r1.y), v1i = fma(a1.x, r1.y, -a1.y * r1.x);
-      term[g].x = fma(L.o0[g].x, v0r, fma(-L.o0[g].y, v0i, fma(L.o1[g].x, v1r, -L.o1[g].y * v1i)));
-      term[g].y = fma(L.o0[g].x, v0i, fma(L.o0[g].y, v0r, fma(L.o1[g].x, v1i, L.o1[g].y * v1r)));
     }
-    acc.x = (term[0].x + term[1].x) + (term[2].x + term[3].x);
-    acc.y = (term[0].y + term[1].y) + (term[2].y + term[3].y);
+    if (G == 1) acc = term[0];
+    else if (G == 2) acc = make_double2(term[0].x + term[1].x, term[0].y + term[1].y);
+    else if (G == 3) acc = make_double2((term[0].x + term[1].x) + term[2].x, (term[0].y + term[1].y) + term[2].y);
+    else acc = make_double2((term[0].x + term[1].x) + (term[2].x + term[3].x),
+                            (term[0].y + term[1].y) + (term[2].y + term[3].y));
   } else {
     acc = make_double2(0.0, 0.0);
     for (int g = 0; g < L.G; ++g) {
       const int f = sh.flip[g], fl = f & 7;
       double2 r0 = (f & 8) ? a1 : a0, r1 = (f & 8) ? a0 : a1;
-      if (fl) {
-        r0 = shfl_xor2(r0, fl, 8);
-        r1 = shfl_xor2(r1, fl, 8);
-      }
+      r0 = shfl_xor2(r0, fl, 8);
+      r1 = shfl_xor2(r1, fl, 8);
       const double2 o0 = sh.tab[g * 16 + L.sl], o1 = sh.tab[g * 16 + 8 + L.sl];
       const double v0r = fma(a0.x, r0.x, a0.y * r0.y), v0i = fma(a0.x, r0.y, -a0.y * r0.x);
       const double v1r = fma(a1.x, r1.x, a1.y * r1.y), v1i = fma(a1.x, r1.y, -a1.y * r1.x);
@@ -641,8 +646,8 @@ __device__ __forceinline__ void h2_energies(const Shared& sh, const H2Lane& L, d
     acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, 8);
   }
   own = acc;
-  ep = shfl2(acc, 8);
-  em = shfl2(acc, 16);
+  ep_re = __shfl_sync(0xffffffffu, acc.x, 8);
+  em_re = __shfl_sync(0xffffffffu, acc.x, 16);
 }
 
 // One iteration of run_vqe's loop (vqe.hpp:225-243) on one warp: energies,
@@ -654,24 +659,25 @@ struct H2State {
   double th, m, v;
 };
 
-template <bool REG, bool FAST>
+template <int G, bool FAST>
 __device__ __forceinline__ int h2_step(const Shared& sh, const SmallParams& p, int prob, const double* bc,
                                        const H2Lane& L, int iter, H2State& s, double tol, double* traj) {
   const int lane = threadIdx.x & 31;
   const bool range_bad = FAST && !(fabs(s.th) < kFastTrigTheta);  // warp-uniform
-  double2 own, ep, em;
-  h2_energies<REG, FAST>(sh, L, s.th, own, ep, em);
+  double2 own;
+  double ep_re, em_re;
+  h2_energies<G, FAST>(sh, L, s.th, own, ep_re, em_re);
   // checked_energy, then the gradient's two expectations (vqe.hpp:227-229):
   // each lane checks its own circuit, one vote
   const bool my_bad = range_bad || fabs(own.y) >= 1e-10 || (L.circ == 0 && !isfinite(own.x));
   if (__any_sync(0xffffffffu, my_bad)) {
     if (range_bad) return 3;
-    const double2 e0 = shfl2(own, 0);
+    const double2 e0 = shfl2(own, 0), ep = shfl2(own, 8), em = shfl2(own, 16);
     if (lane == 0) h2_fail(p, prob, iter, s.th, e0, ep, em);
     return 2;
   }
   if (lane == 0) traj[iter] = own.x;
-  const double g = 0.5 * (ep.x - em.x);
+  const double g = 0.5 * (ep_re - em_re);
   if (fabs(g) < tol) return 1;
   // adam_step (vqe.hpp:152-174), t = iter + 1; the bias corrections are
   // applied as host-computed reciprocals 1 / (1 - beta^t)
@@ -687,7 +693,7 @@ __device__ __forceinline__ int h2_step(const Shared& sh, const SmallParams& p, i
 
 // run_vqe's loop (vqe.hpp:225-247) for one bond: the fast-trig loop, and
 // the library-sincos continuation should theta ever leave its range.
-template <bool REG>
+template <int G>
 __device__ __forceinline__ void h2_optimise(const Shared& sh, const SmallParams& p, int prob, const double* bc,
                                             const H2Lane& L, unsigned long long g_entry, unsigned long long g_loop) {
   const int lane = threadIdx.x & 31;
@@ -704,12 +710,12 @@ __device__ __forceinline__ void h2_optimise(const Shared& sh, const SmallParams&
     if (iter == 100) c100 = clock64();
     if (iter == 101) c101 = clock64();
 #endif
-    rc = h2_step<REG, true>(sh, p, prob, bc, L, iter, s, tol, traj);
+    rc = h2_step<G, true>(sh, p, prob, bc, L, iter, s, tol, traj);
     if (rc != 0) break;
   }
   if (rc == 3) {
     for (rc = 0; iter < T; ++iter) {
-      rc = h2_step<REG, false>(sh, p, prob, bc, L, iter, s, tol, traj);
+      rc = h2_step<G, false>(sh, p, prob, bc, L, iter, s, tol, traj);
       if (rc != 0) break;
     }
   }
@@ -719,9 +725,10 @@ __device__ __forceinline__ void h2_optimise(const Shared& sh, const SmallParams&
   if (converged) {
     e_final = traj[iters];
   } else {  // the final checked_energy (vqe.hpp:244-247)
-    double2 own, ep, em;
-    if (fabs(s.th) < kFastTrigTheta) h2_energies<REG, true>(sh, L, s.th, own, ep, em);
-    else h2_energies<REG, false>(sh, L, s.th, own, ep, em);
+    double2 own;
+    double ep_re, em_re;
+    if (fabs(s.th) < kFastTrigTheta) h2_energies<G, true>(sh, L, s.th, own, ep_re, em_re);
+    else h2_energies<G, false>(sh, L, s.th, own, ep_re, em_re);
     const double2 e0 = shfl2(own, 0);
     if (fabs(e0.y) >= 1e-10 || !isfinite(e0.x)) {
       if (lane == 0) h2_fail(p, prob, T, s.th, e0, make_double2(0.0, 0.0), make_double2(0.0, 0.0));
@@ -774,6 +781,7 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
   const int lane = threadIdx.x & 31, seg = lane >> 3;
   L.sl = lane & 7;
   L.circ = seg < 3 ? seg : 0;
+  L.shift = L.circ == 1 ? kShift : L.circ == 2 ? -kShift : 0.0;
   L.G = sh.n_groups;
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
@@ -789,8 +797,13 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
   L.in1 = make_double2(L.sl == 4 ? 1.0 : 0.0, 0.0);
   L.q0 = shfl_xor2(L.in1, 7, 8);
   L.q1 = shfl_xor2(L.in0, 7, 8);
-  if (L.G <= 4) h2_optimise<true>(sh, p, prob, bc, L, g_entry, g_loop);
-  else h2_optimise<false>(sh, p, prob, bc, L, g_entry, g_loop);
+  switch (L.G) {  // warp-uniform: one specialised loop per group count
+    case 1: h2_optimise<1>(sh, p, prob, bc, L, g_entry, g_loop); break;
+    case 2: h2_optimise<2>(sh, p, prob, bc, L, g_entry, g_loop); break;
+    case 3: h2_optimise<3>(sh, p, prob, bc, L, g_entry, g_loop); break;
+    case 4: h2_optimise<4>(sh, p, prob, bc, L, g_entry, g_loop); break;
+    default: h2_optimise<0>(sh, p, prob, bc, L, g_entry, g_loop); break;
+  }
 }
 
 template <int A, bool PES, bool H2>
