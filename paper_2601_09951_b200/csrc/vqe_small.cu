@@ -37,7 +37,13 @@ namespace vqf {
 namespace {
 
 constexpr double kShift = 1.5707963267948966;  // std::numbers::pi / 2 (vqe.hpp:115)
-constexpr int kPesThreads = 512;  // chemistry prologue width; warps 1.. exit before the loop
+#ifndef VQF_PES_THREADS
+#define VQF_PES_THREADS 256
+#endif
+// Chemistry prologue width; warps 1.. exit before the loop.  256 keeps the
+// register cap at 255 for the optimisation loop (512 threads cap it at 128
+// and the loop then spills its constants through uniform registers).
+constexpr int kPesThreads = VQF_PES_THREADS;
 constexpr int kMaxGates = 2 * kSmallMaxP + 8;
 
 enum : int { G_X = 0, G_RY = 1, G_CNOT = 2, G_DE = 3 };
@@ -768,7 +774,7 @@ __device__ __forceinline__ void h2_optimise(const Shared& sh, const SmallParams&
 // and 3 energy shuffles; the DoubleExcitation partner exchange of the fixed
 // input state is done once.
 template <bool PES>
-__global__ void __launch_bounds__(PES ? kPesThreads : 32) k_h2(SmallParams p) {
+__global__ void __launch_bounds__(PES ? kPesThreads : 32, 1) k_h2(SmallParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
   double* bc = reinterpret_cast<double*>(smem_raw + sizeof(Shared));
