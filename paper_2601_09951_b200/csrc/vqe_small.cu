@@ -38,11 +38,12 @@ namespace {
 
 constexpr double kShift = 1.5707963267948966;  // std::numbers::pi / 2 (vqe.hpp:115)
 #ifndef VQF_PES_THREADS
-#define VQF_PES_THREADS 256
+#define VQF_PES_THREADS 288
 #endif
-// Chemistry prologue width; warps 1.. exit before the loop.  256 keeps the
-// register cap at 255 for the optimisation loop (512 threads cap it at 128
-// and the loop then spills its constants through uniform registers).
+// Chemistry prologue width; warps 1.. exit before the loop.  288 threads:
+// the 273 distinct Boys evaluations run in one round, and the register cap
+// stays at 224 for the optimisation loop (512 threads cap it at 128 and the
+// loop then spills its constants through uniform registers).
 constexpr int kPesThreads = VQF_PES_THREADS;
 constexpr int kMaxGates = 2 * kSmallMaxP + 8;
 
@@ -316,18 +317,17 @@ __device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
   // primitives of a same-centre pair, so it is evaluated once per unordered
   // pair of the 21 distinct pair factors (231 + 42 nuclear instead of
   // 1296 + 72) - bitwise the values eri_prim / nuclear_prim compute.
-  for (int idx = threadIdx.x; idx < 441 + 42; idx += blockDim.x) {
-    if (idx < 441) {
-      const int u = idx / 21, v = idx % 21;
-      if (u <= v) {
-        const PairFactor& a = sh.pf[sh.pf_rep[u]];
-        const PairFactor& b = sh.pf[sh.pf_rep[v]];
-        const int pi = pf_pair(u, v);
-        sh.eri_pref[pi] = eri_pref(k, a.p, b.p);
-        sh.eri_boys[pi] = boys_f0(a.p * b.p / (a.p + b.p) * d2z(a.P, b.P));
-      }
+  for (int idx = threadIdx.x; idx < 231 + 42; idx += blockDim.x) {
+    if (idx < 231) {
+      int u = 0;  // decode pf_pair: row u starts at u * 21 - u * (u - 1) / 2
+      while (u < 20 && pf_pair(u + 1, u + 1) <= idx) ++u;
+      const int v = u + (idx - pf_pair(u, u));
+      const PairFactor& a = sh.pf[sh.pf_rep[u]];
+      const PairFactor& b = sh.pf[sh.pf_rep[v]];
+      sh.eri_pref[idx] = eri_pref(k, a.p, b.p);
+      sh.eri_boys[idx] = boys_f0(a.p * b.p / (a.p + b.p) * d2z(a.P, b.P));
     } else {
-      const int o = idx - 441, u = o >> 1;
+      const int o = idx - 231, u = o >> 1;
       const PairFactor& f = sh.pf[sh.pf_rep[u]];
       sh.nuc_boys[o] = boys_f0(f.p * d2z(f.P, (o & 1) ? d : 0.0));
     }
@@ -519,6 +519,19 @@ __device__ void build_h2_device(Shared& sh, const SmallParams& p, int prob) {
 // mask terms (built on device in PES mode), then the lane tables.  Returns
 // false for threads that take no part in the optimisation (warps 1..3 of a
 // PES CTA, or a problem that already failed).
+#ifdef VQF_STAGE_CLOCKS
+__device__ unsigned long long g_marks[4];  // bond 0: after bias tables, Hamiltonian, lane tables
+__device__ __forceinline__ void gmark(int prob, int i) {
+  if (prob == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_marks[i] = t;
+  }
+}
+#else
+__device__ __forceinline__ void gmark(int, int) {}
+#endif
+
 template <bool PES>
 __device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int prob, double* bc, int D) {
   const int lane = threadIdx.x & 31;
@@ -528,6 +541,7 @@ __device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int p
     bc[2 * t + 1] = p.bc2[t];
   }
   __syncthreads();
+  gmark(prob, 0);
   if (PES) {
     if (p.grid_n > 0) {  // grid mode: the range check (chem.hpp:33-34) is ours
       const double b = pes_bond(p, prob);
@@ -542,6 +556,7 @@ __device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int p
       if (threadIdx.x == 0) p.status[prob] = sh.stop;
       return false;
     }
+    gmark(prob, 1);
     if (threadIdx.x >= 32) return false;  // warp 0 runs the optimisation
   } else {
     const uint32_t t0 = p.term_off[prob], t1 = p.term_off[prob + 1];
@@ -550,6 +565,7 @@ __device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int p
     __syncwarp();
   }
   build_tables(sh, D, lane);
+  gmark(prob, 2);
   return true;
 }
 
@@ -677,6 +693,13 @@ __device__ __forceinline__ int h2_step(const Shared& sh, const SmallParams& p, i
   double2 own;
   double ep_re, em_re;
   h2_energies<G, FAST>(sh, L, s.th, own, ep_re, em_re);
+  // gradient and the Adam update (vqe.hpp:152-174, t = iter + 1; bias
+  // corrections as host-computed reciprocals 1 / (1 - beta^t)) are formed
+  // first and committed after the checks, so their latency overlaps the vote
+  const double g = 0.5 * (ep_re - em_re);
+  const double mk = p.beta1 * s.m + (1.0 - p.beta1) * g;
+  const double vk = p.beta2 * s.v + (1.0 - p.beta2) * g * g;
+  const double th_next = s.th - adam_delta_fast(p.lr, mk * bcs.x, vk * bcs.y, p.eps);
   // checked_energy, then the gradient's two expectations (vqe.hpp:227-229):
   // each lane checks its own circuit, one vote
   const bool my_bad = range_bad || fabs(own.y) >= 1e-10 || (L.circ == 0 && !isfinite(own.x));
@@ -687,15 +710,8 @@ __device__ __forceinline__ int h2_step(const Shared& sh, const SmallParams& p, i
     return 2;
   }
   if (lane == 0) traj[iter] = own.x;
-  const double g = 0.5 * (ep_re - em_re);
   if (fabs(g) < tol) return 1;
-  // adam_step (vqe.hpp:152-174), t = iter + 1; the bias corrections are
-  // applied as host-computed reciprocals 1 / (1 - beta^t)
-  const double mk = p.beta1 * s.m + (1.0 - p.beta1) * g;
-  const double vk = p.beta2 * s.v + (1.0 - p.beta2) * g * g;
-  const double m_hat = mk * bcs.x;
-  const double v_hat = vk * bcs.y;
-  s.th = s.th - adam_delta(p.lr, m_hat, v_hat, p.eps);
+  s.th = th_next;
   s.m = mk;
   s.v = vk;
   return 0;
@@ -754,6 +770,9 @@ __device__ __forceinline__ void h2_optimise(const Shared& sh, const SmallParams&
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
     printf("TIMELINE bond %d sm %u entry %llu prologue_ns %llu loop_ns %llu end %llu\n", prob,
            static_cast<unsigned>(__mysmid()), g_entry, g_loop - g_entry, g_end - g_loop, g_end);
+    if (prob == 0)
+      printf("PROLOGUE_NS bias %llu hamiltonian %llu tables %llu\n", g_marks[0] - g_entry, g_marks[1] - g_marks[0],
+             g_marks[2] - g_marks[1]);
   }
 #else
   (void)g_entry;

@@ -8,4 +8,4 @@ cp -r "$ROOT/paper_2601_09951_b200" "$ROOT/include" "$ROOT/scripts" "$ROOT/tools
 cd /tmp/vqf_clk/paper_2601_09951_b200/csrc
 sed -i "s/^FLAGS := \$(ARCH)/FLAGS := -DVQF_STAGE_CLOCKS ${EXTRA_FLAGS:-} \$(ARCH)/" Makefile
 rm -rf build ../libvqf_b200.so && make -j8 >/dev/null 2>&1
-cd /tmp/vqf_clk && python scripts/prof_targets.py pes 2>&1 | grep -E "STAGES|PROLOGUE|TIMELINE" > /tmp/stage.txt; grep -E "STAGES|PROLOGUE" /tmp/stage.txt | head -2; python3 scripts/timeline.py /tmp/stage.txt
+cd /tmp/vqf_clk && python scripts/prof_targets.py pes 2>&1 | grep -E "STAGES|PROLOGUE|TIMELINE" > /tmp/stage.txt; grep -E "STAGES|PROLOGUE" /tmp/stage.txt | head -3; python3 scripts/timeline.py /tmp/stage.txt
