@@ -275,6 +275,14 @@ int vqf_expectation_complex(vqf_sv sv, const vqf_hamiltonian* h, double* out);
  * two states of one register (batch entry 0), as (re, im): the shard-pair
  * term of a distributed expectation whose Pauli string flips global wires. */
 int vqf_cross_expectation(vqf_sv a, vqf_sv b, const vqf_hamiltonian* h, double* out);
+/* How vqf_expectation reads the state for h (host only, no device work):
+ * state_passes = HBM passes over the state (diagonal pass + one per
+ * multi-group pass + one per remaining flip group), flip_groups = distinct
+ * non-zero flip masks (the reference's per-group pass count, minus the
+ * diagonal), multi_passes = register-resident passes that serve several
+ * flip groups each.  Any out pointer may be NULL. */
+int vqf_expectation_plan(const vqf_hamiltonian* h, uint32_t* state_passes, uint32_t* flip_groups,
+                         uint32_t* multi_passes);
 /* Raw device address and byte size of the amplitudes (for exchanging
  * shards with NCCL / peer copies; the handle keeps ownership). */
 int vqf_sv_device_ptr(vqf_sv sv, void** ptr, uint64_t* bytes);

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <utility>
 
 #include "sv.cuh"
 #include "tile.cuh"
@@ -125,9 +126,9 @@ __global__ void __launch_bounds__(kThreads) k_cnot(typename V2<T>::type* __restr
     ok[u] = p < total;
     const uint64_t b = p >> qlog, k = p & ((uint64_t{1} << qlog) - 1);
     i0[u] = (b << n) | insert_zeros<2>(k, pos) | cbit;
-    if (ok[u]) {
-      x0[u] = a[i0[u]];
-      x1[u] = a[i0[u] | tbit];
+    if (ok[u]) {  // L2-only loads: no L1 line fill around sparse sectors
+      x0[u] = __ldcg(a + i0[u]);
+      x1[u] = __ldcg(a + (i0[u] | tbit));
     }
   }
 #pragma unroll
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) k_givens(typename V2<T>::type* __res
     if (p >= total) continue;
     const uint64_t b = p >> qlog, k = p & ((uint64_t{1} << qlog) - 1);
     const uint64_t r = (b << n) | insert_zeros<M>(k, pos);
-    const A x = a[r | pat_a], y = a[r | pat_b];
+    const A x = __ldcg(a + (r | pat_a)), y = __ldcg(a + (r | pat_b));  // L2-only: sparse sectors
     T c, s;
     entry_cs<T>(g, b, c, s);
     A xa, yb;
@@ -320,6 +321,126 @@ __global__ void __launch_bounds__(kThreads) k_expect_diag_tiled(
   }
 }
 
+// Diagonal group, factorised (n >= kDiagB).  Thread t of a 256-thread CTA
+// owns the amplitudes lo_u = t + 256 u (u < 8) of every 2048-amplitude tile
+// it visits, so with i = (tile << 11) | lo_u each Z-string sign factorises
+// into a per-thread constant, a per-u pattern and a per-tile sign:
+//   * low terms (Z support below bit 11): the thread's sign for lo_u is fixed
+//     across tiles, so it accumulates P_u = sum_tiles |psi|^2 and applies the
+//     low terms once at the end;
+//   * high terms (support at bit 11 and above): one complex scalar H(tile),
+//     evaluated lane-parallel (one term per lane, xor-butterfly sum, identical
+//     in every lane) and applied to q = sum_u |psi_u|^2;
+//   * mixed terms: sign = parity(((tile << 8) | t) & m) * (-1)^popc(u & v)
+//     with m = (yz_hi << 8) | yz[0..8) and v = yz[8..11), so the per-u part
+//     is an 8-point Walsh-Hadamard transform W of the thread's |psi_u|^2 and
+//     each term costs one parity + one FMA per tile (host packs m into .yz
+//     and v into .flip, terms sorted by v).
+// Per amplitude that leaves one 16-byte load, |psi|^2 and a few adds: the
+// pass is HBM-bound for any number of diagonal terms.  Summation order is
+// fixed by (n, grid), so results are deterministic.
+constexpr uint32_t kDiagB = 11, kDiagU = 8;
+static_assert(kThreads * kDiagU == (1u << kDiagB), "diag tile = CTA x unroll");
+
+struct DiagSplit {
+  uint32_t n_lo, n_hi, n_mx;
+  uint32_t mx_off[9];  // mixed terms with v = j are [mx_off[j], mx_off[j + 1])
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_expect_diag_fact(const typename V2<T>::type* __restrict__ a, uint32_t n,
+                                                               const MaskTerm* __restrict__ lo_t,
+                                                               const MaskTerm* __restrict__ hi_t,
+                                                               const MaskTerm* __restrict__ mx_t, const DiagSplit ds,
+                                                               double* __restrict__ partials, uint32_t G,
+                                                               uint32_t stride) {
+  using A = typename V2<T>::type;
+  __shared__ MaskTerm sh_hi[64];
+  __shared__ MaskTerm sh_mx[64];
+  for (uint32_t t = threadIdx.x; t < ds.n_hi; t += kThreads) sh_hi[t] = hi_t[t];
+  for (uint32_t t = threadIdx.x; t < ds.n_mx; t += kThreads) sh_mx[t] = mx_t[t];
+  __syncthreads();
+  const uint32_t b = blockIdx.y, lane = threadIdx.x & 31;
+  const uint64_t n_tiles = uint64_t{1} << (n - kDiagB);
+  const A* s = a + ((uint64_t)b << n) + threadIdx.x;
+  double P[kDiagU];
+#pragma unroll
+  for (int u = 0; u < (int)kDiagU; ++u) P[u] = 0.0;
+  double acc_re = 0.0, acc_im = 0.0;
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const A* src = s + (tile << kDiagB);
+    A x[kDiagU];
+#pragma unroll
+    for (int u = 0; u < (int)kDiagU; ++u) x[u] = src[u * kThreads];
+    // H(tile) while the loads are in flight
+    double hr = 0.0, hi = 0.0;
+    if (ds.n_hi) {
+      for (uint32_t t = lane; t < ds.n_hi; t += 32) {
+        const double sg = parity_sign(tile & (sh_hi[t].yz >> kDiagB));
+        hr += sg * sh_hi[t].cb_re;
+        hi += sg * sh_hi[t].cb_im;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        hr += __shfl_xor_sync(0xffffffffu, hr, o);
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+      }
+    }
+    double p[kDiagU];
+#pragma unroll
+    for (int u = 0; u < (int)kDiagU; ++u) {
+      p[u] = (double)x[u].x * (double)x[u].x + (double)x[u].y * (double)x[u].y;
+      P[u] += p[u];
+    }
+    if (ds.n_hi) {
+      const double q = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+      acc_re += q * hr;
+      acc_im += q * hi;
+    }
+    if (ds.n_mx) {
+      double w[kDiagU];  // w[v] = sum_u (-1)^popc(u & v) p[u]
+#pragma unroll
+      for (int u = 0; u < (int)kDiagU; ++u) w[u] = p[u];
+#pragma unroll
+      for (int h = 1; h < (int)kDiagU; h <<= 1)
+#pragma unroll
+        for (int u = 0; u < (int)kDiagU; ++u)
+          if ((u & h) == 0) {
+            const double l = w[u], r = w[u | h];
+            w[u] = l + r;
+            w[u | h] = l - r;
+          }
+      const uint64_t xt = (tile << 8) | threadIdx.x;
+#pragma unroll
+      for (int v = 0; v < (int)kDiagU; ++v)
+        for (uint32_t t = ds.mx_off[v]; t < ds.mx_off[v + 1]; ++t) {
+          const double sw = parity_sign(xt & sh_mx[t].yz) * w[v];
+          acc_re += sw * sh_mx[t].cb_re;
+          acc_im += sw * sh_mx[t].cb_im;
+        }
+    }
+  }
+  // low terms, once per owned lo_u
+#pragma unroll
+  for (int u = 0; u < (int)kDiagU; ++u) {
+    const uint32_t lo = threadIdx.x + u * kThreads;
+    double lr = 0.0, li = 0.0;
+    for (uint32_t t = 0; t < ds.n_lo; ++t) {
+      const double sg = parity_sign(lo & lo_t[t].yz);
+      lr += sg * lo_t[t].cb_re;
+      li += sg * lo_t[t].cb_im;
+    }
+    acc_re += P[u] * lr;
+    acc_im += P[u] * li;
+  }
+  const double2 acc = block_sum(make_double2(acc_re, acc_im));
+  if (threadIdx.x == 0) {
+    const size_t o = ((size_t)b * G + 0) * stride + blockIdx.x;
+    partials[2 * o] = acc.x;
+    partials[2 * o + 1] = acc.y;
+  }
+}
+
 // Cross term between two states a, b of one register:
 //   sum_t cb_t sum_i (-1)^popc(i & yz_t) conj(a_i) b_{i ^ flip_t}
 // (the shard-pair contribution of a Pauli term that flips global wires of a
@@ -367,6 +488,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_flip(const typename V2<T>::
                                                           uint64_t flip, uint32_t hb,
                                                           const MaskTerm* __restrict__ terms, uint32_t n_terms,
                                                           double* __restrict__ partials, uint32_t G, uint32_t group) {
+  constexpr int U = kExpU;
   __shared__ MaskTerm st[64];
   __shared__ double sig[64];
   const uint32_t b = blockIdx.y;
@@ -382,11 +504,11 @@ __global__ void __launch_bounds__(kThreads) k_expect_flip(const typename V2<T>::
     }
     __syncthreads();
     const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-    for (uint64_t k0 = (uint64_t)blockIdx.x * kThreads + threadIdx.x; k0 < half; k0 += stride * kExpU) {
-      typename V2<T>::type x[kExpU], y[kExpU];
-      uint64_t idx[kExpU];
+    for (uint64_t k0 = (uint64_t)blockIdx.x * kThreads + threadIdx.x; k0 < half; k0 += stride * U) {
+      typename V2<T>::type x[U], y[U];
+      uint64_t idx[U];
 #pragma unroll
-      for (int u = 0; u < kExpU; ++u) {  // pairs in flight before arithmetic
+      for (int u = 0; u < U; ++u) {  // pairs in flight before arithmetic
         const uint64_t k = k0 + u * stride;
         idx[u] = insert_zero(k, hb);
         if (k < half) {
@@ -395,7 +517,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_flip(const typename V2<T>::
         }
       }
 #pragma unroll
-      for (int u = 0; u < kExpU; ++u) {
+      for (int u = 0; u < U; ++u) {
         if (k0 + u * stride >= half) break;
         const uint64_t i = idx[u];
         // v = conj(x) * y
@@ -423,6 +545,200 @@ __global__ void __launch_bounds__(kThreads) k_expect_flip(const typename V2<T>::
     const size_t o = ((size_t)b * G + group) * gridDim.x + blockIdx.x;
     partials[2 * o] = acc.x;
     partials[2 * o + 1] = acc.y;
+  }
+}
+
+// Several flip groups in one pass.  Each thread holds the 16 amplitudes that
+// differ in four "register" index bits R (all >= 5) of one base index whose
+// bits 0..4 are the lane, so warp loads stay 512 B contiguous.  A group whose
+// flip mask lies inside R u {0..4} pairs amplitudes inside the thread
+// (register bits) or across lanes (__shfl_xor on the lane bits): the pass
+// reads the state once for all of them instead of once per group.
+//
+// Per group the thread forms v_k = conj(psi_i) psi_{i ^ f} for its pairs
+// (each unordered pair once, from the side where f's top bit is clear; 8
+// pairs when f has register bits, else 16 on the lanes whose top flip bit is
+// clear).  A term's sign (-1)^popc(i & yz) splits into the base part
+// (-1)^popc(base & yz) and a register pattern p over the pair index k (host
+// packed into .flip), so each term costs one Walsh sum
+// W_p = sum_k (-1)^popc(k & p) v_k with compile-time signs, then
+// cb s_base (W + sigma conj W) as in k_expect_flip.
+constexpr int kRegBits = 4, kRegAmps = 1 << kRegBits;
+constexpr int kMultiMaxGroups = 32, kMultiMaxTerms = 128;
+
+struct MultiPass {
+  uint32_t rb[kRegBits];                // register bits, ascending, all >= 5
+  uint32_t n_groups;
+  uint32_t goff[kMultiMaxGroups + 1];   // group j's terms: [goff[j], goff[j + 1])
+  uint64_t flip[kMultiMaxGroups];
+  uint32_t im_groups;  // bit j: group j has a term with sigma = -1 (needs Im v)
+};
+
+// index bits of register slot r (r compile time after unrolling)
+__device__ __forceinline__ uint64_t reg_offset(int r, const uint64_t (&rb)[kRegBits]) {
+  uint64_t m = 0;
+#pragma unroll
+  for (int j = 0; j < kRegBits; ++j)
+    if (r & (1 << j)) m |= rb[j];
+  return m;
+}
+
+// x with its sign flipped when bit is set (xor on the sign bit: no select,
+// no multiply)
+__device__ __forceinline__ double flip_sign(double x, uint32_t bit) {
+  return __hiloint2double(__double2hiint(x) ^ static_cast<int>(bit << 31), __double2loint(x));
+}
+
+// W_p = sum_k (-1)^popc(k & p) v_k over NP pairs; p = 0 (no Z/Y on the
+// register bits, e.g. every TFIM term) is a plain sum
+template <int NP>
+__device__ __forceinline__ double walsh(const double (&v)[NP], uint32_t p) {
+  double w = 0.0;
+  if (p == 0) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) w += v[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) w += flip_sign(v[k], __popc(k & p) & 1u);
+  }
+  return w;
+}
+
+// The terms of one group from its 8 pair products v_k: each term adds
+// cb s_base (W + sigma conj W) (k_expect_flip's pair formula summed over k).
+// `neg` flips s_base for the lanes of a lane-pair group that hold the side-1
+// amplitudes (see multi_group_lane).
+__device__ __forceinline__ void multi_terms(const double (&vr)[kRegAmps / 2], const double (&vi)[kRegAmps / 2],
+                                            bool need_im, uint64_t base, bool side, const MaskTerm* st,
+                                            const double* sig, uint32_t t0, uint32_t t1, double& acc_re,
+                                            double& acc_im) {
+  for (uint32_t t = t0; t < t1; ++t) {
+    const MaskTerm m = st[t];
+    const uint32_t pk = static_cast<uint32_t>(m.flip) & (kRegAmps / 2 - 1);
+    double sb = parity_sign(base & m.yz);
+    if (side && ((sig[t] < 0.0) != (((m.flip >> (kRegBits - 1)) & 1u) != 0))) sb = -sb;
+    if (sig[t] > 0.0) {  // cb s (W + conj W) = cb s 2 Re W
+      const double w = 2.0 * sb * walsh<kRegAmps / 2>(vr, pk);
+      acc_re += m.cb_re * w;
+      acc_im += m.cb_im * w;
+    } else if (need_im) {  // cb s (W - conj W) = cb s 2i Im W
+      const double w = 2.0 * sb * walsh<kRegAmps / 2>(vi, pk);
+      acc_re -= m.cb_im * w;
+      acc_im += m.cb_re * w;
+    }
+  }
+}
+
+// A group with register flip pattern FR != 0 (compile time: partners are
+// fixed registers; f's top bit is a register bit, so the pairs are the 8
+// slots with that bit clear) and lane pattern fl (partner lane via
+// __shfl_xor, every lane joins).
+template <int FR, typename A>
+__device__ __forceinline__ void multi_group(const A (&x)[kRegAmps], uint32_t fl, bool need_im, uint64_t base,
+                                            const MaskTerm* st, const double* sig, uint32_t t0, uint32_t t1,
+                                            double& acc_re, double& acc_im) {
+  constexpr int top = 31 - __builtin_clz((unsigned)FR);
+  double vr[kRegAmps / 2], vi[kRegAmps / 2];
+  int k = 0;
+#pragma unroll
+  for (int r = 0; r < kRegAmps; ++r) {
+    if ((r >> top) & 1) continue;
+    A y = x[r ^ FR];
+    if (fl) {
+      y.x = __shfl_xor_sync(0xffffffffu, y.x, fl);
+      y.y = __shfl_xor_sync(0xffffffffu, y.y, fl);
+    }
+    vr[k] = __fma_rn((double)x[r].x, (double)y.x, (double)x[r].y * (double)y.y);
+    vi[k] = __fma_rn((double)x[r].x, (double)y.y, -((double)x[r].y * (double)y.x));
+    ++k;
+  }
+  multi_terms(vr, vi, need_im, base, false, st, sig, t0, t1, acc_re, acc_im);
+}
+
+// Lane-only flip (FR = 0): the lane whose top flip bit is clear ("side 0")
+// takes the pairs of slots 0..7, its partner ("side 1") those of slots
+// 8..15; one shuffle per slot serves both (each sends what the other needs).
+// v_k is always conj(side-0 amplitude) * side-1 amplitude, and side-1 lanes
+// evaluate the side-0 sign: s(base ^ fl) = s(base) sigma (f = fl), times the
+// pattern's bit 3 for slots k + 8.
+template <typename A>
+__device__ __forceinline__ void multi_group_lane(const A (&x)[kRegAmps], uint32_t fl, bool side, bool need_im,
+                                                 uint64_t base, const MaskTerm* st, const double* sig, uint32_t t0,
+                                                 uint32_t t1, double& acc_re, double& acc_im) {
+  double vr[kRegAmps / 2], vi[kRegAmps / 2];
+#pragma unroll
+  for (int k = 0; k < kRegAmps / 2; ++k) {
+    const A own = side ? x[k + kRegAmps / 2] : x[k];
+    A y = side ? x[k] : x[k + kRegAmps / 2];
+    y.x = __shfl_xor_sync(0xffffffffu, y.x, fl);
+    y.y = __shfl_xor_sync(0xffffffffu, y.y, fl);
+    vr[k] = __fma_rn((double)own.x, (double)y.x, (double)own.y * (double)y.y);
+    vi[k] = flip_sign(__fma_rn((double)own.x, (double)y.y, -((double)own.y * (double)y.x)), side ? 1u : 0u);
+  }
+  multi_terms(vr, vi, need_im, base, side, st, sig, t0, t1, acc_re, acc_im);
+}
+
+template <typename A, int... FR>
+__device__ __forceinline__ void multi_dispatch(uint32_t fr, std::integer_sequence<int, FR...>,
+                                               const A (&x)[kRegAmps], uint32_t fl, bool need_im, uint64_t base,
+                                               const MaskTerm* st, const double* sig, uint32_t t0, uint32_t t1,
+                                               double& acc_re, double& acc_im) {
+  ((fr == (uint32_t)(FR + 1) ? multi_group<FR + 1>(x, fl, need_im, base, st, sig, t0, t1, acc_re, acc_im) : void()),
+   ...);
+}
+
+// grid = (blocks, batch); partials[(entry * G + slot) * stride + block].
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 2) k_expect_multi(const typename V2<T>::type* __restrict__ a, uint32_t n,
+                                                              const MaskTerm* __restrict__ terms, const MultiPass mp,
+                                                              double* __restrict__ partials, uint32_t G,
+                                                              uint32_t slot, uint32_t stride) {
+  using A = typename V2<T>::type;
+  __shared__ MaskTerm st[kMultiMaxTerms];
+  __shared__ double sig[kMultiMaxTerms];
+  for (uint32_t j = 0; j < mp.n_groups; ++j)
+    for (uint32_t t = mp.goff[j] + threadIdx.x; t < mp.goff[j + 1]; t += kThreads) {
+      st[t] = terms[t];
+      sig[t] = parity_sign(mp.flip[j] & terms[t].yz);
+    }
+  __syncthreads();
+  const uint32_t b = blockIdx.y, lane = threadIdx.x & 31;
+  const uint64_t n_bases = uint64_t{1} << (n - kRegBits);
+  const A* s = a + ((uint64_t)b << n);
+  uint64_t rmask[kRegBits];
+#pragma unroll
+  for (int j = 0; j < kRegBits; ++j) rmask[j] = uint64_t{1} << mp.rb[j];
+  double acc_re = 0.0, acc_im = 0.0;
+  const uint64_t stride_k = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t k = (uint64_t)blockIdx.x * kThreads + threadIdx.x; k < n_bases; k += stride_k) {
+    uint64_t base = k;
+#pragma unroll
+    for (int j = 0; j < kRegBits; ++j) base = insert_zero(base, mp.rb[j]);
+    A x[kRegAmps];
+#pragma unroll
+    for (int r = 0; r < kRegAmps; ++r) x[r] = s[base | reg_offset(r, rmask)];
+    for (uint32_t g = 0; g < mp.n_groups; ++g) {
+      const uint64_t f = mp.flip[g];
+      const uint32_t fl = static_cast<uint32_t>(f & 31u);
+      uint32_t fr = 0;
+#pragma unroll
+      for (int j = 0; j < kRegBits; ++j)
+        if ((f >> mp.rb[j]) & 1u) fr |= 1u << j;
+      const bool need_im = (mp.im_groups >> g) & 1u;  // any term with sigma = -1
+      if (fr) {
+        multi_dispatch(fr, std::make_integer_sequence<int, kRegAmps - 1>{}, x, fl, need_im, base, st, sig,
+                       mp.goff[g], mp.goff[g + 1], acc_re, acc_im);
+      } else {
+        const bool side = ((lane >> (31 - __clz(fl))) & 1u) != 0;
+        multi_group_lane(x, fl, side, need_im, base, st, sig, mp.goff[g], mp.goff[g + 1], acc_re, acc_im);
+      }
+    }
+  }
+  const double2 acc = block_sum(make_double2(acc_re, acc_im));
+  if (threadIdx.x == 0) {
+    const size_t idx = ((size_t)b * G + slot) * stride + blockIdx.x;
+    partials[2 * idx] = acc.x;
+    partials[2 * idx + 1] = acc.y;
   }
 }
 
@@ -518,6 +834,161 @@ void ensure_terms(vqf_statevector* sv, size_t bytes) {
   sv->terms_cap = bytes;
 }
 
+// Host-side plan of one expectation: which kernel reads the state for each
+// flip group, and the packed term array every kernel indexes into.
+//   diagonal group : k_expect_diag_fact (n >= 11, <= 64 high / mixed terms),
+//                    else k_expect_diag_tiled (<= 64 mixed), else k_expect_diag
+//   flip groups    : packed into k_expect_multi passes when their flip bits
+//                    above bit 4 number <= 4 (first fit in group order), else
+//                    one k_expect_flip pass each
+struct MultiLaunch {
+  MultiPass mp{};
+  uint64_t rset = 0;
+  uint32_t first_group = 0, term_base = 0;
+  std::vector<uint32_t> groups;
+};
+
+struct ExpPlan {
+  enum DiagMode { DIAG_NONE, DIAG_FACT, DIAG_TILED, DIAG_PLAIN } diag = DIAG_NONE;
+  std::vector<MaskTerm> all;  // h.terms, then per-kernel repacked term lists
+  uint32_t B = 0, o_lo = 0, o_hi = 0, o_mx = 0, n_lo = 0, n_hi = 0, n_mx = 0;  // tiled split
+  DiagSplit ds{};
+  uint32_t o_flo = 0, o_fhi = 0, o_fmx = 0;  // factorised split
+  std::vector<MultiLaunch> multi;
+  std::vector<uint32_t> single;  // flip groups read by their own k_expect_flip pass
+  uint32_t state_passes() const {
+    return (diag != DIAG_NONE ? 1u : 0u) + static_cast<uint32_t>(multi.size() + single.size());
+  }
+};
+
+ExpPlan plan_expectation(const CompiledHam& h, uint32_t n) {
+  ExpPlan pl;
+  const uint32_t G = static_cast<uint32_t>(h.group_flip.size());
+  pl.all = h.terms;
+  if (G > 0 && h.group_offset[1] > h.group_offset[0]) {
+    // tiled split: support all below / all above the 2048-amplitude tile, mixed
+    pl.B = std::min<uint32_t>(n, 11);
+    const uint64_t lo_mask = (uint64_t{1} << pl.B) - 1;
+    std::vector<MaskTerm> lo, hi, mx;
+    for (uint32_t t = h.group_offset[0]; t < h.group_offset[1]; ++t) {
+      const MaskTerm& m = h.terms[t];
+      if ((m.yz & ~lo_mask) == 0) lo.push_back(m);
+      else if ((m.yz & lo_mask) == 0) hi.push_back(m);
+      else mx.push_back(m);
+    }
+    pl.o_lo = static_cast<uint32_t>(pl.all.size());
+    pl.all.insert(pl.all.end(), lo.begin(), lo.end());
+    pl.o_hi = static_cast<uint32_t>(pl.all.size());
+    pl.all.insert(pl.all.end(), hi.begin(), hi.end());
+    pl.o_mx = static_cast<uint32_t>(pl.all.size());
+    pl.all.insert(pl.all.end(), mx.begin(), mx.end());
+    pl.n_lo = static_cast<uint32_t>(lo.size());
+    pl.n_hi = static_cast<uint32_t>(hi.size());
+    pl.n_mx = static_cast<uint32_t>(mx.size());
+    pl.diag = mx.size() <= 64 ? ExpPlan::DIAG_TILED : ExpPlan::DIAG_PLAIN;
+    // factorised split: mixed terms re-packed as {flip = v, yz = (yz_hi << 8) | yz[0..8)}, sorted by v
+    if (n >= kDiagB) {
+      const uint64_t fmask = (uint64_t{1} << kDiagB) - 1;
+      std::vector<MaskTerm> f_lo, f_hi, f_mx;
+      for (uint32_t t = h.group_offset[0]; t < h.group_offset[1]; ++t) {
+        const MaskTerm& m = h.terms[t];
+        if ((m.yz & ~fmask) == 0) f_lo.push_back(m);
+        else if ((m.yz & fmask) == 0) f_hi.push_back(m);
+        else f_mx.push_back(MaskTerm{(m.yz >> 8) & 7, ((m.yz >> kDiagB) << 8) | (m.yz & 0xff), m.cb_re, m.cb_im});
+      }
+      if (f_hi.size() <= 64 && f_mx.size() <= 64) {
+        std::stable_sort(f_mx.begin(), f_mx.end(),
+                         [](const MaskTerm& x, const MaskTerm& y) { return x.flip < y.flip; });
+        pl.ds.n_lo = static_cast<uint32_t>(f_lo.size());
+        pl.ds.n_hi = static_cast<uint32_t>(f_hi.size());
+        pl.ds.n_mx = static_cast<uint32_t>(f_mx.size());
+        for (uint32_t v = 0, j = 0; v <= 8; ++v) {
+          while (j < f_mx.size() && f_mx[j].flip < v) ++j;
+          pl.ds.mx_off[v] = j;
+        }
+        pl.o_flo = static_cast<uint32_t>(pl.all.size());
+        pl.all.insert(pl.all.end(), f_lo.begin(), f_lo.end());
+        pl.o_fhi = static_cast<uint32_t>(pl.all.size());
+        pl.all.insert(pl.all.end(), f_hi.begin(), f_hi.end());
+        pl.o_fmx = static_cast<uint32_t>(pl.all.size());
+        pl.all.insert(pl.all.end(), f_mx.begin(), f_mx.end());
+        pl.diag = ExpPlan::DIAG_FACT;
+      }
+    }
+  }
+  for (uint32_t g = 1; g < G; ++g) {
+    const uint32_t cnt = h.group_offset[g + 1] - h.group_offset[g];
+    if (cnt == 0) continue;
+    const uint64_t out = h.group_flip[g] & ~uint64_t{31};
+    if (n < 5 + kRegBits || cnt > (uint32_t)kMultiMaxTerms || __builtin_popcountll(out) > kRegBits) {
+      pl.single.push_back(g);
+      continue;
+    }
+    MultiLaunch* dst = nullptr;
+    for (MultiLaunch& ml : pl.multi) {
+      uint32_t terms = 0;
+      for (uint32_t q : ml.groups) terms += h.group_offset[q + 1] - h.group_offset[q];
+      if (__builtin_popcountll(ml.rset | out) <= kRegBits && ml.groups.size() < (size_t)kMultiMaxGroups &&
+          terms + cnt <= (uint32_t)kMultiMaxTerms) {
+        dst = &ml;
+        break;
+      }
+    }
+    if (dst == nullptr) {
+      pl.multi.emplace_back();
+      dst = &pl.multi.back();
+      dst->first_group = g;
+    }
+    dst->rset |= out;
+    dst->groups.push_back(g);
+  }
+  for (MultiLaunch& ml : pl.multi) {
+    for (uint32_t bit = 5; bit < n && __builtin_popcountll(ml.rset) < kRegBits; ++bit) ml.rset |= uint64_t{1} << bit;
+    uint32_t j = 0;
+    for (uint32_t bit = 5; bit < n; ++bit)
+      if ((ml.rset >> bit) & 1u) ml.mp.rb[j++] = bit;
+    ml.term_base = static_cast<uint32_t>(pl.all.size());
+    ml.mp.n_groups = static_cast<uint32_t>(ml.groups.size());
+    ml.mp.goff[0] = 0;
+    for (uint32_t q = 0; q < ml.groups.size(); ++q) {
+      const uint32_t g = ml.groups[q];
+      const uint64_t f = h.group_flip[g];
+      ml.mp.flip[q] = f;
+      uint32_t fr = 0;
+      for (uint32_t j = 0; j < (uint32_t)kRegBits; ++j)
+        if ((f >> ml.mp.rb[j]) & 1u) fr |= 1u << j;
+      const uint32_t top = fr ? 31u - __builtin_clz(fr) : 0u;
+      for (uint32_t t = h.group_offset[g]; t < h.group_offset[g + 1]; ++t) {
+        // yz on the register bits as a pattern over the pair index k: all
+        // four bits when the pairs are lane pairs, else the three bits left
+        // after removing f's top register bit (always clear on the pair side)
+        MaskTerm m = h.terms[t];
+        uint32_t p = 0;
+        for (uint32_t j = 0; j < (uint32_t)kRegBits; ++j)
+          if ((m.yz >> ml.mp.rb[j]) & 1u) p |= 1u << j;
+        if (fr) p = (p & ((1u << top) - 1)) | ((p >> (top + 1)) << top);
+        m.flip = p;  // (base has zeros on R, so popc(base & yz) skips the register part)
+        if (__builtin_popcountll(f & m.yz) & 1) ml.mp.im_groups |= 1u << q;
+        pl.all.push_back(m);
+      }
+      ml.mp.goff[q + 1] = static_cast<uint32_t>(pl.all.size()) - ml.term_base;
+    }
+  }
+  return pl;
+}
+
+template <typename K>
+uint32_t resident_grid(K kernel, uint32_t cap, uint64_t need) {
+  // one resident wave: grid = SMs x CTAs per SM (no tail), capped by the
+  // partial-sum stride and by the work
+  int occ = 0, dev = 0, sms = 148;
+  VQF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0));
+  VQF_CUDA(cudaGetDevice(&dev));
+  VQF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  return static_cast<uint32_t>(
+      std::max<uint64_t>(1, std::min<uint64_t>({(uint64_t)cap, need, (uint64_t)std::max(occ, 1) * sms})));
+}
+
 template <typename T>
 void expectation_t(vqf_statevector* sv, const CompiledHam& h, double* dev_out) {
   using A = typename V2<T>::type;
@@ -529,45 +1000,55 @@ void expectation_t(vqf_statevector* sv, const CompiledHam& h, double* dev_out) {
   const uint32_t nb = std::max(nb_diag, nb_flip);
   ensure_partials(sv, 2 * (size_t)sv->batch * G * nb);
   VQF_CUDA(cudaMemsetAsync(sv->partials, 0, 2 * sizeof(double) * sv->batch * G * nb, sv->stream));
-  // Diagonal group split for the tiled kernel (k_expect_diag_tiled): terms
-  // whose Z/Y support is all below / all above the tile width, and mixed.
-  const uint32_t B = std::min<uint32_t>(n, 11);  // 2048-amplitude tiles, 32 KB table
-  const uint64_t lo_mask = (uint64_t{1} << B) - 1;
-  std::vector<MaskTerm> all = h.terms, lo, hi, mx;
-  for (uint32_t t = h.group_offset[0]; t < h.group_offset[1]; ++t) {
-    const MaskTerm& m = h.terms[t];
-    if ((m.yz & ~lo_mask) == 0) lo.push_back(m);
-    else if ((m.yz & lo_mask) == 0) hi.push_back(m);
-    else mx.push_back(m);
-  }
-  const bool tiled = mx.size() <= 64;
-  const uint32_t o_lo = static_cast<uint32_t>(all.size());
-  all.insert(all.end(), lo.begin(), lo.end());
-  const uint32_t o_hi = static_cast<uint32_t>(all.size());
-  all.insert(all.end(), hi.begin(), hi.end());
-  const uint32_t o_mx = static_cast<uint32_t>(all.size());
-  all.insert(all.end(), mx.begin(), mx.end());
-  ensure_terms(sv, std::max<size_t>(1, all.size()) * sizeof(MaskTerm));
-  if (!all.empty())
-    VQF_CUDA(cudaMemcpyAsync(sv->terms_dev, all.data(), all.size() * sizeof(MaskTerm), cudaMemcpyHostToDevice,
+  const ExpPlan pl = plan_expectation(h, n);
+  ensure_terms(sv, std::max<size_t>(1, pl.all.size()) * sizeof(MaskTerm));
+  if (!pl.all.empty())
+    VQF_CUDA(cudaMemcpyAsync(sv->terms_dev, pl.all.data(), pl.all.size() * sizeof(MaskTerm), cudaMemcpyHostToDevice,
                              sv->stream));
   const MaskTerm* td = static_cast<const MaskTerm*>(sv->terms_dev);
-  for (uint32_t g = 0; g < G; ++g) {
-    const uint32_t t0 = h.group_offset[g], cnt = h.group_offset[g + 1] - t0;
-    if (cnt == 0) continue;
-    if (g == 0 && tiled) {
-      k_expect_diag_tiled<T><<<dim3(nb, sv->batch), kThreads, sizeof(double2) << B, sv->stream>>>(
-          a, n, B, td + o_lo, static_cast<uint32_t>(lo.size()), td + o_hi, static_cast<uint32_t>(hi.size()),
-          td + o_mx, static_cast<uint32_t>(mx.size()), sv->partials, G);
-    } else if (g == 0) {
-      k_expect_diag<T><<<dim3(nb, sv->batch), kThreads, 0, sv->stream>>>(a, n, td + t0, cnt, sv->partials, G, 0);
-    } else {
-      const uint64_t f = h.group_flip[g];
-      const uint32_t hb = 63 - __builtin_clzll(f);
-      k_expect_flip<T><<<dim3(nb, sv->batch), kThreads, 0, sv->stream>>>(a, n, f, hb, td + t0, cnt, sv->partials,
-                                                                         G, g);
+  const dim3 grid(nb, sv->batch);
+  switch (pl.diag) {
+    case ExpPlan::DIAG_FACT: {
+      static thread_local uint32_t nbf = 0, nbf_n = 0;
+      if (nbf_n != n) {
+        nbf = resident_grid(k_expect_diag_fact<T>, nb, uint64_t{1} << (n - kDiagB));
+        nbf_n = n;
+      }
+      k_expect_diag_fact<T><<<dim3(nbf, sv->batch), kThreads, 0, sv->stream>>>(
+          a, n, td + pl.o_flo, td + pl.o_fhi, td + pl.o_fmx, pl.ds, sv->partials, G, nb);
+      VQF_LAUNCHED();
+      break;
     }
+    case ExpPlan::DIAG_TILED:
+      k_expect_diag_tiled<T><<<grid, kThreads, sizeof(double2) << pl.B, sv->stream>>>(
+          a, n, pl.B, td + pl.o_lo, pl.n_lo, td + pl.o_hi, pl.n_hi, td + pl.o_mx, pl.n_mx, sv->partials, G);
+      VQF_LAUNCHED();
+      break;
+    case ExpPlan::DIAG_PLAIN:
+      k_expect_diag<T><<<grid, kThreads, 0, sv->stream>>>(a, n, td + h.group_offset[0],
+                                                          h.group_offset[1] - h.group_offset[0], sv->partials, G, 0);
+      VQF_LAUNCHED();
+      break;
+    case ExpPlan::DIAG_NONE: break;
+  }
+  for (const uint32_t g : pl.single) {
+    const uint32_t t0 = h.group_offset[g], cnt = h.group_offset[g + 1] - t0;
+    const uint64_t f = h.group_flip[g];
+    const uint32_t hb = 63 - __builtin_clzll(f);
+    k_expect_flip<T><<<grid, kThreads, 0, sv->stream>>>(a, n, f, hb, td + t0, cnt, sv->partials, G, g);
     VQF_LAUNCHED();
+  }
+  if (!pl.multi.empty()) {
+    static thread_local uint32_t nbm = 0, nbm_n = 0;
+    if (nbm_n != n) {
+      nbm = resident_grid(k_expect_multi<T>, nb, ((uint64_t{1} << (n - kRegBits)) + kThreads - 1) / kThreads);
+      nbm_n = n;
+    }
+    for (const MultiLaunch& ml : pl.multi) {
+      k_expect_multi<T><<<dim3(nbm, sv->batch), kThreads, 0, sv->stream>>>(a, n, td + ml.term_base, ml.mp,
+                                                                            sv->partials, G, ml.first_group, nb);
+      VQF_LAUNCHED();
+    }
   }
   k_final_sum<<<sv->batch, kThreads, 0, sv->stream>>>(sv->partials, G * nb, dev_out);
   VQF_LAUNCHED();
@@ -835,6 +1316,20 @@ int vqf_expectation_complex(vqf_sv sv, const vqf_hamiltonian* h, double* out) {
     const CompiledHam c = compile_hamiltonian(h);
     VQF_CUDA(cudaSetDevice(sv->device));
     sv_expectation(sv, c, out);
+  });
+}
+
+int vqf_expectation_plan(const vqf_hamiltonian* h, uint32_t* state_passes, uint32_t* flip_groups,
+                         uint32_t* multi_passes) {
+  return guarded([&] {
+    if (h == nullptr) throw_invalid("null hamiltonian");
+    const CompiledHam c = compile_hamiltonian(h);
+    const ExpPlan pl = plan_expectation(c, h->n_qubits);
+    uint32_t groups = 0;
+    for (size_t g = 1; g < c.group_flip.size(); ++g) groups += c.group_offset[g + 1] > c.group_offset[g] ? 1 : 0;
+    if (state_passes) *state_passes = pl.state_passes();
+    if (flip_groups) *flip_groups = groups;
+    if (multi_passes) *multi_passes = static_cast<uint32_t>(pl.multi.size());
   });
 }
 

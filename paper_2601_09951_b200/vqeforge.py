@@ -236,6 +236,16 @@ def expectation(psi: StateVector, h: QubitHamiltonian):
     return float(out[0]) if psi.batch == 1 else out
 
 
+def expectation_plan(h: QubitHamiltonian) -> dict:
+    """How expectation() reads the state for h: HBM passes over the state,
+    distinct flip groups (the reference's per-group passes, statevector.hpp:
+    235-241) and the multi-group register passes among them.  Host only."""
+    keep, hs = h.as_c()
+    sp, fg, mp = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    check(lib.vqf_expectation_plan(C.byref(hs), C.byref(sp), C.byref(fg), C.byref(mp)))
+    return {"state_passes": sp.value, "flip_groups": fg.value, "multi_passes": mp.value}
+
+
 # ------------------------------------------------------------------- vqe
 H2_DOUBLE_EXCITATION, HARDWARE_EFFICIENT = 0, 1
 

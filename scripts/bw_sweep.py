@@ -72,12 +72,14 @@ def main():
             gate(V.Gate.double_excitation(0.2, 0, 1, 2, 3), S // 4)
             gate(V.Gate.double_excitation(0.2, n - 4, n - 3, n - 2, n - 1), S // 4)
             gate(V.Gate.single_excitation(0.2, 2, n - 2), S)
+            plans = {}
             for name, h, groups in [
                 ("zsum", V.build_z_sum(n), 1),
                 ("tfim", V.build_tfim(n, 1.0, 1.0), n + 1),
             ]:
                 t = timed(stream, lambda: V.expectation(psi, h), reps=3)
                 rows.append(("expect:" + name, (), S * groups, t))
+                plans["expect:" + name] = V.expectation_plan(h)
             import random
 
             rh = random_hamiltonian(random.Random(20260804), n, 32)
@@ -88,10 +90,15 @@ def main():
                 flips.add(f)
             t = timed(stream, lambda: V.expectation(psi, hv), reps=3)
             rows.append(("expect:random32", (), S * len(flips | {0}), t))
+            plans["expect:random32"] = V.expectation_plan(hv)
         for kind, wires, alg, t in rows:
             gbs = alg / t / 1e9
             rec = {"n": n, "dtype": "f32" if f32 else "f64", "kernel": kind, "wires": list(wires), "alg_bytes": alg,
                    "ms": t * 1e3, "GBps": gbs, "frac_of_measured_peak": gbs / P}
+            if kind in plans:  # alg_bytes = S per flip group (+ diagonal); the engine reads the state per pass
+                rec["plan"] = plans[kind]
+                rec["pass_GBps"] = plans[kind]["state_passes"] * S / t / 1e9
+                rec["pass_frac"] = rec["pass_GBps"] / P
             out.append(rec)
             print(json.dumps(rec), flush=True)
         del psi

@@ -27,13 +27,17 @@ def main():
     elif what == "gates":
         n = int(sys.argv[2])
         psi = V.StateVector(n)
-        V.apply_circuit(psi, [V.Gate.ry(0.3, q) for q in (0, 1, n // 2, n - 2, n - 1)])
-        V.apply_circuit(psi, [V.Gate.cnot(0, 1), V.Gate.cnot(n - 2, n - 1), V.Gate.double_excitation(0.4, 0, 1, 2, 3)])
+        # per-gate kernels (apply_gate), not the fused tile path
+        for g in [V.Gate.ry(0.3, q) for q in (0, 1, n // 2, n - 2, n - 1)] + [
+                V.Gate.cnot(0, 1), V.Gate.cnot(n - 2, n - 1), V.Gate.double_excitation(0.4, 0, 1, 2, 3),
+                V.Gate.double_excitation(0.4, n - 4, n - 3, n - 2, n - 1), V.Gate.single_excitation(0.4, 2, n - 2)]:
+            V.apply_gate(psi, g)
     elif what == "expect":
         n = int(sys.argv[2])
         psi = V.StateVector(n)
         V.apply_circuit(psi, [V.Gate.ry(0.3, q) for q in range(n)])
         print(V.expectation(psi, V.build_tfim(n, 1.0, 1.0)))
+        print(V.expectation(psi, V.build_z_sum(n)))
     else:
         raise SystemExit(f"unknown target {what}")
 

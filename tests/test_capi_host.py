@@ -174,3 +174,25 @@ def test_speedup_arithmetic(V):
         V.measured_speedup(0.0, 1.0)
     with pytest.raises(ValueError):
         V.amdahl_speedup(1.1, 4)
+
+
+def test_expectation_plan_packs_flip_groups(V):
+    """Host plan of the expectation (no GPU): TFIM's n single-X flip groups
+    share register passes four high bits at a time plus every lane-bit
+    group; a Z-only sum is one diagonal pass; dense random strings fall back
+    to one pass per group."""
+    for n in [9, 12, 20, 30]:
+        p = V.expectation_plan(V.build_tfim(n, 1.0, 1.0))
+        assert p["flip_groups"] == n
+        high = n - 5  # X on index bits 5..n-1
+        assert p["multi_passes"] == -(-high // 4)
+        assert p["state_passes"] == 1 + p["multi_passes"]
+    assert V.expectation_plan(V.build_z_sum(24)) == {"state_passes": 1, "flip_groups": 0, "multi_passes": 0}
+    # below 9 qubits there are no register passes: one pass per group
+    p = V.expectation_plan(V.build_tfim(6, 1.0, 1.0))
+    assert p == {"state_passes": 7, "flip_groups": 6, "multi_passes": 0}
+    rh = random_hamiltonian(random.Random(20260804), 26, 32)
+    h = V.canonicalize(V.QubitHamiltonian(26, [V.PauliTerm(c, a) for c, a in rh.terms]))
+    p = V.expectation_plan(h)
+    assert p["flip_groups"] >= 28 and p["multi_passes"] <= 2
+    assert p["flip_groups"] - 2 <= p["state_passes"] <= p["flip_groups"] + 1

@@ -118,7 +118,7 @@ def test_gate_validation(gpu):
         V.apply_gate(psi, V.Gate(1, 0.1, (0, 1)))
 
 
-@pytest.mark.parametrize("n", [1, 4, 6, 9, 12])
+@pytest.mark.parametrize("n", [1, 4, 6, 9, 11, 12, 14, 17])
 def test_expectation_matches_oracle(gpu, orc, n):
     V = gpu
     rng = np.random.default_rng(300 + n)
@@ -146,6 +146,54 @@ def test_expectation_tfim_and_diagonal(gpu, orc):
     assert abs(V.expectation(ones, V.build_z_sum(4)) + 4.0) < 1e-15
     with pytest.raises(ValueError, match="qubit count mismatch"):
         V.expectation(V.StateVector(2), V.QubitHamiltonian(3, [V.PauliTerm(1.0, [(0, 3)])]))
+
+
+@pytest.mark.parametrize("n,n_terms", [(11, 30), (13, 60), (15, 150)])
+def test_expectation_diagonal_factorised_pass(gpu, orc, n, n_terms):
+    # Z-only strings exercise every split of the factorised diagonal pass:
+    # support below bit 11, at/above bit 11, and straddling it with every
+    # bits-8..10 pattern; 150 terms overflow the 64-term tables (fallback).
+    V = gpu
+    pr = random.Random(77 * n + n_terms)
+    terms = []
+    for t in range(n_terms):
+        k = 1 + pr.randrange(min(n, 6))
+        wires = sorted(pr.sample(range(n), k))
+        terms.append((pr.uniform(-2, 2), [(w, 3) for w in wires]))
+    terms += [(0.5, [(n - 1 - b, 3) for b in range(8, min(n, 11))]), (-0.25, [(0, 3), (n - 1, 3)])]
+    h = orc.canonicalize(Ham(n, terms))
+    psi0 = random_state(np.random.default_rng(n), n)
+    psi = V.StateVector(n)
+    psi.amplitudes = psi0
+    assert abs(V.expectation(psi, to_v(V, h)) - orc.expectation(n, psi0, h)) < E_TOL
+
+
+@pytest.mark.parametrize("n,n_terms", [(9, 40), (12, 120), (16, 300)])
+def test_expectation_multi_group_passes(gpu, orc, n, n_terms):
+    # few-body Pauli strings: most flip groups have <= 4 flip bits above the
+    # lane bits and are packed into register-resident multi-group passes;
+    # shared flips with different Z/Y patterns give multi-term groups, and
+    # 300 terms open several passes (first fit) next to per-group fallbacks
+    V = gpu
+    pr = random.Random(4242 + n)
+    terms = []
+    for t in range(n_terms):
+        k = 1 + pr.randrange(4)
+        wires = sorted(pr.sample(range(n), k))
+        terms.append((pr.uniform(-2, 2), [(w, 1 + pr.randrange(3)) for w in wires]))
+    for t in range(n_terms // 10):  # repeat flips with other Z patterns
+        c, axes = terms[pr.randrange(len(terms))]
+        extra = [w for w in range(n) if w not in [q for q, _ in axes]]
+        axes = sorted(axes + [(pr.choice(extra), 3)]) if extra else axes
+        terms.append((pr.uniform(-1, 1), axes))
+    h = orc.canonicalize(Ham(n, terms))
+    psi0 = random_state(np.random.default_rng(n + 1), n)
+    psi = V.StateVector(n)
+    psi.amplitudes = psi0
+    assert abs(V.expectation(psi, to_v(V, h)) - orc.expectation(n, psi0, h)) < E_TOL
+    psi32 = V.StateVector(n, dtype="f32")
+    psi32.amplitudes = psi0
+    assert abs(V.expectation(psi32, to_v(V, h)) - orc.expectation(n, psi0, h)) < 1e-5 * max(1.0, len(terms) / 10)
 
 
 def test_expectation_imaginary_residue_raises(gpu):
