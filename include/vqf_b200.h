@@ -275,6 +275,12 @@ int vqf_expectation_complex(vqf_sv sv, const vqf_hamiltonian* h, double* out);
  * two states of one register (batch entry 0), as (re, im): the shard-pair
  * term of a distributed expectation whose Pauli string flips global wires. */
 int vqf_cross_expectation(vqf_sv a, vqf_sv b, const vqf_hamiltonian* h, double* out);
+/* How vqf_apply_circuit would run `gates` on an n-qubit state of `dtype`
+ * (host only, no device work): passes = HBM passes over the state (fused
+ * shared-memory tile passes + single-gate launches), fused_ops = register
+ * ops inside those passes (each one shared-memory round trip of a tile). */
+int vqf_circuit_plan(uint32_t n_qubits, int32_t dtype, const vqf_gate* gates, uint32_t n_gates, uint32_t* passes,
+                     uint32_t* fused_ops);
 /* How vqf_expectation reads the state for h (host only, no device work):
  * state_passes = HBM passes over the state (diagonal pass + one per
  * multi-group pass + one per remaining flip group), flip_groups = distinct

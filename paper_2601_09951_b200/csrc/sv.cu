@@ -1319,6 +1319,28 @@ int vqf_expectation_complex(vqf_sv sv, const vqf_hamiltonian* h, double* out) {
   });
 }
 
+int vqf_circuit_plan(uint32_t n_qubits, int32_t dtype, const vqf_gate* gates, uint32_t n_gates, uint32_t* passes,
+                     uint32_t* fused_ops) {
+  return guarded([&] {
+    if (n_qubits < 1 || n_qubits > 36) throw_invalid("circuit plan: n_qubits must be in [1, 36]");
+    if (dtype != VQF_F64 && dtype != VQF_F32) throw_invalid("circuit plan: unknown dtype");
+    vqf_statevector probe;
+    probe.n_qubits = n_qubits;
+    for (uint32_t i = 0; i < n_gates; ++i) sv_check_gate(&probe, gates[i]);
+    uint32_t p = n_gates, f = 0;
+    if (n_gates > 1) {
+      std::vector<TGate> tg(n_gates);
+      for (uint32_t i = 0; i < n_gates; ++i) {
+        const vqf_gate& g = gates[i];
+        tg[i] = TGate{g.kind, g.n_wires, {g.wires[0], g.wires[1], g.wires[2], g.wires[3]}, -1, 1.0, 0.0};
+      }
+      plan_tile_counts(n_qubits, dtype, tg, &p, &f);
+    }
+    if (passes) *passes = p;
+    if (fused_ops) *fused_ops = f;
+  });
+}
+
 int vqf_expectation_plan(const vqf_hamiltonian* h, uint32_t* state_passes, uint32_t* flip_groups,
                          uint32_t* multi_passes) {
   return guarded([&] {

@@ -16,7 +16,11 @@
 // Per-gate arithmetic is exactly that of the single-gate kernels (sv.cu);
 // commuting gates may be applied in a different order, so amplitudes agree
 // with the unfused path to rounding (~1e-16).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <mutex>
 
 #include "tile.cuh"
 
@@ -24,28 +28,43 @@ namespace vqf {
 
 namespace {
 
-constexpr int kTileThreads = 1024;  // one persistent CTA per SM, 8 warps per SMSP
-constexpr int kMaxOps = 64;  // TileParams stays under the 4 KB kernel-parameter limit
+constexpr int kMaxOps = 64;        // TileParams stays under the 4 KB kernel-parameter limit
 constexpr int kMaxHigh = 6;
-constexpr int kTileBlocks = 148;  // persistent: one CTA per SM
-constexpr int kStages = 3;       // TMA ring depth (3 x 64 KB)
+constexpr int kTileBlocks = 148;   // persistent: one CTA per SM
+constexpr int kStages = 3;         // TMA ring depth (3 x 64 KB)
+constexpr int kMaxFuse = 4;        // local bits of one fused op (16 amplitudes per thread)
+constexpr uint32_t kMatElems = 2560;  // composed fused-op matrices per pass (20 KB of fp64)
+// fp64 passes run 512 threads with fused ops of <= 3 bits (8 amplitudes in
+// registers, <= 128 registers), or 256 threads when a DoubleExcitation needs
+// a 4-bit op; fp32 always 512 threads x <= 4 bits
 
-enum : int32_t { OP_SWAP = 0, OP_ROT = 1 };
-
-struct TileOp {
-  int32_t mode;   // OP_SWAP (X, CNOT) or OP_ROT (RY, DE, SE)
+// One gate inside a fused op: pairs (r | A, r | B) of the op's 2^m register
+// slots, for every r with the bits of A | B clear; ROT: a' = c a - s b,
+// b' = s a + c b (statevector.hpp:160-163, :195-196), else swap.
+//   X / RY on slot bit j : A = 0,        B = 1 << j
+//   CNOT (c, t)          : A = C,        B = C | T
+//   SingleExcitation     : A = 1 << w0,  B = 1 << w1
+//   DoubleExcitation     : A = w0 | w1,  B = w2 | w3
+struct TileSub {
+  uint32_t code;  // (rot << 8) | (A << 4) | B
   int32_t param;  // per-entry (c, s) index or -1
-  uint32_t ma, mb;  // local index patterns of the two amplitudes of a pair
-  uint32_t pos;   // local bit positions, 8 bits each, ascending
-  uint32_t npos;
   double c, s;
 };
 
+// A fused op: m <= 4 local bit positions (ascending, 8 bits each) and its
+// gates [sub0, sub0 + n_sub).  Each thread loads the 2^m amplitudes of one
+// work item into registers, applies all the gates, and stores them back:
+// one shared-memory round trip per op instead of per gate.
+struct TileFop {
+  uint32_t m, pos, sub0, n_sub, uoff;  // uoff: the op's matrix in the composed-matrix area
+};
+
 struct TileParams {
-  uint32_t n, B, k, n_ops, batch;
+  uint32_t n, B, k, n_fops, batch;
   uint32_t hb[kMaxHigh];  // global bit of local bit B + j, ascending
   const double* cs;
-  TileOp ops[kMaxOps];
+  TileFop fops[kMaxOps];
+  TileSub subs[kMaxOps];
 };
 
 template <typename T>
@@ -64,7 +83,7 @@ __device__ __forceinline__ uint64_t insert_zero64(uint64_t k, uint32_t bit) {
   return ((k >> bit) << (bit + 1)) | low;
 }
 
-// ---- TMA bulk-copy helpers (sm_90+ PTX; SASS: UBLKCP / SYNCS)
+// ---- TMA helpers (sm_90+ PTX; SASS: UTMALDG / SYNCS)
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -85,34 +104,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// global -> shared, completion counted on the mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// one 4 KB run (box {128 B, 32 rows, 1}) of the state, 128 B-swizzled into
+// shared memory; completion counted on the mbarrier
+__device__ __forceinline__ void tma_load_run(void* dst, const CUtensorMap* map, int32_t row, int32_t entry,
+                                             uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(0), "r"(row), "r"(entry), "r"(smem_addr(bar))
       : "memory");
 }
-// shared -> global, tracked by bulk groups
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Inserts zero bits at the op's (ascending) local bit positions; npos is
-// 1, 2 or 4 so every case is a fixed shift/mask sequence.
-__device__ __forceinline__ uint32_t ins0(uint32_t r, uint32_t b) { return ((r >> b) << (b + 1)) | (r & ((1u << b) - 1)); }
-__device__ __forceinline__ uint32_t spread(uint32_t r, const TileOp& op) {
-  r = ins0(r, op.pos & 0xffu);
-  if (op.npos == 1) return r;
-  r = ins0(r, (op.pos >> 8) & 0xffu);
-  if (op.npos == 2) return r;
-  r = ins0(r, (op.pos >> 16) & 0xffu);
-  return ins0(r, (op.pos >> 24) & 0xffu);
+// Shared-memory slot of local amplitude L under the TMA 128 B swizzle: the
+// 16-byte chunk index (bits 4..6 of the byte offset) is xor-ed with the
+// 128-byte row index mod 8 (bits 7..9), so amplitudes one row apart land in
+// different banks.
+template <typename T>
+__device__ __forceinline__ uint32_t swz(uint32_t L) {
+  if (sizeof(T) == 8) return L ^ ((L >> 3) & 7u);        // 16 B amplitude = one chunk
+  return L ^ (((L >> 4) & 7u) << 1);                     // 8 B amplitude: chunk = L >> 1
 }
 
 // Global start index of run j (0 <= j < 2^k) of tile `tile`.
@@ -123,37 +133,128 @@ __device__ __forceinline__ uint64_t run_start(const TileParams& p, uint64_t tile
   return base;
 }
 
-// Persistent tile kernel with a kStages-deep TMA ring.  Thread 0 is the
-// copy engine: it keeps kStages - 1 tiles in flight, issuing the 2^k
-// contiguous 2^B-amplitude runs of each as TMA bulk copies (one mbarrier per
-// stage, expect_tx = tile bytes), while all threads apply the pass's gates to
-// the current tile in shared memory; the tile then leaves as bulk stores.
+// Every gate here is a real orthogonal map on its pairs, so a fused op is
+// one real 2^m x 2^m matrix U (row-major, in shared memory) composed once
+// per CTA from its gates and the CTA's batch entry angles: start from the
+// identity and apply each gate to the rows of every column.
 template <typename T>
-__global__ void __launch_bounds__(kTileThreads, 1) k_tile(typename V2<T>::type* __restrict__ a, const TileParams p) {
+__device__ void compose_fops(const TileParams& p, T* U) {
+  for (uint32_t o = 0; o < p.n_fops; ++o) {
+    const TileFop& f = p.fops[o];
+    const uint32_t d = 1u << f.m;
+    T* u = U + f.uoff;
+    for (uint32_t col = threadIdx.x; col < d; col += blockDim.x) {
+      for (uint32_t r = 0; r < d; ++r) u[r * d + col] = r == col ? T(1) : T(0);
+      for (uint32_t q = 0; q < f.n_sub; ++q) {
+        const TileSub& g = p.subs[f.sub0 + q];
+        double c = g.c, sn = g.s;
+        if (g.param >= 0) {
+          const double* cs = p.cs + 2 * ((size_t)g.param * p.batch + blockIdx.y);
+          c = cs[0];
+          sn = cs[1];
+        }
+        const uint32_t A = (g.code >> 4) & 15u, B = g.code & 15u, S = A | B;
+        for (uint32_t r = 0; r < d; ++r) {
+          if (r & S) continue;
+          const T x = u[(r | A) * d + col], y = u[(r | B) * d + col];
+          if (g.code >> 8) {  // a' = c a - s b, b' = s a + c b (statevector.hpp:160-163, :195-196)
+            u[(r | A) * d + col] = static_cast<T>(c) * x - static_cast<T>(sn) * y;
+            u[(r | B) * d + col] = static_cast<T>(sn) * x + static_cast<T>(c) * y;
+          } else {
+            u[(r | A) * d + col] = y;
+            u[(r | B) * d + col] = x;
+          }
+        }
+      }
+    }
+  }
+}
+
+// One fused op over the whole tile: work item w -> base with zeros at the
+// op's bits; 2^M amplitudes in registers, y = U x with U broadcast from
+// shared memory.  The swizzle is xor-linear and base / slot offsets have
+// disjoint bits, so slot addresses are swz(base) ^ swz(offset).
+template <int M, typename T, int NT>
+__device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, const TileFop& f, const T* U) {
   using A = typename V2<T>::type;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int D = 1 << M;
+  uint32_t pos[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) pos[j] = (f.pos >> (8 * j)) & 0xffu;
+  uint32_t sd[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    uint32_t d = 0;
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+      if (r & (1 << j)) d |= 1u << pos[j];
+    sd[r] = swz<T>(d);
+  }
+  const T* u = U + f.uoff;
+  for (uint32_t w = threadIdx.x; w < (NL >> M); w += NT) {
+    uint32_t base = w;
+#pragma unroll
+    for (int j = 0; j < M; ++j) base = ((base >> pos[j]) << (pos[j] + 1)) | (base & ((1u << pos[j]) - 1));
+    const uint32_t sb = swz<T>(base);
+    A x[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) x[r] = t[sb ^ sd[r]];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      A y;
+      y.x = T(0);
+      y.y = T(0);
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const T m = u[r * D + c];
+        y.x = fma(m, x[c].x, y.x);
+        y.y = fma(m, x[c].y, y.y);
+      }
+      t[sb ^ sd[r]] = y;
+    }
+  }
+}
+
+// Persistent tile kernel with a kStages-deep TMA ring.  Warp 0 keeps
+// kStages - 1 tiles in flight, issuing the 2^k 4 KB runs of each as TMA
+// tensor loads (128 B swizzle, one mbarrier per stage, expect_tx = tile
+// bytes), while all threads apply the pass's fused ops to the current tile
+// in shared memory; the tile then leaves with coalesced 16-byte stores.
+template <typename T, int NT, int MAXM>
+__global__ void __launch_bounds__(NT, 1)
+    k_tile(typename V2<T>::type* __restrict__ a, const __grid_constant__ CUtensorMap map, const TileParams p) {
+  using A = typename V2<T>::type;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 128 B swizzle atoms are 1024 B: align the ring (the launch adds 1 KB
+  // slack); indexing smem_raw keeps the pointer in the shared window (LDS/STS)
+  unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const uint32_t LB = p.B + p.k, NL = 1u << LB;
   const uint32_t run_amps = 1u << p.B, n_runs = 1u << p.k;
   const uint32_t tile_bytes = NL * sizeof(A), run_bytes = run_amps * sizeof(A);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + kStages * (size_t)tile_bytes);
+  const uint32_t amps_per_row = 128 / sizeof(A);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kStages * (size_t)tile_bytes);
+  T* U = reinterpret_cast<T*>(smem + kStages * (size_t)tile_bytes + 64);  // composed fused-op matrices
   __shared__ uint64_t run_off[1 << kMaxHigh];
   A* s = a + ((uint64_t)blockIdx.y << p.n);
   const uint64_t n_tiles = uint64_t{1} << (p.n - LB);
   if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
     for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  compose_fops<T>(p, U);
   __syncthreads();
-  const auto stage_buf = [&](int st) { return reinterpret_cast<A*>(smem_raw + (size_t)st * tile_bytes); };
+  const auto stage_buf = [&](int st) { return reinterpret_cast<A*>(smem + (size_t)st * tile_bytes); };
   // warp 0 issues a tile: lane 0 arms the stage's mbarrier with the tile's
   // byte count, lane j copies run j (the arm and the copies may land in any
   // order: the phase needs both the arrival and the bytes)
   const auto issue_load = [&](uint64_t tile, int st) {
     const uint32_t lane = threadIdx.x;
     if (lane == 0) mbar_expect_tx(&bar[st], tile_bytes);
-    A* dst = stage_buf(st);
+    unsigned char* dst = reinterpret_cast<unsigned char*>(stage_buf(st));
     for (uint32_t j = lane; j < n_runs; j += 32)
-      bulk_g2s(dst + (size_t)j * run_amps, s + run_start(p, tile, j), run_bytes, &bar[st]);
+      tma_load_run(dst + (size_t)j * run_bytes, &map, static_cast<int32_t>(run_start(p, tile, j) / amps_per_row),
+                   static_cast<int32_t>(blockIdx.y), &bar[st]);
   };
   if (threadIdx.x < 32)
     for (int st = 0; st < kStages - 1; ++st) {
@@ -169,46 +270,15 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(typename V2<T>::type* 
     if (threadIdx.x < 32 && ahead < n_tiles) issue_load(ahead, (it + kStages - 1) % kStages);
     mbar_wait(&bar[cur], (it / kStages) & 1u);
     A* t = stage_buf(cur);
-    for (uint32_t o = 0; o < p.n_ops; ++o) {
-      const TileOp op = p.ops[o];
-      T c = static_cast<T>(op.c), sn = static_cast<T>(op.s);
-      if (op.param >= 0) {
-        const double* cs = p.cs + 2 * ((size_t)op.param * p.batch + blockIdx.y);
-        c = static_cast<T>(cs[0]);
-        sn = static_cast<T>(cs[1]);
-      }
-      const uint32_t npairs = NL >> op.npos;
-      // two pairs per thread per step, all four shared-memory loads issued
-      // before any arithmetic (pairs of one op never overlap)
-      for (uint32_t q0 = threadIdx.x; q0 < npairs; q0 += 2 * kTileThreads) {
-        uint32_t ia[2], ib[2];
-        A x[2], y[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const uint32_t r = spread(q0 + u * kTileThreads, op);
-          ia[u] = r | op.ma;
-          ib[u] = r | op.mb;
-          if (q0 + u * kTileThreads < npairs) {
-            x[u] = t[ia[u]];
-            y[u] = t[ib[u]];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (q0 + u * kTileThreads >= npairs) break;
-          if (op.mode == OP_SWAP) {
-            t[ia[u]] = y[u];
-            t[ib[u]] = x[u];
-          } else {  // a' = c a - s b, b' = s a + c b (statevector.hpp:160-163, :195-196)
-            A xa, yb;
-            xa.x = c * x[u].x - sn * y[u].x;
-            xa.y = c * x[u].y - sn * y[u].y;
-            yb.x = sn * x[u].x + c * y[u].x;
-            yb.y = sn * x[u].y + c * y[u].y;
-            t[ia[u]] = xa;
-            t[ib[u]] = yb;
-          }
-        }
+    for (uint32_t o = 0; o < p.n_fops; ++o) {
+      const TileFop f = p.fops[o];
+      switch (f.m) {
+        case 1: run_fop<1, T, NT>(t, NL, f, U); break;
+        case 2: run_fop<2, T, NT>(t, NL, f, U); break;
+        case 3: run_fop<3, T, NT>(t, NL, f, U); break;
+        default:
+          if constexpr (MAXM >= 4) run_fop<4, T, NT>(t, NL, f, U);
+          break;
       }
       __syncthreads();
     }
@@ -216,7 +286,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(typename V2<T>::type* 
     if (threadIdx.x < n_runs) run_off[threadIdx.x] = run_start(p, tile, threadIdx.x);
     __syncthreads();
     const uint32_t low_mask = run_amps - 1;
-    for (uint32_t li = threadIdx.x; li < NL; li += kTileThreads) s[run_off[li >> p.B] | (li & low_mask)] = t[li];
+#pragma unroll 4
+    for (uint32_t li = threadIdx.x; li < NL; li += NT) s[run_off[li >> p.B] | (li & low_mask)] = t[swz<T>(li)];
     __syncthreads();  // buffer free for the stage's next TMA load
   }
 }
@@ -228,13 +299,10 @@ struct Pass {
 
 // Local bit budget: 64 KB of shared memory per tile (kStages tiles resident).
 void tile_shape(uint32_t n, int32_t dtype, uint32_t& B, uint32_t& kmax) {
+  // runs of 1 KB (one TMA box of 8 rows x 128 B): B = 6 (fp64) / 7 (fp32),
+  // leaving 6 gathered high bits per pass
   const uint32_t LB = dtype == VQF_F64 ? 12 : 13;
-  if (n <= LB) {
-    B = n;
-    kmax = 0;
-    return;
-  }
-  B = std::max<uint32_t>(LB - kMaxHigh + 2, 7);  // >= 2 KB contiguous runs (fp64: B = 8)
+  B = std::min<uint32_t>(n, LB - kMaxHigh);
   kmax = std::min<uint32_t>(LB - B, n - B);
 }
 
@@ -263,23 +331,37 @@ std::vector<Pass> schedule(uint32_t n, uint32_t B, uint32_t kmax, const std::vec
   while (remaining) {
     Pass pass;
     bool added = true;
+    // greedy: among ready gates that fit, take the one adding the fewest new
+    // high bits, then sharing the most bits with the pass, then the earliest
+    // (keeps a CNOT chain advancing instead of letting independent RYs claim
+    // the bit budget)
     while (added && pass.gates.size() < static_cast<size_t>(kMaxOps)) {
       added = false;
+      int best = -1, best_new = 1 << 20, best_share = -1;
       for (size_t i = 0; i < G; ++i) {
         if (done[i]) continue;
         bool ready = true;
         for (int pr : preds[i]) ready = ready && done[pr];
         if (!ready) continue;
-        std::vector<uint32_t> u = pass.hbits;
-        for (uint32_t b : high_bits(gates[i]))
-          if (std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
-        if (u.size() > kmax) continue;
-        pass.hbits = u;
-        pass.gates.push_back(static_cast<int>(i));
-        done[i] = 1;
+        int fresh = 0, share = 0;
+        for (uint32_t b : high_bits(gates[i])) {
+          if (std::find(pass.hbits.begin(), pass.hbits.end(), b) == pass.hbits.end()) ++fresh;
+          else ++share;
+        }
+        if (pass.hbits.size() + fresh > kmax) continue;
+        if (fresh < best_new || (fresh == best_new && share > best_share)) {
+          best = static_cast<int>(i);
+          best_new = fresh;
+          best_share = share;
+        }
+      }
+      if (best >= 0) {
+        for (uint32_t b : high_bits(gates[best]))
+          if (std::find(pass.hbits.begin(), pass.hbits.end(), b) == pass.hbits.end()) pass.hbits.push_back(b);
+        pass.gates.push_back(best);
+        done[best] = 1;
         --remaining;
         added = true;
-        break;  // rescan from the first gate: readiness changed
       }
     }
     if (pass.gates.empty()) {
@@ -303,15 +385,66 @@ std::vector<Pass> schedule(uint32_t n, uint32_t B, uint32_t kmax, const std::vec
   return passes;
 }
 
-template <typename T>
-void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pass& pass, uint32_t B,
-                 const double* cs_dev) {
-  const uint32_t n = sv->n_qubits;
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  if (fn == nullptr) throw Error(VQF_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// The state as a 3-d tensor {128 B row, rows, batch entry}; box = one run of
+// 2^B amplitudes (<= 32 rows), 128 B swizzle.
+CUtensorMap state_map(const vqf_statevector* sv, uint32_t run_bytes) {
+  const bool f64 = sv->dtype == VQF_F64;
+  const uint64_t amp = f64 ? 16 : 8;
+  const cuuint64_t dims[3] = {f64 ? 16u : 32u, (sv->dim() * amp) / 128, sv->batch};
+  const cuuint64_t strides[2] = {128, sv->dim() * amp};
+  const cuuint32_t box[3] = {f64 ? 16u : 32u, run_bytes / 128, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = encode_fn()(&m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                 sv->amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(VQF_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+// Gate -> (local bits, code over those bits) for the fused-op merge.
+struct LocalGate {
+  uint32_t bits;  // local bit mask
+  uint32_t rot, ma, mb;  // pair patterns as local bit masks
+  int32_t param;
+  double c, s;
+};
+
+uint32_t compress(uint32_t mask, const uint32_t* pos, uint32_t m) {
+  uint32_t out = 0;
+  for (uint32_t j = 0; j < m; ++j)
+    if ((mask >> pos[j]) & 1u) out |= 1u << j;
+  return out;
+}
+
+// Kernel parameters of one pass: the gates mapped to local bits and merged
+// into fused ops.
+// Gates [first, *next) of the pass go into this launch: the composed
+// matrices must fit kMatElems, otherwise the pass is split into several
+// launches over the same tiles.
+TileParams build_params(uint32_t n, uint32_t batch, uint32_t B, const std::vector<TGate>& gates, const Pass& pass,
+                        const double* cs_dev, uint32_t fuse_bits, size_t first, size_t* next) {
   TileParams p{};
   p.n = n;
   p.B = B;
   p.k = static_cast<uint32_t>(pass.hbits.size());
-  p.batch = sv->batch;
+  p.batch = batch;
   p.cs = cs_dev;
   for (uint32_t j = 0; j < p.k; ++j) p.hb[j] = pass.hbits[j];
   const auto local = [&](uint32_t wire) -> uint32_t {
@@ -321,51 +454,116 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
       if (p.hb[j] == b) return B + j;
     throw Error(VQF_LOGIC_ERROR, "tile scheduler: wire outside the pass");
   };
+  std::vector<LocalGate> lg;
   for (int gi : pass.gates) {
     const TGate& g = gates[gi];
-    TileOp op{};
-    op.param = g.param;
-    op.c = g.c;
-    op.s = g.s;
+    LocalGate o{};
+    o.param = g.param;
+    o.c = g.c;
+    o.s = g.s;
     uint32_t lb[4];
-    for (uint32_t w = 0; w < g.n_wires; ++w) lb[w] = local(g.wires[w]);
+    for (uint32_t w = 0; w < g.n_wires; ++w) {
+      lb[w] = local(g.wires[w]);
+      o.bits |= 1u << lb[w];
+    }
     switch (g.kind) {
       case VQF_GATE_PAULI_X:
       case VQF_GATE_RY:
-        op.mode = g.kind == VQF_GATE_PAULI_X ? OP_SWAP : OP_ROT;
-        op.ma = 0;
-        op.mb = 1u << lb[0];
+        o.rot = g.kind == VQF_GATE_RY;
+        o.ma = 0;
+        o.mb = 1u << lb[0];
         break;
       case VQF_GATE_CNOT:
-        op.mode = OP_SWAP;
-        op.ma = 1u << lb[0];
-        op.mb = (1u << lb[0]) | (1u << lb[1]);
+        o.rot = 0;
+        o.ma = 1u << lb[0];
+        o.mb = (1u << lb[0]) | (1u << lb[1]);
         break;
       case VQF_GATE_DOUBLE_EXCITATION:
-        op.mode = OP_ROT;
-        op.ma = (1u << lb[0]) | (1u << lb[1]);  // |1100>
-        op.mb = (1u << lb[2]) | (1u << lb[3]);  // |0011>
+        o.rot = 1;
+        o.ma = (1u << lb[0]) | (1u << lb[1]);  // |1100>
+        o.mb = (1u << lb[2]) | (1u << lb[3]);  // |0011>
         break;
       case VQF_GATE_SINGLE_EXCITATION:
-        op.mode = OP_ROT;
-        op.ma = 1u << lb[0];  // |10>
-        op.mb = 1u << lb[1];  // |01>
+        o.rot = 1;
+        o.ma = 1u << lb[0];  // |10>
+        o.mb = 1u << lb[1];  // |01>
         break;
       default:
         throw Error(VQF_LOGIC_ERROR, "unknown gate kind");
     }
-    std::sort(lb, lb + g.n_wires);
-    op.npos = g.n_wires;
-    op.pos = 0;
-    for (uint32_t w = 0; w < g.n_wires; ++w) op.pos |= lb[w] << (8 * w);
-    p.ops[p.n_ops++] = op;
+    lg.push_back(o);
   }
+  // merge consecutive gates (the pass order respects the circuit's DAG)
+  // while their local bits fit one fused op
+  size_t i = first;
+  uint32_t uoff = 0;
+  while (i < lg.size()) {
+    uint32_t u = lg[i].bits;
+    bool wide = fuse_bits == kMaxFuse || __builtin_popcount(u) == 4;
+    size_t j = i + 1;
+    while (j < lg.size()) {
+      const bool w2 = wide || __builtin_popcount(lg[j].bits) == 4;
+      if (__builtin_popcount(u | lg[j].bits) > (w2 ? kMaxFuse : fuse_bits)) break;
+      wide = w2;
+      u |= lg[j++].bits;
+    }
+    TileFop f{};
+    uint32_t pos[kMaxFuse], m = 0;
+    for (uint32_t b = 0; b < 32; ++b)
+      if ((u >> b) & 1u) pos[m++] = b;
+    f.m = m;
+    if (uoff + (1u << (2 * m)) > kMatElems) break;  // matrix area full: the rest goes to the next launch
+    f.uoff = uoff;
+    uoff += 1u << (2 * m);
+    for (uint32_t q = 0; q < m; ++q) f.pos |= pos[q] << (8 * q);
+    f.sub0 = p.n_fops == 0 ? 0 : p.fops[p.n_fops - 1].sub0 + p.fops[p.n_fops - 1].n_sub;
+    for (size_t q = i; q < j; ++q) {
+      TileSub& t = p.subs[f.sub0 + f.n_sub++];
+      t.code = (lg[q].rot << 8) | (compress(lg[q].ma, pos, m) << 4) | compress(lg[q].mb, pos, m);
+      t.param = lg[q].param;
+      t.c = lg[q].c;
+      t.s = lg[q].s;
+    }
+    p.fops[p.n_fops++] = f;
+    i = j;
+  }
+  *next = i;
+  return p;
+}
+
+template <typename T>
+void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pass& pass, uint32_t B,
+                 const double* cs_dev) {
+  const uint32_t n = sv->n_qubits;
+  for (size_t first = 0, next = 0; first < pass.gates.size(); first = next) {
+  const TileParams p = build_params(n, sv->batch, B, gates, pass, cs_dev, sizeof(T) == 8 ? 3 : 4, first, &next);
+  bool wide = false;
+  for (uint32_t o = 0; o < p.n_fops; ++o) wide = wide || p.fops[o].m == 4;
   const uint32_t LB = B + p.k;
   const uint64_t n_tiles = uint64_t{1} << (n - LB);
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n_tiles, kTileBlocks));
-  const size_t smem = kStages * (sizeof(typename V2<T>::type) << LB) + 8 * kStages;  // ring + mbarriers
-  k_tile<T><<<dim3(grid, sv->batch), kTileThreads, smem, sv->stream>>>(static_cast<typename V2<T>::type*>(sv->amps), p);
+  const uint32_t run_bytes = static_cast<uint32_t>(sizeof(typename V2<T>::type) << B);
+  // the encoded map is cached per (state allocation, run size)
+  static thread_local std::vector<std::pair<std::pair<const void*, uint64_t>, CUtensorMap>> maps;
+  const auto key = std::make_pair(static_cast<const void*>(sv->amps),
+                                  (uint64_t)run_bytes | ((uint64_t)n << 32) | ((uint64_t)sv->batch << 40) |
+                                      ((uint64_t)sv->dtype << 62));
+  const CUtensorMap* map = nullptr;
+  for (auto& e : maps)
+    if (e.first == key) map = &e.second;
+  if (map == nullptr) {
+    if (maps.size() > 16) maps.erase(maps.begin());
+    maps.emplace_back(key, state_map(sv, run_bytes));
+    map = &maps.back().second;
+  }
+  const size_t smem = kStages * (sizeof(typename V2<T>::type) << LB) + 64 + kMatElems * sizeof(T) + 1024;  // ring + mbarriers + matrices + align
+  auto* amps = static_cast<typename V2<T>::type*>(sv->amps);
+  if (sizeof(T) == 4 || !wide)
+    k_tile<T, 512, sizeof(T) == 4 ? 4 : 3><<<dim3(grid, sv->batch), 512, smem, sv->stream>>>(amps, *map, p);
+  else
+    k_tile<T, 256, 4><<<dim3(grid, sv->batch), 256, smem, sv->stream>>>(amps, *map, p);
   VQF_LAUNCHED();
+  }
 }
 
 }  // namespace
@@ -378,6 +576,24 @@ std::vector<int> plan_tile_passes(uint32_t n_qubits, int32_t dtype, const std::v
   return out;
 }
 
+void plan_tile_counts(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>& gates, uint32_t* passes,
+                      uint32_t* fused_ops) {
+  uint32_t B, kmax;
+  tile_shape(n_qubits, dtype, B, kmax);
+  const std::vector<Pass> ps = schedule(n_qubits, B, kmax, gates);
+  uint32_t fops = 0, launches = 0;
+  for (const Pass& p : ps) {
+    if (!p.hbits.empty() && p.hbits[0] == 0xffffffffu) {
+      ++launches;
+      continue;
+    }
+    for (size_t first = 0, next = 0; first < p.gates.size(); first = next, ++launches)
+      fops += build_params(n_qubits, 1, B, gates, p, nullptr, dtype == VQF_F64 ? 3 : 4, first, &next).n_fops;
+  }
+  *passes = launches;
+  *fused_ops = fops;
+}
+
 int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, const double* cs_dev) {
   if (gates.empty()) return 0;
   const uint32_t n = sv->n_qubits;
@@ -385,12 +601,24 @@ int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, cons
   tile_shape(n, sv->dtype, B, kmax);
   static thread_local int opted = -1;
   if (opted != sv->device) {
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * 64 * 1024 + 8 * kStages));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * 64 * 1024 + 8 * kStages));
+    const int bytes = kStages * 64 * 1024 + 64 + kMatElems * 8 + 1024;
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 512, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, 512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     opted = sv->device;
   }
   const std::vector<Pass> passes = schedule(n, B, kmax, gates);
+  const bool tiny = (sv->amp_bytes() << B) < 128;  // 2-3 qubits: a run is below one 128 B row
   for (const Pass& pass : passes) {
+    if (tiny) {
+      for (int gi : pass.gates) {
+        const TGate& g = gates[gi];
+        GateArgs ga{g.kind, g.n_wires, {g.wires[0], g.wires[1], g.wires[2], g.wires[3]}, g.c, g.s,
+                    g.param >= 0 ? cs_dev + 2 * (size_t)g.param * sv->batch : nullptr};
+        sv_apply(sv, ga);
+      }
+      continue;
+    }
     if (!pass.hbits.empty() && pass.hbits[0] == 0xffffffffu) {
       const TGate& g = gates[pass.gates[0]];
       GateArgs ga{g.kind, g.n_wires, {g.wires[0], g.wires[1], g.wires[2], g.wires[3]}, g.c, g.s,

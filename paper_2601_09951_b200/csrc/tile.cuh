@@ -27,4 +27,9 @@ int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, cons
 // Tile plan statistics for tests / docs: passes and gates per pass.
 std::vector<int> plan_tile_passes(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>& gates);
 
+// HBM passes (fused tile passes + single-gate fallbacks) and fused register
+// ops (shared-memory round trips) apply_circuit would issue.  Host only.
+void plan_tile_counts(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>& gates, uint32_t* passes,
+                      uint32_t* fused_ops);
+
 }  // namespace vqf

@@ -236,6 +236,16 @@ def expectation(psi: StateVector, h: QubitHamiltonian):
     return float(out[0]) if psi.batch == 1 else out
 
 
+def circuit_plan(n_qubits: int, gates: Sequence[Gate], dtype: str = "f64") -> dict:
+    """How apply_circuit would run `gates`: HBM passes over the state and
+    fused register ops inside them (statevector.hpp:205-207 makes one pass
+    per gate).  Host only."""
+    arr = (A.Gate * max(1, len(gates)))(*[g.as_c() for g in gates])
+    p, f = C.c_uint32(), C.c_uint32()
+    check(lib.vqf_circuit_plan(n_qubits, A.F64 if dtype == "f64" else A.F32, arr, len(gates), C.byref(p), C.byref(f)))
+    return {"passes": p.value, "fused_ops": f.value}
+
+
 def expectation_plan(h: QubitHamiltonian) -> dict:
     """How expectation() reads the state for h: HBM passes over the state,
     distinct flip groups (the reference's per-group passes, statevector.hpp:

@@ -3,6 +3,7 @@
   python scripts/prof_targets.py pes        # fused PES kernel, 3 launches
   python scripts/prof_targets.py gates N    # RY / CNOT / DE on an N-qubit fp64 state
   python scripts/prof_targets.py expect N   # TFIM expectation (diag + N flip groups)
+  python scripts/prof_targets.py hea N      # two fused HEA layers (k_tile passes)
 """
 from __future__ import annotations
 
@@ -38,6 +39,12 @@ def main():
         V.apply_circuit(psi, [V.Gate.ry(0.3, q) for q in range(n)])
         print(V.expectation(psi, V.build_tfim(n, 1.0, 1.0)))
         print(V.expectation(psi, V.build_z_sum(n)))
+    elif what == "hea":
+        n = int(sys.argv[2])
+        psi = V.StateVector(n)
+        layer = [V.Gate.ry(0.1 * (q + 1), q) for q in range(n)] + [V.Gate.cnot(q, q + 1) for q in range(n - 1)]
+        for _ in range(2):
+            V.apply_circuit(psi, layer)
     else:
         raise SystemExit(f"unknown target {what}")
 

@@ -196,3 +196,18 @@ def test_expectation_plan_packs_flip_groups(V):
     p = V.expectation_plan(h)
     assert p["flip_groups"] >= 28 and p["multi_passes"] <= 2
     assert p["flip_groups"] - 2 <= p["state_passes"] <= p["flip_groups"] + 1
+
+
+def test_circuit_plan_fuses_hea_layers(V):
+    """Host plan of apply_circuit (no GPU): one HEA layer (RY on every wire +
+    CNOT chain, vqe.hpp:81-93) needs far fewer HBM passes than gates; the
+    scheduler advances the CNOT chain five wires per pass (six gathered high
+    bits) and composes the gates into few register ops per pass."""
+    for n in [12, 20, 26, 30, 33]:
+        layer = [V.Gate.ry(0.1, q) for q in range(n)] + [V.Gate.cnot(q, q + 1) for q in range(n - 1)]
+        p = V.circuit_plan(n, layer)
+        assert p["passes"] <= 1 + max(0, -(-(n - 6 - 1) // 5)), (n, p)
+        assert p["fused_ops"] <= len(layer) // 2
+    assert V.circuit_plan(10, [V.Gate.ry(0.3, 0)]) == {"passes": 1, "fused_ops": 0}
+    with pytest.raises(ValueError, match="exceeds register"):
+        V.circuit_plan(4, [V.Gate.ry(0.1, 5), V.Gate.ry(0.1, 0)])

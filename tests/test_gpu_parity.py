@@ -73,6 +73,26 @@ def test_gates_match_oracle(gpu, orc, n):
         assert np.max(np.abs(psi.amplitudes - cur)) < A_TOL
 
 
+@pytest.mark.parametrize("n,dtype", [(3, "f64"), (4, "f32"), (5, "f64"), (12, "f64"), (13, "f32"), (16, "f64"),
+                                     (17, "f32"), (19, "f64")])
+def test_fused_circuit_equals_per_gate(gpu, n, dtype):
+    # apply_circuit (k_tile: TMA-swizzled tiles, gates fused into register
+    # ops of <= 4 local bits) against one apply_gate launch per gate, on
+    # every gate kind with random wires (low and high index bits)
+    V = gpu
+    pr = random.Random(9000 + n)
+    gates = [gpu_gate(V, *g) for g in rand_gates(pr, n, 120)]
+    psi0 = random_state(np.random.default_rng(n), n)
+    a, b = V.StateVector(n, dtype=dtype), V.StateVector(n, dtype=dtype)
+    a.amplitudes = psi0
+    b.amplitudes = psi0
+    V.apply_circuit(a, gates)
+    for g in gates:
+        V.apply_gate(b, g)
+    tol = 1e-12 if dtype == "f64" else 2e-5
+    assert np.max(np.abs(a.amplitudes - b.amplitudes)) < tol
+
+
 def test_gate_goldens(gpu, golden):
     V = gpu
     for c in golden("gates_expectation.json")["cases"]:
