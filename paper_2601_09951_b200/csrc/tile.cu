@@ -175,7 +175,8 @@ __device__ void compose_fops(const TileParams& p, T* U) {
 // shared memory.  The swizzle is xor-linear and base / slot offsets have
 // disjoint bits, so slot addresses are swz(base) ^ swz(offset).
 template <int M, typename T, int NT>
-__device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, const TileFop& f, const T* U) {
+__device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, const TileFop& f, const T* U,
+                                        uint32_t gt) {
   using A = typename V2<T>::type;
   constexpr int D = 1 << M;
   uint32_t pos[M];
@@ -191,7 +192,7 @@ __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, co
     sd[r] = swz<T>(d);
   }
   const T* u = U + f.uoff;
-  for (uint32_t w = threadIdx.x; w < (NL >> M); w += NT) {
+  for (uint32_t w = gt; w < (NL >> M); w += NT) {
     uint32_t base = w;
 #pragma unroll
     for (int j = 0; j < M; ++j) base = ((base >> pos[j]) << (pos[j] + 1)) | (base & ((1u << pos[j]) - 1));
@@ -201,94 +202,120 @@ __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, co
     for (int r = 0; r < D; ++r) x[r] = t[sb ^ sd[r]];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-      A y;
-      y.x = T(0);
-      y.y = T(0);
+      // row r of U as 16-byte broadcast loads; two accumulation chains per
+      // component (even / odd columns) halve the dependent-FMA depth
+      A y0, y1;
+      y0.x = y0.y = y1.x = y1.y = T(0);
+      if constexpr (D == 1) {
+        y0.x = u[0] * x[0].x;
+        y0.y = u[0] * x[0].y;
+      } else {
+        using P2 = typename V2<T>::type;
+        const P2* row = reinterpret_cast<const P2*>(u + r * D);
 #pragma unroll
-      for (int c = 0; c < D; ++c) {
-        const T m = u[r * D + c];
-        y.x = fma(m, x[c].x, y.x);
-        y.y = fma(m, x[c].y, y.y);
+        for (int c = 0; c < D; c += 2) {
+          const P2 m = row[c / 2];
+          y0.x = fma(m.x, x[c].x, y0.x);
+          y0.y = fma(m.x, x[c].y, y0.y);
+          y1.x = fma(m.y, x[c + 1].x, y1.x);
+          y1.y = fma(m.y, x[c + 1].y, y1.y);
+        }
       }
+      A y;
+      y.x = y0.x + y1.x;
+      y.y = y0.y + y1.y;
       t[sb ^ sd[r]] = y;
     }
   }
 }
 
-// Persistent tile kernel with a kStages-deep TMA ring.  Warp 0 keeps
-// kStages - 1 tiles in flight, issuing the 2^k 4 KB runs of each as TMA
-// tensor loads (128 B swizzle, one mbarrier per stage, expect_tx = tile
-// bytes), while all threads apply the pass's fused ops to the current tile
-// in shared memory; the tile then leaves with coalesced 16-byte stores.
+// Named barrier over the NT threads of one consumer group (ids 1, 2; 0 is
+// __syncthreads).
+template <int NT>
+__device__ __forceinline__ void group_sync(uint32_t group) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(NT) : "memory");
+}
+
+// Persistent tile kernel.  The CTA runs two independent consumer groups of
+// NT threads; group g takes every other tile of the CTA's sequence, with its
+// own kStages-deep TMA ring (lane 0 of the group's first warp arms the
+// stage's mbarrier with the tile's bytes, its lanes issue the 2^k runs as
+// TMA tensor loads, 128 B swizzle) and its own named barrier, so one group's
+// barrier waits and shared-memory phases overlap the other group's work.
+// Each tile: the pass's fused ops (y = U x on 2^m amplitudes per thread),
+// then coalesced 16-byte stores back to HBM.
 template <typename T, int NT, int MAXM>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(2 * NT, 1)
     k_tile(typename V2<T>::type* __restrict__ a, const __grid_constant__ CUtensorMap map, const TileParams p) {
   using A = typename V2<T>::type;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 128 B swizzle atoms are 1024 B: align the ring (the launch adds 1 KB
+  // 128 B swizzle atoms are 1024 B: align the rings (the launch adds 1 KB
   // slack); indexing smem_raw keeps the pointer in the shared window (LDS/STS)
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const uint32_t LB = p.B + p.k, NL = 1u << LB;
   const uint32_t run_amps = 1u << p.B, n_runs = 1u << p.k;
   const uint32_t tile_bytes = NL * sizeof(A), run_bytes = run_amps * sizeof(A);
   const uint32_t amps_per_row = 128 / sizeof(A);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kStages * (size_t)tile_bytes);
-  T* U = reinterpret_cast<T*>(smem + kStages * (size_t)tile_bytes + 64);  // composed fused-op matrices
-  __shared__ uint64_t run_off[1 << kMaxHigh];
+  const uint32_t group = threadIdx.x / NT, gt = threadIdx.x % NT;
+  unsigned char* ring = smem + (size_t)group * kStages * tile_bytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * kStages * (size_t)tile_bytes) + group * kStages;
+  T* U = reinterpret_cast<T*>(smem + 2 * kStages * (size_t)tile_bytes + 128);  // composed fused-op matrices
+  __shared__ uint64_t run_off_all[2][1 << kMaxHigh];
+  uint64_t* run_off = run_off_all[group];
   A* s = a + ((uint64_t)blockIdx.y << p.n);
   const uint64_t n_tiles = uint64_t{1} << (p.n - LB);
-  if (threadIdx.x == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
+  if (gt == 0) {
+    if (group == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
     for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   compose_fops<T>(p, U);
   __syncthreads();
-  const auto stage_buf = [&](int st) { return reinterpret_cast<A*>(smem + (size_t)st * tile_bytes); };
-  // warp 0 issues a tile: lane 0 arms the stage's mbarrier with the tile's
-  // byte count, lane j copies run j (the arm and the copies may land in any
-  // order: the phase needs both the arrival and the bytes)
+  const auto stage_buf = [&](int st) { return reinterpret_cast<A*>(ring + (size_t)st * tile_bytes); };
   const auto issue_load = [&](uint64_t tile, int st) {
-    const uint32_t lane = threadIdx.x;
+    const uint32_t lane = gt;
     if (lane == 0) mbar_expect_tx(&bar[st], tile_bytes);
     unsigned char* dst = reinterpret_cast<unsigned char*>(stage_buf(st));
     for (uint32_t j = lane; j < n_runs; j += 32)
       tma_load_run(dst + (size_t)j * run_bytes, &map, static_cast<int32_t>(run_start(p, tile, j) / amps_per_row),
                    static_cast<int32_t>(blockIdx.y), &bar[st]);
   };
-  if (threadIdx.x < 32)
+  // the group's tiles: blockIdx.x + (2 i + group) * gridDim.x
+  const uint64_t step = 2 * (uint64_t)gridDim.x;
+  const uint64_t first = blockIdx.x + (uint64_t)group * gridDim.x;
+  if (gt < 32)
     for (int st = 0; st < kStages - 1; ++st) {
-      const uint64_t t0 = blockIdx.x + (uint64_t)st * gridDim.x;
+      const uint64_t t0 = first + (uint64_t)st * step;
       if (t0 < n_tiles) issue_load(t0, st);
     }
-  uint64_t tile = blockIdx.x;
-  for (uint32_t it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
+  uint64_t tile = first;
+  for (uint32_t it = 0; tile < n_tiles; tile += step, ++it) {
     const int cur = it % kStages;
-    const uint64_t ahead = tile + (uint64_t)(kStages - 1) * gridDim.x;
-    // that stage's previous tile was written back (and the buffer released)
-    // before the __syncthreads that closed the previous iteration
-    if (threadIdx.x < 32 && ahead < n_tiles) issue_load(ahead, (it + kStages - 1) % kStages);
+    const uint64_t ahead = tile + (uint64_t)(kStages - 1) * step;
+    // that stage's previous tile was written back before the group barrier
+    // that closed the previous iteration
+    if (gt < 32 && ahead < n_tiles) issue_load(ahead, (it + kStages - 1) % kStages);
     mbar_wait(&bar[cur], (it / kStages) & 1u);
     A* t = stage_buf(cur);
     for (uint32_t o = 0; o < p.n_fops; ++o) {
       const TileFop f = p.fops[o];
       switch (f.m) {
-        case 1: run_fop<1, T, NT>(t, NL, f, U); break;
-        case 2: run_fop<2, T, NT>(t, NL, f, U); break;
-        case 3: run_fop<3, T, NT>(t, NL, f, U); break;
+        case 1: run_fop<1, T, NT>(t, NL, f, U, gt); break;
+        case 2: run_fop<2, T, NT>(t, NL, f, U, gt); break;
+        case 3: run_fop<3, T, NT>(t, NL, f, U, gt); break;
         default:
-          if constexpr (MAXM >= 4) run_fop<4, T, NT>(t, NL, f, U);
+          if constexpr (MAXM >= 4) run_fop<4, T, NT>(t, NL, f, U, gt);
           break;
       }
-      __syncthreads();
+      group_sync<NT>(group);
     }
     // write-back: coalesced 16-byte stores, consecutive threads along a run
-    if (threadIdx.x < n_runs) run_off[threadIdx.x] = run_start(p, tile, threadIdx.x);
-    __syncthreads();
+    if (gt < n_runs) run_off[gt] = run_start(p, tile, gt);
+    group_sync<NT>(group);
     const uint32_t low_mask = run_amps - 1;
 #pragma unroll 4
-    for (uint32_t li = threadIdx.x; li < NL; li += NT) s[run_off[li >> p.B] | (li & low_mask)] = t[swz<T>(li)];
-    __syncthreads();  // buffer free for the stage's next TMA load
+    for (uint32_t li = gt; li < NL; li += NT) s[run_off[li >> p.B] | (li & low_mask)] = t[swz<T>(li)];
+    group_sync<NT>(group);  // buffer free for the stage's next TMA load
   }
 }
 
@@ -299,9 +326,9 @@ struct Pass {
 
 // Local bit budget: 64 KB of shared memory per tile (kStages tiles resident).
 void tile_shape(uint32_t n, int32_t dtype, uint32_t& B, uint32_t& kmax) {
-  // runs of 1 KB (one TMA box of 8 rows x 128 B): B = 6 (fp64) / 7 (fp32),
-  // leaving 6 gathered high bits per pass
-  const uint32_t LB = dtype == VQF_F64 ? 12 : 13;
+  // 32 KB tiles (two groups x kStages per CTA) in runs of 512 B (one TMA box
+  // of 4 rows x 128 B): B = 5 (fp64) / 6 (fp32), leaving 6 gathered high bits
+  const uint32_t LB = dtype == VQF_F64 ? 11 : 12;
   B = std::min<uint32_t>(n, LB - kMaxHigh);
   kmax = std::min<uint32_t>(LB - B, n - B);
 }
@@ -556,12 +583,12 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
     maps.emplace_back(key, state_map(sv, run_bytes));
     map = &maps.back().second;
   }
-  const size_t smem = kStages * (sizeof(typename V2<T>::type) << LB) + 64 + kMatElems * sizeof(T) + 1024;  // ring + mbarriers + matrices + align
+  const size_t smem = 2 * kStages * (sizeof(typename V2<T>::type) << LB) + 128 + kMatElems * sizeof(T) + 1024;  // rings + mbarriers + matrices + align
   auto* amps = static_cast<typename V2<T>::type*>(sv->amps);
   if (sizeof(T) == 4 || !wide)
-    k_tile<T, 512, sizeof(T) == 4 ? 4 : 3><<<dim3(grid, sv->batch), 512, smem, sv->stream>>>(amps, *map, p);
+    k_tile<T, 256, sizeof(T) == 4 ? 4 : 3><<<dim3(grid, sv->batch), 512, smem, sv->stream>>>(amps, *map, p);
   else
-    k_tile<T, 256, 4><<<dim3(grid, sv->batch), 256, smem, sv->stream>>>(amps, *map, p);
+    k_tile<T, 128, 4><<<dim3(grid, sv->batch), 256, smem, sv->stream>>>(amps, *map, p);
   VQF_LAUNCHED();
   }
 }
@@ -601,10 +628,10 @@ int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, cons
   tile_shape(n, sv->dtype, B, kmax);
   static thread_local int opted = -1;
   if (opted != sv->device) {
-    const int bytes = kStages * 64 * 1024 + 64 + kMatElems * 8 + 1024;
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 512, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, 512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    const int bytes = 2 * kStages * 32 * 1024 + 128 + kMatElems * 8 + 1024;
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, 256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     opted = sv->device;
   }
   const std::vector<Pass> passes = schedule(n, B, kmax, gates);
