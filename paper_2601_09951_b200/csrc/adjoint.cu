@@ -17,6 +17,7 @@
 #include <cstring>
 
 #include "adjoint.cuh"
+#include "tile.cuh"
 
 namespace vqf {
 
@@ -310,6 +311,27 @@ void run_t(AdjointPlan& pl, const std::vector<AdjGate>& prog, const std::vector<
   for (size_t gi = prog.size(); gi-- > 0;) {
     const AdjGate& g = prog[gi];
     const auto bit_of = [n](uint32_t w) { return n - 1 - w; };
+    // a run of >= 2 parameter-free self-inverse gates (CNOT / X chains) is
+    // un-applied to both vectors by the fused tile path: one pass per vector
+    // for the run instead of one two-vector pass per gate
+    size_t run0 = gi + 1;
+    while (run0 > 0 && prog[run0 - 1].param < 0 &&
+           (prog[run0 - 1].kind == VQF_GATE_CNOT || prog[run0 - 1].kind == VQF_GATE_PAULI_X))
+      --run0;
+    if (gi + 1 - run0 >= 2) {
+      std::vector<TGate> inv;
+      for (size_t k = gi + 1; k-- > run0;) {  // reversed: (G_m ... G_1)^dag = G_1 ... G_m for self-inverse G
+        const AdjGate& q = prog[k];
+        inv.push_back(TGate{q.kind, q.kind == VQF_GATE_CNOT ? 2u : 1u, {q.wires[0], q.wires[1], 0, 0}, -1, 1.0, 0.0});
+      }
+      run_circuit_tiled(pl.psi, inv, nullptr);
+      cudaStream_t own = pl.lam->stream;  // keep every launch of the sweep on psi's stream
+      pl.lam->stream = st;
+      run_circuit_tiled(pl.lam, inv, nullptr);
+      pl.lam->stream = own;
+      gi = run0;
+      continue;
+    }
     if (g.kind == VQF_GATE_CNOT) {
       const uint32_t bc = bit_of(g.wires[0]), bt = bit_of(g.wires[1]);
       const uint64_t total = uint64_t{1} << (n - 2);

@@ -11,6 +11,8 @@ ncu --set full --clock-control none --import-source on -k regex:k_gate1 -s 3 -c 
     python scripts/prof_targets.py gates 30 > $OUT/full_ry30.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_h2 -c 1 -o $OUT/full_pes \
     python scripts/prof_targets.py pes > $OUT/full_pes.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_expect -c 3 -o $OUT/full_expect28 \
+ncu --set full --clock-control none --import-source on -k regex:k_expect -c 4 -o $OUT/full_expect28 \
     python scripts/prof_targets.py expect 28 > $OUT/full_expect28.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_tile -s 2 -c 3 -o $OUT/full_tile26 \
+    python scripts/prof_targets.py hea 26 > $OUT/full_tile26.log 2>&1
 ls -la $OUT
