@@ -234,6 +234,107 @@ __global__ void __launch_bounds__(kThreads) k_adj_givens(typename V2<T>::type* _
   if (threadIdx.x == 0) partials[blockIdx.x] = t.x;
 }
 
+// K consecutive RY gates on distinct wires (they commute), un-applied in
+// one pass over both vectors.  Each thread holds the 2^K amplitudes of psi
+// and lambda that differ in the K gate bits (slot bit j <-> gate j, so every
+// pair is a fixed pair of registers) and runs k_adj_givens' step for gate
+// 0, 1, ..., K-1 in turn: psi' = G^dag psi, g_j += Re<lambda| dG psi'>,
+// lambda' = G^dag lambda.  Per-block partials per gate.
+struct RyGroup {
+  uint32_t bit[3];
+  double c[3], s[3];
+  double* part[3];  // gate j's per-block partial row
+};
+
+template <typename T, int K>
+__global__ void __launch_bounds__(kThreads) k_adj_ry_multi(typename V2<T>::type* __restrict__ psi,
+                                                           typename V2<T>::type* __restrict__ lam, uint32_t n,
+                                                           const RyGroup gr) {
+  using A = typename V2<T>::type;
+  constexpr int D = 1 << K;
+  uint32_t pos[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) pos[j] = gr.bit[j];
+  // ascending insertion order for the base index
+  uint32_t asc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) asc[j] = pos[j];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = i + 1; j < K; ++j)
+      if (asc[j] < asc[i]) {
+        const uint32_t t = asc[i];
+        asc[i] = asc[j];
+        asc[j] = t;
+      }
+  uint64_t off[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    uint64_t o = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (r & (1 << j)) o |= uint64_t{1} << pos[j];
+    off[r] = o;
+  }
+  double acc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) acc[j] = 0.0;
+  const uint64_t total = uint64_t{1} << (n - K);
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t k = (uint64_t)blockIdx.x * kThreads + threadIdx.x; k < total; k += stride) {
+    uint64_t base = k;
+#pragma unroll
+    for (int j = 0; j < K; ++j) base = insert_zero(base, asc[j]);
+    A a[D], l[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      a[r] = psi[base | off[r]];
+      l[r] = lam[base | off[r]];
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const double c = gr.c[j], sn = gr.s[j];
+      const T ct = static_cast<T>(c), st = static_cast<T>(sn);
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        if (r & (1 << j)) continue;
+        A& x = a[r];
+        A& y = a[r | (1 << j)];
+        A& lx = l[r];
+        A& ly = l[r | (1 << j)];
+        A pa, pb;  // psi' = G^dag psi
+        pa.x = ct * x.x + st * y.x;
+        pa.y = ct * x.y + st * y.y;
+        pb.x = ct * y.x - st * x.x;
+        pb.y = ct * y.y - st * x.y;
+        const double mar = 0.5 * (-sn * (double)pa.x - c * (double)pb.x), mai = 0.5 * (-sn * (double)pa.y - c * (double)pb.y);
+        const double mbr = 0.5 * (c * (double)pa.x - sn * (double)pb.x), mbi = 0.5 * (c * (double)pa.y - sn * (double)pb.y);
+        acc[j] += (double)lx.x * mar + (double)lx.y * mai + (double)ly.x * mbr + (double)ly.y * mbi;
+        A qa, qb;  // lambda' = G^dag lambda
+        qa.x = ct * lx.x + st * ly.x;
+        qa.y = ct * lx.y + st * ly.y;
+        qb.x = ct * ly.x - st * lx.x;
+        qb.y = ct * ly.y - st * lx.y;
+        x = pa;
+        y = pb;
+        lx = qa;
+        ly = qb;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      psi[base | off[r]] = a[r];
+      lam[base | off[r]] = l[r];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double2 t = block_sum(make_double2(acc[j], 0.0));
+    if (threadIdx.x == 0) gr.part[j][blockIdx.x] = t.x;
+  }
+}
+
 // Self-inverse CNOT on both vectors in one pass.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_adj_cnot(typename V2<T>::type* __restrict__ psi,
@@ -331,6 +432,33 @@ void run_t(AdjointPlan& pl, const std::vector<AdjGate>& prog, const std::vector<
       pl.lam->stream = own;
       gi = run0;
       continue;
+    }
+    // up to three consecutive RYs on distinct wires (they commute): one
+    // two-vector pass for the group instead of one per gate
+    if (g.kind == VQF_GATE_RY && g.param >= 0) {
+      size_t cnt = 1;
+      while (cnt < 3 && gi >= cnt && prog[gi - cnt].kind == VQF_GATE_RY && prog[gi - cnt].param >= 0) {
+        bool distinct = true;
+        for (size_t q = 0; q < cnt; ++q) distinct = distinct && prog[gi - cnt].wires[0] != prog[gi - q].wires[0];
+        if (!distinct) break;
+        ++cnt;
+      }
+      if (cnt >= 2) {
+        RyGroup gr{};
+        for (size_t q = 0; q < cnt; ++q) {  // gate q of the group = prog[gi - q] (backward order)
+          const AdjGate& h = prog[gi - q];
+          const double th = theta[h.param];
+          gr.bit[q] = bit_of(h.wires[0]);
+          gr.c[q] = std::cos(0.5 * th);
+          gr.s[q] = std::sin(0.5 * th);
+          gr.part[q] = pl.gpart + (size_t)h.param * pl.nb;
+        }
+        if (cnt == 2) k_adj_ry_multi<T, 2><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr);
+        else k_adj_ry_multi<T, 3><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr);
+        VQF_LAUNCHED();
+        gi -= cnt - 1;
+        continue;
+      }
     }
     if (g.kind == VQF_GATE_CNOT) {
       const uint32_t bc = bit_of(g.wires[0]), bt = bit_of(g.wires[1]);
