@@ -63,6 +63,11 @@ struct TileParams {
   uint32_t n, B, k, n_fops, batch;
   uint32_t hb[kMaxHigh];  // global bit of local bit B + j, ascending
   const double* cs;
+  // Permutation-only pass (every gate X / CNOT): no fused ops; the tile is
+  // written back as out[L] = in[F(L)] with F(L) = c ^ xor of col[b] over
+  // the set bits b of L (an affine map over GF(2) on the local index).
+  uint32_t perm_only, perm_c;
+  uint32_t perm_col[16];
   TileFop fops[kMaxOps];
   TileSub subs[kMaxOps];
 };
@@ -244,7 +249,7 @@ __device__ __forceinline__ void group_sync(uint32_t group) {
 // barrier waits and shared-memory phases overlap the other group's work.
 // Each tile: the pass's fused ops (y = U x on 2^m amplitudes per thread),
 // then coalesced 16-byte stores back to HBM.
-template <typename T, int NT, int MAXM>
+template <typename T, int NT, int MAXM, bool PERM>
 __global__ void __launch_bounds__(2 * NT, 1)
     k_tile(typename V2<T>::type* __restrict__ a, const __grid_constant__ CUtensorMap map, const TileParams p) {
   using A = typename V2<T>::type;
@@ -269,7 +274,17 @@ __global__ void __launch_bounds__(2 * NT, 1)
     for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  compose_fops<T>(p, U);
+  if constexpr (!PERM) compose_fops<T>(p, U);
+  // permutation-only pass: F as two 64-entry tables (bits 0-5, bits 6-11)
+  __shared__ uint16_t ftab[PERM ? 2 : 1][64];
+  if constexpr (PERM)
+    for (uint32_t e = threadIdx.x; e < 128; e += blockDim.x) {
+      const uint32_t half = e >> 6, j = e & 63u;
+      uint32_t v = 0;
+      for (uint32_t b = 0; b < 6; ++b)
+        if ((j >> b) & 1u) v ^= p.perm_col[6 * half + b];
+      ftab[half][j] = static_cast<uint16_t>(v);
+    }
   __syncthreads();
   const auto stage_buf = [&](int st) { return reinterpret_cast<A*>(ring + (size_t)st * tile_bytes); };
   const auto issue_load = [&](uint64_t tile, int st) {
@@ -297,7 +312,7 @@ __global__ void __launch_bounds__(2 * NT, 1)
     if (gt < 32 && ahead < n_tiles) issue_load(ahead, (it + kStages - 1) % kStages);
     mbar_wait(&bar[cur], (it / kStages) & 1u);
     A* t = stage_buf(cur);
-    for (uint32_t o = 0; o < p.n_fops; ++o) {
+    for (uint32_t o = 0; o < (PERM ? 0u : p.n_fops); ++o) {
       const TileFop f = p.fops[o];
       switch (f.m) {
         case 1: run_fop<1, T, NT>(t, NL, f, U, gt); break;
@@ -313,8 +328,16 @@ __global__ void __launch_bounds__(2 * NT, 1)
     if (gt < n_runs) run_off[gt] = run_start(p, tile, gt);
     group_sync<NT>(group);
     const uint32_t low_mask = run_amps - 1;
+    if constexpr (PERM) {
 #pragma unroll 4
-    for (uint32_t li = gt; li < NL; li += NT) s[run_off[li >> p.B] | (li & low_mask)] = t[swz<T>(li)];
+      for (uint32_t li = gt; li < NL; li += NT) {
+        const uint32_t src = p.perm_c ^ ftab[0][li & 63u] ^ ftab[1][li >> 6];
+        s[run_off[li >> p.B] | (li & low_mask)] = t[swz<T>(src)];
+      }
+    } else {
+#pragma unroll 4
+      for (uint32_t li = gt; li < NL; li += NT) s[run_off[li >> p.B] | (li & low_mask)] = t[swz<T>(li)];
+    }
     group_sync<NT>(group);  // buffer free for the stage's next TMA load
   }
 }
@@ -520,6 +543,27 @@ TileParams build_params(uint32_t n, uint32_t batch, uint32_t B, const std::vecto
     }
     lg.push_back(o);
   }
+  // a pass of X / CNOT gates only is an affine index map F on the local
+  // bits: out[L] = in[F(L)] with F = f_1 o ... o f_m (gate 1 first in the
+  // circuit, so f_m acts on L first); applied in the write-back
+  bool perm = first == 0;
+  for (const LocalGate& o : lg) perm = perm && !o.rot;
+  if (perm) {
+    const auto F = [&](uint32_t x) {
+      for (size_t q = lg.size(); q-- > 0;) {
+        const LocalGate& o = lg[q];
+        if (o.ma == 0) x ^= o.mb;                                            // X: mb = target bit
+        else if (x & o.ma) x ^= o.mb ^ o.ma;                                 // CNOT: ma = control, mb = control | target
+      }
+      return x;
+    };
+    const uint32_t LB = B + p.k;
+    p.perm_only = 1;
+    p.perm_c = F(0);
+    for (uint32_t b = 0; b < 16; ++b) p.perm_col[b] = b < LB ? (F(1u << b) ^ p.perm_c) : 0u;
+    *next = lg.size();
+    return p;
+  }
   // merge consecutive gates (the pass order respects the circuit's DAG)
   // while their local bits fit one fused op
   size_t i = first;
@@ -585,10 +629,12 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
   }
   const size_t smem = 2 * kStages * (sizeof(typename V2<T>::type) << LB) + 128 + kMatElems * sizeof(T) + 1024;  // rings + mbarriers + matrices + align
   auto* amps = static_cast<typename V2<T>::type*>(sv->amps);
-  if (sizeof(T) == 4 || !wide)
-    k_tile<T, 256, sizeof(T) == 4 ? 4 : 3><<<dim3(grid, sv->batch), 512, smem, sv->stream>>>(amps, *map, p);
+  if (p.perm_only)
+    k_tile<T, 256, 1, true><<<dim3(grid, sv->batch), 512, smem, sv->stream>>>(amps, *map, p);
+  else if (sizeof(T) == 4 || !wide)
+    k_tile<T, 256, sizeof(T) == 4 ? 4 : 3, false><<<dim3(grid, sv->batch), 512, smem, sv->stream>>>(amps, *map, p);
   else
-    k_tile<T, 128, 4><<<dim3(grid, sv->batch), 256, smem, sv->stream>>>(amps, *map, p);
+    k_tile<T, 128, 4, false><<<dim3(grid, sv->batch), 256, smem, sv->stream>>>(amps, *map, p);
   VQF_LAUNCHED();
   }
 }
@@ -629,9 +675,11 @@ int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, cons
   static thread_local int opted = -1;
   if (opted != sv->device) {
     const int bytes = 2 * kStages * 32 * 1024 + 128 + kMatElems * 8 + 1024;
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, 256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 256, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 128, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, 256, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 256, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, 256, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     opted = sv->device;
   }
   const std::vector<Pass> passes = schedule(n, B, kmax, gates);

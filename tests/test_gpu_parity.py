@@ -93,6 +93,24 @@ def test_fused_circuit_equals_per_gate(gpu, n, dtype):
     assert np.max(np.abs(a.amplitudes - b.amplitudes)) < tol
 
 
+@pytest.mark.parametrize("n,dtype", [(5, "f64"), (12, "f64"), (16, "f64"), (19, "f32")])
+def test_fused_permutation_passes(gpu, n, dtype):
+    # X / CNOT-only circuits: every tile pass is an affine index map applied
+    # in the write-back (no register ops); against one launch per gate
+    V = gpu
+    pr = random.Random(4000 + n)
+    gates = [gpu_gate(V, *g) for g in rand_gates(pr, n, 80, kinds=(0, 2))]
+    psi0 = random_state(np.random.default_rng(n + 7), n)
+    a, b = V.StateVector(n, dtype=dtype), V.StateVector(n, dtype=dtype)
+    a.amplitudes = psi0
+    b.amplitudes = psi0
+    V.apply_circuit(a, gates)
+    for g in gates:
+        V.apply_gate(b, g)
+    assert np.array_equal(a.amplitudes, b.amplitudes)  # pure data movement: bitwise
+    assert V.circuit_plan(n, gates, dtype)["fused_ops"] == 0
+
+
 def test_gate_goldens(gpu, golden):
     V = gpu
     for c in golden("gates_expectation.json")["cases"]:
