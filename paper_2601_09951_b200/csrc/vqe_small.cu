@@ -219,27 +219,41 @@ __device__ __forceinline__ double2 circuit_energy(const Shared& sh, const double
 }
 
 // Folds the mask terms into per-flip-group amplitude tables (warp 0).
+// Groups are numbered in order of first appearance after the diagonal
+// group 0: lane t flags term t when no earlier term has its flip, and a
+// ballot prefix count gives its group index (no serial scan).
 __device__ void build_tables(Shared& sh, int D, int lane) {
-  if (lane == 0) {
-    int G = 0;
-    sh.flip[G++] = 0;
-    for (int t = 0; t < sh.n_terms; ++t) {
-      const int f = static_cast<int>(sh.terms[t].flip);
-      bool found = false;
-      for (int g = 0; g < G; ++g) found |= (sh.flip[g] == f);
-      if (!found) sh.flip[G++] = f;
+  const int T = sh.n_terms;
+  int n_new = 0;
+  for (int t0 = 0; t0 < T; t0 += 32) {
+    const int t = t0 + lane;
+    int f = -1;
+    bool first = false;
+    if (t < T) {
+      f = static_cast<int>(sh.terms[t].flip);
+      first = f != 0;
+      for (int u = 0; u < t && first; ++u) first = static_cast<int>(sh.terms[u].flip) != f;
     }
-    sh.n_groups = G;
+    const unsigned m = __ballot_sync(0xffffffffu, first);
+    if (first) sh.flip[1 + n_new + __popc(m & ((1u << lane) - 1))] = f;
+    n_new += __popc(m);
+  }
+  if (lane == 0) {
+    sh.flip[0] = 0;
+    sh.n_groups = 1 + n_new;
   }
   __syncwarp();
-  for (int idx = lane; idx < sh.n_groups * D; idx += 32) {
+  const int G = 1 + n_new;
+  for (int idx = lane; idx < G * D; idx += 32) {
     const int g = idx / D, i = idx % D;
+    const int fg = sh.flip[g];
     double re = 0.0, im = 0.0;
-    for (int t = 0; t < sh.n_terms; ++t) {
-      if (static_cast<int>(sh.terms[t].flip) != sh.flip[g]) continue;
-      const bool odd = __popcll(static_cast<uint64_t>(i) & sh.terms[t].yz) & 1;
-      re += odd ? -sh.terms[t].cb_re : sh.terms[t].cb_re;
-      im += odd ? -sh.terms[t].cb_im : sh.terms[t].cb_im;
+    for (int t = 0; t < T; ++t) {
+      const MaskTerm m = sh.terms[t];
+      if (static_cast<int>(m.flip) != fg) continue;
+      const bool odd = __popcll(static_cast<uint64_t>(i) & m.yz) & 1;
+      re += odd ? -m.cb_re : m.cb_re;
+      im += odd ? -m.cb_im : m.cb_im;
     }
     sh.tab[g * D + i] = make_double2(re, im);
   }
