@@ -554,7 +554,10 @@ __device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int p
     bc[2 * t] = p.bc1[t];
     bc[2 * t + 1] = p.bc2[t];
   }
-  __syncthreads();
+  // single-warp CTAs read bc after build_tables' __syncwarp; PES CTAs after
+  // the chemistry's first __syncthreads, so the copy's load latency overlaps
+  // the pair-factor stage instead of stalling the whole CTA here
+  if (!PES) __syncthreads();
   gmark(prob, 0);
   if (PES) {
     if (p.grid_n > 0) {  // grid mode: the range check (chem.hpp:33-34) is ours
