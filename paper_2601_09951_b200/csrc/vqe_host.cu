@@ -226,7 +226,7 @@ const double* device_bias_tables(int device, const vqf_adam_config& c, int32_t T
 // their D2H copy).  One H2D copy in, one D2H copy out.
 struct SmallStage {
   size_t o_bc1, o_bc2, o_bonds, o_terms, o_toff, o_init, o_status, in_end;
-  size_t o_energy, o_theta, o_iters, o_conv, o_errv, o_erri, o_errt, o_hk, o_hc, o_hn, o_hf, o_traj, out_end, total;
+  size_t o_energy, o_theta, o_iters, o_conv, o_errv, o_erri, o_errt, o_hk, o_hc, o_hn, o_hf, o_clk, o_traj, out_end, total;
   uint32_t stride = 1;
   std::vector<double> bc1, bc2;
 
@@ -255,6 +255,7 @@ struct SmallStage {
     o_hc = c.take<double>(j.want_ham ? (size_t)B * 16 : 0);
     o_hn = c.take<int32_t>(j.want_ham ? B : 0);
     o_hf = c.take<double>(j.want_ham ? (size_t)B * 4 : 0);
+    o_clk = c.take<uint64_t>(2 * (size_t)B);
     out_end = c.off;
     o_traj = c.take<double>((size_t)B * stride);
     total = c.off;
@@ -327,6 +328,7 @@ struct SmallStage {
       p.ham_count = reinterpret_cast<int32_t*>(out + o_hn);
       p.hf_out = reinterpret_cast<double*>(out + o_hf);
     }
+    p.clk = reinterpret_cast<unsigned long long*>(out + o_clk);
     return p;
   }
 
@@ -373,9 +375,9 @@ void run_small(SmallJob& j, int device, bool want_traj = true, size_t* h2d = nul
   const bool staged = p.grid_n == 0;  // grid mode needs no inputs from the host
   HMARK("stage+params");
   if (staged) VQF_CUDA(cudaMemcpyAsync(dev, pin, st.in_end, cudaMemcpyHostToDevice, ws.stream));
-  VQF_CUDA(cudaEventRecord(ws.ev0, ws.stream));
+  auto* clk = reinterpret_cast<uint64_t*>(pin + st.o_clk);  // zero-copy: the kernel stamps CTA entry / result
+  std::memset(clk, 0, 2 * sizeof(uint64_t) * j.batch);
   launch_vqe_small(p, j.batch, j.pes, ws.stream);
-  VQF_CUDA(cudaEventRecord(ws.ev1, ws.stream));
   HMARK("launch");
   if (want_traj)  // outputs arrive zero-copy; only trajectories need a copy
     VQF_CUDA(cudaMemcpyAsync(pin + st.o_traj, dev + st.o_traj, st.total - st.o_traj, cudaMemcpyDeviceToHost,
@@ -383,9 +385,13 @@ void run_small(SmallJob& j, int device, bool want_traj = true, size_t* h2d = nul
   HMARK("d2h issue");
   VQF_CUDA(cudaStreamSynchronize(ws.stream));
   HMARK("sync");
-  float ms = 0.f;
-  VQF_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
-  j.device_seconds = ms * 1e-3;
+  // device time of the launch: first CTA entry to last result write
+  uint64_t t0 = UINT64_MAX, t1 = 0;
+  for (uint32_t b = 0; b < j.batch; ++b) {
+    if (clk[2 * b]) t0 = std::min<uint64_t>(t0, clk[2 * b]);
+    t1 = std::max<uint64_t>(t1, clk[2 * b + 1]);
+  }
+  j.device_seconds = (t1 > t0 && t0 != UINT64_MAX) ? (t1 - t0) * 1e-9 : 0.0;
   st.unpack(j, pin, want_traj);
   HMARK("unpack");
   if (h2d) *h2d = staged ? st.in_end : 0;

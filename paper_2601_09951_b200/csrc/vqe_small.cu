@@ -218,6 +218,12 @@ __device__ __forceinline__ double2 circuit_energy(const Shared& sh, const double
   return acc;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Folds the mask terms into per-flip-group amplitude tables (warp 0).
 // Groups are numbered in order of first appearance after the diagonal
 // group 0: lane t flags term t when no earlier term has its flip, and a
@@ -549,7 +555,10 @@ __device__ __forceinline__ void gmark(int, int) {}
 template <bool PES>
 __device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int prob, double* bc, int D) {
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) sh.stop = 0;
+  if (threadIdx.x == 0) {
+    sh.stop = 0;
+    if (p.clk) p.clk[2 * prob] = global_ns();
+  }
   for (int t = threadIdx.x; t < p.max_iterations; t += blockDim.x) {
     bc[2 * t] = p.bc1[t];
     bc[2 * t + 1] = p.bc2[t];
@@ -796,6 +805,7 @@ __device__ __forceinline__ void h2_optimise(const Shared& sh, const SmallParams&
   (void)g_loop;
 #endif
   if (lane == 0) {
+    if (p.clk) p.clk[2 * prob + 1] = global_ns();
     p.iters[prob] = iters;
     p.converged[prob] = converged;
     p.energy[prob] = e_final;
@@ -990,6 +1000,7 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32) k_vqe_warp(SmallParams
   }
   if (status) return;
   if (lane == 0) {
+    if (p.clk) p.clk[2 * prob + 1] = global_ns();
     p.iters[prob] = iters;
     p.converged[prob] = converged;
     p.energy[prob] = traj[converged ? iters : p.max_iterations];

@@ -57,6 +57,9 @@ struct SmallParams {
   double* ham_coeffs;   // batch * 16
   int32_t* ham_count;   // batch
   double* hf_out;       // batch * 4
+  // optional device timing (may be null): %globaltimer at CTA entry and at
+  // the CTA's result write, 2 per problem (ns); replaces host-side events
+  unsigned long long* clk;
 };
 
 size_t small_smem_bytes();
