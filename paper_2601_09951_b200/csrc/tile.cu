@@ -31,7 +31,18 @@ namespace {
 constexpr int kMaxOps = 64;        // TileParams stays under the 4 KB kernel-parameter limit
 constexpr int kMaxHigh = 6;
 constexpr int kTileBlocks = 148;   // persistent: one CTA per SM
-constexpr int kStages = 3;         // TMA ring depth (3 x 64 KB)
+#ifndef VQF_TILE_GROUPS
+#define VQF_TILE_GROUPS 3
+#endif
+#ifndef VQF_TILE_STAGES
+#define VQF_TILE_STAGES 2
+#endif
+#ifndef VQF_TILE_NT
+#define VQF_TILE_NT 128
+#endif
+constexpr int kGroups = VQF_TILE_GROUPS;  // consumer groups per CTA
+constexpr int kNT = VQF_TILE_NT;          // threads per group (half of it for 4-bit fused ops in fp64)
+constexpr int kStages = VQF_TILE_STAGES;  // TMA ring depth per group (32 KB tiles)
 constexpr int kMaxFuse = 4;        // local bits of one fused op (16 amplitudes per thread)
 constexpr uint32_t kMatElems = 2560;  // composed fused-op matrices per pass (20 KB of fp64)
 // fp64 passes run 512 threads with fused ops of <= 3 bits (8 amplitudes in
@@ -250,7 +261,7 @@ __device__ __forceinline__ void group_sync(uint32_t group) {
 // Each tile: the pass's fused ops (y = U x on 2^m amplitudes per thread),
 // then coalesced 16-byte stores back to HBM.
 template <typename T, int NT, int MAXM, bool PERM>
-__global__ void __launch_bounds__(2 * NT, 1)
+__global__ void __launch_bounds__(kGroups * NT, 1)
     k_tile(typename V2<T>::type* __restrict__ a, const __grid_constant__ CUtensorMap map, const TileParams p) {
   using A = typename V2<T>::type;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -263,9 +274,9 @@ __global__ void __launch_bounds__(2 * NT, 1)
   const uint32_t amps_per_row = 128 / sizeof(A);
   const uint32_t group = threadIdx.x / NT, gt = threadIdx.x % NT;
   unsigned char* ring = smem + (size_t)group * kStages * tile_bytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * kStages * (size_t)tile_bytes) + group * kStages;
-  T* U = reinterpret_cast<T*>(smem + 2 * kStages * (size_t)tile_bytes + 128);  // composed fused-op matrices
-  __shared__ uint64_t run_off_all[2][1 << kMaxHigh];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kGroups * kStages * (size_t)tile_bytes) + group * kStages;
+  T* U = reinterpret_cast<T*>(smem + kGroups * kStages * (size_t)tile_bytes + 256);  // composed fused-op matrices
+  __shared__ uint64_t run_off_all[kGroups][1 << kMaxHigh];
   uint64_t* run_off = run_off_all[group];
   A* s = a + ((uint64_t)blockIdx.y << p.n);
   const uint64_t n_tiles = uint64_t{1} << (p.n - LB);
@@ -295,8 +306,8 @@ __global__ void __launch_bounds__(2 * NT, 1)
       tma_load_run(dst + (size_t)j * run_bytes, &map, static_cast<int32_t>(run_start(p, tile, j) / amps_per_row),
                    static_cast<int32_t>(blockIdx.y), &bar[st]);
   };
-  // the group's tiles: blockIdx.x + (2 i + group) * gridDim.x
-  const uint64_t step = 2 * (uint64_t)gridDim.x;
+  // the group's tiles: blockIdx.x + (kGroups i + group) * gridDim.x
+  const uint64_t step = kGroups * (uint64_t)gridDim.x;
   const uint64_t first = blockIdx.x + (uint64_t)group * gridDim.x;
   if (gt < 32)
     for (int st = 0; st < kStages - 1; ++st) {
@@ -627,14 +638,14 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
     maps.emplace_back(key, state_map(sv, run_bytes));
     map = &maps.back().second;
   }
-  const size_t smem = 2 * kStages * (sizeof(typename V2<T>::type) << LB) + 128 + kMatElems * sizeof(T) + 1024;  // rings + mbarriers + matrices + align
+  const size_t smem = kGroups * kStages * (sizeof(typename V2<T>::type) << LB) + 256 + kMatElems * sizeof(T) + 1024;  // rings + mbarriers + matrices + align
   auto* amps = static_cast<typename V2<T>::type*>(sv->amps);
   if (p.perm_only)
-    k_tile<T, 256, 1, true><<<dim3(grid, sv->batch), 512, smem, sv->stream>>>(amps, *map, p);
+    k_tile<T, kNT, 1, true><<<dim3(grid, sv->batch), kGroups * kNT, smem, sv->stream>>>(amps, *map, p);
   else if (sizeof(T) == 4 || !wide)
-    k_tile<T, 256, sizeof(T) == 4 ? 4 : 3, false><<<dim3(grid, sv->batch), 512, smem, sv->stream>>>(amps, *map, p);
+    k_tile<T, kNT, sizeof(T) == 4 ? 4 : 3, false><<<dim3(grid, sv->batch), kGroups * kNT, smem, sv->stream>>>(amps, *map, p);
   else
-    k_tile<T, 128, 4, false><<<dim3(grid, sv->batch), 256, smem, sv->stream>>>(amps, *map, p);
+    k_tile<T, kNT / 2, 4, false><<<dim3(grid, sv->batch), kGroups * kNT / 2, smem, sv->stream>>>(amps, *map, p);
   VQF_LAUNCHED();
   }
 }
@@ -674,12 +685,12 @@ int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, cons
   tile_shape(n, sv->dtype, B, kmax);
   static thread_local int opted = -1;
   if (opted != sv->device) {
-    const int bytes = 2 * kStages * 32 * 1024 + 128 + kMatElems * 8 + 1024;
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 256, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 128, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, 256, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, 256, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, 256, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    const int bytes = kGroups * kStages * 32 * 1024 + 256 + kMatElems * 8 + 1024;
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, kNT, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, kNT / 2, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, kNT, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, kNT, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, kNT, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     opted = sv->device;
   }
   const std::vector<Pass> passes = schedule(n, B, kmax, gates);
