@@ -37,6 +37,9 @@ constexpr int kTileBlocks = 148;   // persistent: one CTA per SM
 #ifndef VQF_TILE_STAGES
 #define VQF_TILE_STAGES 2
 #endif
+#ifndef VQF_TILE_LB
+#define VQF_TILE_LB 11  // fp64 tile = 2^11 amplitudes (32 KB); fp32 one bit more
+#endif
 #ifndef VQF_TILE_NT
 #define VQF_TILE_NT 128
 #endif
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(kGroups * NT, 1)
       group_sync<NT>(group);
     }
     // write-back: coalesced 16-byte stores, consecutive threads along a run
-    if (gt < n_runs) run_off[gt] = run_start(p, tile, gt);
+    for (uint32_t j = gt; j < n_runs; j += NT) run_off[j] = run_start(p, tile, j);
     group_sync<NT>(group);
     const uint32_t low_mask = run_amps - 1;
     if constexpr (PERM) {
@@ -362,7 +365,7 @@ struct Pass {
 void tile_shape(uint32_t n, int32_t dtype, uint32_t& B, uint32_t& kmax) {
   // 32 KB tiles (two groups x kStages per CTA) in runs of 512 B (one TMA box
   // of 4 rows x 128 B): B = 5 (fp64) / 6 (fp32), leaving 6 gathered high bits
-  const uint32_t LB = dtype == VQF_F64 ? 11 : 12;
+  const uint32_t LB = dtype == VQF_F64 ? VQF_TILE_LB : VQF_TILE_LB + 1;
   B = std::min<uint32_t>(n, LB - kMaxHigh);
   kmax = std::min<uint32_t>(LB - B, n - B);
 }
@@ -685,7 +688,7 @@ int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, cons
   tile_shape(n, sv->dtype, B, kmax);
   static thread_local int opted = -1;
   if (opted != sv->device) {
-    const int bytes = kGroups * kStages * 32 * 1024 + 256 + kMatElems * 8 + 1024;
+    const int bytes = kGroups * kStages * (16 << VQF_TILE_LB) + 256 + kMatElems * 8 + 1024;
     VQF_CUDA(cudaFuncSetAttribute(k_tile<double, kNT, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     VQF_CUDA(cudaFuncSetAttribute(k_tile<double, kNT / 2, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     VQF_CUDA(cudaFuncSetAttribute(k_tile<float, kNT, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
