@@ -211,25 +211,71 @@ __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, co
     sd[r] = swz<T>(d);
   }
   const T* u = U + f.uoff;
-  for (uint32_t w = gt; w < (NL >> M); w += NT) {
+  const uint32_t items = NL >> M;
+  const auto base_of = [&](uint32_t w) {
     uint32_t base = w;
 #pragma unroll
     for (int j = 0; j < M; ++j) base = ((base >> pos[j]) << (pos[j] + 1)) | (base & ((1u << pos[j]) - 1));
-    const uint32_t sb = swz<T>(base);
-    A x[D];
+    return swz<T>(base);
+  };
+  using P2 = typename V2<T>::type;
+  if constexpr (M <= 3) {
+    // two work items per step: both items' loads in flight together and each
+    // 16-byte matrix-row load feeds both (the tile has 2 x NT items for m = 3)
+    for (uint32_t w = gt; w < items; w += 2 * NT) {
+      const bool two = w + NT < items;
+      const uint32_t sb0 = base_of(w), sb1 = two ? base_of(w + NT) : sb0;
+      A x0[D], x1[D];
 #pragma unroll
-    for (int r = 0; r < D; ++r) x[r] = t[sb ^ sd[r]];
+      for (int r = 0; r < D; ++r) {
+        x0[r] = t[sb0 ^ sd[r]];
+        x1[r] = t[sb1 ^ sd[r]];
+      }
 #pragma unroll
-    for (int r = 0; r < D; ++r) {
-      // row r of U as 16-byte broadcast loads; two accumulation chains per
-      // component (even / odd columns) halve the dependent-FMA depth
-      A y0, y1;
-      y0.x = y0.y = y1.x = y1.y = T(0);
-      if constexpr (D == 1) {
-        y0.x = u[0] * x[0].x;
-        y0.y = u[0] * x[0].y;
-      } else {
-        using P2 = typename V2<T>::type;
+      for (int r = 0; r < D; ++r) {
+        A a0, a1, b0, b1;  // item 0 / item 1, even / odd columns
+        a0.x = a0.y = a1.x = a1.y = b0.x = b0.y = b1.x = b1.y = T(0);
+        if constexpr (D == 1) {
+          a0.x = u[0] * x0[0].x;
+          a0.y = u[0] * x0[0].y;
+          b0.x = u[0] * x1[0].x;
+          b0.y = u[0] * x1[0].y;
+        } else {
+          const P2* row = reinterpret_cast<const P2*>(u + r * D);
+#pragma unroll
+          for (int c = 0; c < D; c += 2) {
+            const P2 m = row[c / 2];
+            a0.x = fma(m.x, x0[c].x, a0.x);
+            a0.y = fma(m.x, x0[c].y, a0.y);
+            a1.x = fma(m.y, x0[c + 1].x, a1.x);
+            a1.y = fma(m.y, x0[c + 1].y, a1.y);
+            b0.x = fma(m.x, x1[c].x, b0.x);
+            b0.y = fma(m.x, x1[c].y, b0.y);
+            b1.x = fma(m.y, x1[c + 1].x, b1.x);
+            b1.y = fma(m.y, x1[c + 1].y, b1.y);
+          }
+        }
+        A y0, y1;
+        y0.x = a0.x + a1.x;
+        y0.y = a0.y + a1.y;
+        y1.x = b0.x + b1.x;
+        y1.y = b0.y + b1.y;
+        t[sb0 ^ sd[r]] = y0;
+        if (two) t[sb1 ^ sd[r]] = y1;
+      }
+    }
+  } else {
+    for (uint32_t w = gt; w < items; w += NT) {
+      const uint32_t sb = base_of(w);
+      A x[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) x[r] = t[sb ^ sd[r]];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        // row r of U as 16-byte broadcast loads; two accumulation chains per
+        // component (even / odd columns) halve the dependent-FMA depth
+        A y0, y1;
+        y0.x = y0.y = y1.x = y1.y = T(0);
         const P2* row = reinterpret_cast<const P2*>(u + r * D);
 #pragma unroll
         for (int c = 0; c < D; c += 2) {
@@ -239,11 +285,11 @@ __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, co
           y1.x = fma(m.y, x[c + 1].x, y1.x);
           y1.y = fma(m.y, x[c + 1].y, y1.y);
         }
+        A y;
+        y.x = y0.x + y1.x;
+        y.y = y0.y + y1.y;
+        t[sb ^ sd[r]] = y;
       }
-      A y;
-      y.x = y0.x + y1.x;
-      y.y = y0.y + y1.y;
-      t[sb ^ sd[r]] = y;
     }
   }
 }
