@@ -47,7 +47,8 @@ constexpr int kGroups = VQF_TILE_GROUPS;  // consumer groups per CTA
 constexpr int kNT = VQF_TILE_NT;          // threads per group (half of it for 4-bit fused ops in fp64)
 constexpr int kStages = VQF_TILE_STAGES;  // TMA ring depth per group (32 KB tiles)
 constexpr int kMaxFuse = 4;        // local bits of one fused op (16 amplitudes per thread)
-constexpr uint32_t kMatElems = 2560;  // composed fused-op matrices per pass (20 KB of fp64)
+constexpr uint32_t kMatElems = 2560;
+constexpr int kDq = 4;  // item groups per step of the tensor-core fused op  // composed fused-op matrices per pass (20 KB of fp64)
 // fp64 passes run 512 threads with fused ops of <= 3 bits (8 amplitudes in
 // registers, <= 128 registers), or 256 threads when a DoubleExcitation needs
 // a 4-bit op; fp32 always 512 threads x <= 4 bits
@@ -219,6 +220,64 @@ __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, co
     return swz<T>(base);
   };
   using P2 = typename V2<T>::type;
+  if constexpr (M == 3 && sizeof(T) == 8) {
+    if (items >= 4 * NT / 32 * kDq) {
+      // fp64 tensor cores: Y (8 slots x 2 columns per item) = U (8 x 8) X as
+      // mma.sync m8n8k4 f64 over groups of four items (eight real columns:
+      // item-major, re / im).  Fragments (PTX m8n8k4 .f64, g = lane / 4,
+      // t = lane % 4): A[g][t] -> U[g][k0 + t]; B[t][g] -> X[k0 + t][col g] =
+      // component (g & 1) of slot k0 + t of item g / 2; D[g][2t + i] ->
+      // component i of slot g of item t.  One warp instruction does 256
+      // FMAs; kDq item groups per step keep loads and MMAs in flight.
+      const uint32_t lane = gt & 31u, g = lane >> 2, tq = lane & 3u;
+      const double a_lo = u[g * 8 + tq], a_hi = u[g * 8 + 4 + tq];
+      const double* td = reinterpret_cast<const double*>(t);
+      // item 4q + i = base(4q) | base(i) for i < 4 (disjoint bits) and the
+      // swizzle is xor-linear, so the per-lane parts are fixed per op and
+      // each item group costs one (warp-uniform) base computation
+      const uint32_t in_lo = 2 * (base_of(g >> 1) ^ sd[tq]) + (g & 1u);
+      const uint32_t in_hi = 2 * (base_of(g >> 1) ^ sd[4 + tq]) + (g & 1u);
+      const uint32_t out_off = base_of(tq) ^ sd[g];
+      const uint32_t groups = items >> 2, wstride = NT / 32;
+      // groups q0 + d (q0 a multiple of kDq): base(4 (q0 + d)) =
+      // base(4 q0) | base(4 d), so one base per step plus fixed offsets
+      uint32_t offd[kDq];
+#pragma unroll
+      for (int d = 0; d < kDq; ++d) offd[d] = base_of(4 * d);
+      for (uint32_t q0 = (gt >> 5) * kDq; q0 < groups; q0 += wstride * kDq) {
+        double b_lo[kDq], b_hi[kDq], c0[kDq], c1[kDq];
+        uint32_t sb_out[kDq];
+        const uint32_t sbq = base_of(4 * q0);
+#pragma unroll
+        for (int d = 0; d < kDq; ++d) {
+          const uint32_t sb4 = sbq ^ offd[d];
+          sb_out[d] = sb4 ^ out_off;
+          b_lo[d] = td[(2 * sb4) ^ in_lo];
+          b_hi[d] = td[(2 * sb4) ^ in_hi];
+          c0[d] = 0.0;
+          c1[d] = 0.0;
+        }
+#pragma unroll
+        for (int d = 0; d < kDq; ++d)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(c0[d]), "+d"(c1[d])
+                       : "d"(a_lo), "d"(b_lo[d]));
+#pragma unroll
+        for (int d = 0; d < kDq; ++d)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(c0[d]), "+d"(c1[d])
+                       : "d"(a_hi), "d"(b_hi[d]));
+#pragma unroll
+        for (int d = 0; d < kDq; ++d) {
+          A y;
+          y.x = c0[d];
+          y.y = c1[d];
+          t[sb_out[d]] = y;
+        }
+      }
+      return;
+    }
+  }
   if constexpr (M <= 3) {
     // two work items per step: both items' loads in flight together and each
     // 16-byte matrix-row load feeds both (the tile has 2 x NT items for m = 3)
