@@ -93,6 +93,26 @@ def test_fused_circuit_equals_per_gate(gpu, n, dtype):
     assert np.max(np.abs(a.amplitudes - b.amplitudes)) < tol
 
 
+@pytest.mark.parametrize("n,batch", [(22, 1), (14, 3)])
+def test_fused_wide_circuits_and_batches(gpu, n, batch):
+    # larger registers: many passes, 4-bit DoubleExcitation ops (wide kernel),
+    # 3-bit tensor-core ops and permutation passes in one circuit; batched
+    # states (one CTA row per entry) against the per-gate kernels
+    V = gpu
+    pr = random.Random(777 + n)
+    gates = [gpu_gate(V, *g) for g in rand_gates(pr, n, 150)]
+    gates += [V.Gate.cnot(q, q + 1) for q in range(n - 1)] + [V.Gate.double_excitation(0.3, n - 4, n - 1, 0, 2)]
+    rng = np.random.default_rng(n)
+    psi0 = np.concatenate([random_state(rng, n) for _ in range(batch)])
+    a, b = V.StateVector(n, batch=batch), V.StateVector(n, batch=batch)
+    a.amplitudes = psi0
+    b.amplitudes = psi0
+    V.apply_circuit(a, gates)
+    for g in gates:
+        V.apply_gate(b, g)
+    assert np.max(np.abs(a.amplitudes - b.amplitudes)) < 1e-12
+
+
 @pytest.mark.parametrize("n,dtype", [(5, "f64"), (12, "f64"), (16, "f64"), (19, "f32")])
 def test_fused_permutation_passes(gpu, n, dtype):
     # X / CNOT-only circuits: every tile pass is an affine index map applied
