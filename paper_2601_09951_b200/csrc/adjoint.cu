@@ -241,9 +241,9 @@ __global__ void __launch_bounds__(kThreads) k_adj_givens(typename V2<T>::type* _
 // 0, 1, ..., K-1 in turn: psi' = G^dag psi, g_j += Re<lambda| dG psi'>,
 // lambda' = G^dag lambda.  Per-block partials per gate.
 struct RyGroup {
-  uint32_t bit[3];
-  double c[3], s[3];
-  double* part[3];  // gate j's per-block partial row
+  uint32_t bit[4];
+  double c[4], s[4];
+  double* part[4];  // gate j's per-block partial row
 };
 
 template <typename T, int K>
@@ -437,7 +437,7 @@ void run_t(AdjointPlan& pl, const std::vector<AdjGate>& prog, const std::vector<
     // two-vector pass for the group instead of one per gate
     if (g.kind == VQF_GATE_RY && g.param >= 0) {
       size_t cnt = 1;
-      while (cnt < 3 && gi >= cnt && prog[gi - cnt].kind == VQF_GATE_RY && prog[gi - cnt].param >= 0) {
+      while (cnt < 4 && gi >= cnt && prog[gi - cnt].kind == VQF_GATE_RY && prog[gi - cnt].param >= 0) {
         bool distinct = true;
         for (size_t q = 0; q < cnt; ++q) distinct = distinct && prog[gi - cnt].wires[0] != prog[gi - q].wires[0];
         if (!distinct) break;
@@ -454,7 +454,8 @@ void run_t(AdjointPlan& pl, const std::vector<AdjGate>& prog, const std::vector<
           gr.part[q] = pl.gpart + (size_t)h.param * pl.nb;
         }
         if (cnt == 2) k_adj_ry_multi<T, 2><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr);
-        else k_adj_ry_multi<T, 3><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr);
+        else if (cnt == 3) k_adj_ry_multi<T, 3><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr);
+        else k_adj_ry_multi<T, 4><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr);
         VQF_LAUNCHED();
         gi -= cnt - 1;
         continue;
