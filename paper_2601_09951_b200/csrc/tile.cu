@@ -48,7 +48,8 @@ constexpr int kNT = VQF_TILE_NT;          // threads per group (half of it for 4
 constexpr int kStages = VQF_TILE_STAGES;  // TMA ring depth per group (32 KB tiles)
 constexpr int kMaxFuse = 4;        // local bits of one fused op (16 amplitudes per thread)
 constexpr uint32_t kMatElems = 2560;
-constexpr int kDq = 4;  // item groups per step of the tensor-core fused op  // composed fused-op matrices per pass (20 KB of fp64)
+constexpr int kDq = 4;  // item groups per step of the tensor-core fused op
+constexpr uint32_t kNoMma = 1u << 31;  // TileFop::ipos: run this op on the FMA path  // composed fused-op matrices per pass (20 KB of fp64)
 // fp64 passes run 512 threads with fused ops of <= 3 bits (8 amplitudes in
 // registers, <= 128 registers), or 256 threads when a DoubleExcitation needs
 // a 4-bit op; fp32 always 512 threads x <= 4 bits
@@ -72,6 +73,10 @@ struct TileSub {
 // one shared-memory round trip per op instead of per gate.
 struct TileFop {
   uint32_t m, pos, sub0, n_sub, uoff;  // uoff: the op's matrix in the composed-matrix area
+  // tensor-core ops: the two free local bits that enumerate the four items of
+  // an MMA column group (chosen on the host against shared-memory bank
+  // conflicts; 0 = the lowest free bits), 5 bits each
+  uint32_t ipos;
 };
 
 struct TileParams {
@@ -221,7 +226,7 @@ __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, co
   };
   using P2 = typename V2<T>::type;
   if constexpr (M == 3 && sizeof(T) == 8) {
-    if (items >= 4 * NT / 32 * kDq) {
+    if (f.ipos != kNoMma && items >= 4 * NT / 32 * kDq) {
       // fp64 tensor cores: Y (8 slots x 2 columns per item) = U (8 x 8) X as
       // mma.sync m8n8k4 f64 over groups of four items (eight real columns:
       // item-major, re / im).  Fragments (PTX m8n8k4 .f64, g = lane / 4,
@@ -235,19 +240,48 @@ __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, co
       // item 4q + i = base(4q) | base(i) for i < 4 (disjoint bits) and the
       // swizzle is xor-linear, so the per-lane parts are fixed per op and
       // each item group costs one (warp-uniform) base computation
-      const uint32_t in_lo = 2 * (base_of(g >> 1) ^ sd[tq]) + (g & 1u);
-      const uint32_t in_hi = 2 * (base_of(g >> 1) ^ sd[4 + tq]) + (g & 1u);
-      const uint32_t out_off = base_of(tq) ^ sd[g];
+      // item 4q + i: i on the two chosen free bits c1, c2, q on the other
+      // free bits (ascending): base = ins2(q) | dep2(i), both swizzled apart
+      const uint32_t c1 = f.ipos & 31u, c2 = (f.ipos >> 5) & 31u;
+      const auto dep2 = [&](uint32_t i) { return swz<T>(((i & 1u) << c1) | (((i >> 1) & 1u) << c2)); };
+      uint32_t p5[M + 2];  // zero-insertion positions for q: op bits + c1, c2, ascending
+      {
+        uint32_t all[M + 2];
+#pragma unroll
+        for (int j = 0; j < M; ++j) all[j] = pos[j];
+        all[M] = c1;
+        all[M + 1] = c2;
+#pragma unroll
+        for (int i = 0; i < M + 2; ++i)
+#pragma unroll
+          for (int j = i + 1; j < M + 2; ++j)
+            if (all[j] < all[i]) {
+              const uint32_t tmp = all[i];
+              all[i] = all[j];
+              all[j] = tmp;
+            }
+#pragma unroll
+        for (int j = 0; j < M + 2; ++j) p5[j] = all[j];
+      }
+      const auto ins2 = [&](uint32_t q) {
+        uint32_t b = q;
+#pragma unroll
+        for (int j = 0; j < M + 2; ++j) b = ((b >> p5[j]) << (p5[j] + 1)) | (b & ((1u << p5[j]) - 1));
+        return swz<T>(b);
+      };
+      const uint32_t in_lo = 2 * (dep2(g >> 1) ^ sd[tq]) + (g & 1u);
+      const uint32_t in_hi = 2 * (dep2(g >> 1) ^ sd[4 + tq]) + (g & 1u);
+      const uint32_t out_off = dep2(tq) ^ sd[g];
       const uint32_t groups = items >> 2, wstride = NT / 32;
       // groups q0 + d (q0 a multiple of kDq): base(4 (q0 + d)) =
       // base(4 q0) | base(4 d), so one base per step plus fixed offsets
       uint32_t offd[kDq];
 #pragma unroll
-      for (int d = 0; d < kDq; ++d) offd[d] = base_of(4 * d);
+      for (int d = 0; d < kDq; ++d) offd[d] = ins2(d);
       for (uint32_t q0 = (gt >> 5) * kDq; q0 < groups; q0 += wstride * kDq) {
         double b_lo[kDq], b_hi[kDq], c0[kDq], c1[kDq];
         uint32_t sb_out[kDq];
-        const uint32_t sbq = base_of(4 * q0);
+        const uint32_t sbq = ins2(q0);
 #pragma unroll
         for (int d = 0; d < kDq; ++d) {
           const uint32_t sb4 = sbq ^ offd[d];
@@ -721,15 +755,71 @@ TileParams build_params(uint32_t n, uint32_t batch, uint32_t B, const std::vecto
   return p;
 }
 
+// Item bits of a tensor-core op: the two free local bits c1 < c2 whose
+// shared-memory bank pattern for the MMA fragments (B loads of both
+// k-chunks: 4 slots x 4 items x re/im per warp access; D stores: 8 slots x 4
+// items) has the fewest lanes per bank, under the 128 B swizzle.
+uint32_t choose_item_bits(const TileFop& f, uint32_t LB) {
+  uint32_t pos[3], used = 0;
+  for (uint32_t j = 0; j < 3; ++j) {
+    pos[j] = (f.pos >> (8 * j)) & 0xffu;
+    used |= 1u << pos[j];
+  }
+  const auto swz8 = [](uint32_t L) { return (L ^ (L >> 3)) & 7u; };
+  const auto dep = [&](uint32_t k) {
+    uint32_t d = 0;
+    for (uint32_t j = 0; j < 3; ++j)
+      if ((k >> j) & 1u) d |= 1u << pos[j];
+    return d;
+  };
+  uint32_t best = 0, best_score = ~0u;
+  for (uint32_t c1 = 0; c1 < LB; ++c1) {
+    if ((used >> c1) & 1u) continue;
+    for (uint32_t c2 = c1 + 1; c2 < LB; ++c2) {
+      if ((used >> c2) & 1u) continue;
+      const auto dep2 = [&](uint32_t i) { return ((i & 1u) << c1) | (((i >> 1) & 1u) << c2); };
+      // 8-byte B loads are served per half-warp (16 lanes, bank pair = (amp
+      // mod 8, re/im)), 16-byte D stores per quarter-warp (8 lanes, amp mod
+      // 8): the score adds the worst lane count per bank in each phase
+      uint32_t score = 0;
+      for (uint32_t chunk = 0; chunk < 2; ++chunk)
+        for (uint32_t half = 0; half < 2; ++half) {
+          uint32_t cnt[16] = {};
+          for (uint32_t lane = 16 * half; lane < 16 * half + 16; ++lane) {
+            const uint32_t g = lane >> 2, tq = lane & 3u;
+            cnt[swz8(dep2(g >> 1) | dep(4 * chunk + tq)) * 2 + (g & 1u)]++;
+          }
+          score += *std::max_element(cnt, cnt + 16);
+        }
+      for (uint32_t quarter = 0; quarter < 4; ++quarter) {
+        uint32_t cnt[8] = {};
+        for (uint32_t lane = 8 * quarter; lane < 8 * quarter + 8; ++lane) cnt[swz8(dep2(lane & 3u) | dep(lane >> 2))]++;
+        score += *std::max_element(cnt, cnt + 8);
+      }
+      if (score < best_score) {
+        best_score = score;
+        best = c1 | (c2 << 5);
+      }
+    }
+  }
+  // ops whose slot bits all lie above the swizzle's reach (index bits >= 6)
+  // put several MMA lanes on one bank whatever the item bits; they take the
+  // FMA path, which spreads lanes over items instead
+  return best_score <= 12 ? best : kNoMma;
+}
+
 template <typename T>
 void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pass& pass, uint32_t B,
                  const double* cs_dev) {
   const uint32_t n = sv->n_qubits;
   for (size_t first = 0, next = 0; first < pass.gates.size(); first = next) {
-  const TileParams p = build_params(n, sv->batch, B, gates, pass, cs_dev, sizeof(T) == 8 ? 3 : 4, first, &next);
+  TileParams p = build_params(n, sv->batch, B, gates, pass, cs_dev, sizeof(T) == 8 ? 3 : 4, first, &next);
   bool wide = false;
   for (uint32_t o = 0; o < p.n_fops; ++o) wide = wide || p.fops[o].m == 4;
   const uint32_t LB = B + p.k;
+  if (sizeof(T) == 8)
+    for (uint32_t o = 0; o < p.n_fops; ++o)
+      if (p.fops[o].m == 3) p.fops[o].ipos = choose_item_bits(p.fops[o], LB);
   const uint64_t n_tiles = uint64_t{1} << (n - LB);
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n_tiles, kTileBlocks));
   const uint32_t run_bytes = static_cast<uint32_t>(sizeof(typename V2<T>::type) << B);
