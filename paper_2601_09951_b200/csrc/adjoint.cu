@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_ham(const typename V2<T>::ty
   if (threadIdx.x < h.n_mx) mx[threadIdx.x] = h.mx_t[threadIdx.x];
   __syncthreads();
   double2 acc = make_double2(0.0, 0.0);
+  __shared__ double2 ohi[kMaxGroups];  // per flip group: its tile-constant operator part
   for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     double hre = 0.0, him = 0.0;
     for (uint32_t t = 0; t < h.n_hi; ++t) {
@@ -102,6 +103,20 @@ __global__ void __launch_bounds__(kThreads) k_apply_ham(const typename V2<T>::ty
       hre += sg * h.hi_t[t].cb_re;
       him += sg * h.hi_t[t].cb_im;
     }
+    // terms whose Z/Y support lies at or above the tile bits have one sign
+    // per tile: sum them once per group here, not per amplitude
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < h.n_groups; g += kThreads) {
+      double re = 0.0, im = 0.0;
+      const uint32_t t0 = h.group_off[g];
+      for (uint32_t t = t0; t < t0 + h.group_hi[g]; ++t) {
+        const double sg = parity_sign(tile & (h.terms[t].yz >> B));
+        re += sg * h.terms[t].cb_re;
+        im += sg * h.terms[t].cb_im;
+      }
+      ohi[g] = make_double2(re, im);
+    }
+    __syncthreads();
     const uint64_t base = tile << B;
     for (uint32_t lo0 = threadIdx.x; lo0 < tile_amps; lo0 += kThreads * kU) {
       A x[kU];
@@ -128,19 +143,35 @@ __global__ void __launch_bounds__(kThreads) k_apply_ham(const typename V2<T>::ty
         }
         l[u] = make_double2(dre * (double)x[u].x - dim * (double)x[u].y, dre * (double)x[u].y + dim * (double)x[u].x);
       }
-      for (uint32_t g = 0; g < h.n_groups; ++g) {
-        const uint64_t f = h.flips[g];
-        A y[kU];
+      // software-pipelined partner loads: group g + 1's partners are in
+      // flight while group g's terms are applied
+      A y[kU], yn[kU];
+      if (h.n_groups > 0) {
+        const uint64_t f0 = h.flips[0];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const uint32_t lo = lo0 + u * kThreads;
-          if (lo < tile_amps) y[u] = psi[(base | lo) ^ f];
+          if (lo < tile_amps) yn[u] = psi[(base | lo) ^ f0];
         }
+      }
+      for (uint32_t g = 0; g < h.n_groups; ++g) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) y[u] = yn[u];
+        if (g + 1 < h.n_groups) {
+          const uint64_t fn = h.flips[g + 1];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const uint32_t lo = lo0 + u * kThreads;
+            if (lo < tile_amps) yn[u] = psi[(base | lo) ^ fn];
+          }
+        }
+        const double2 oc = ohi[g];
+        const uint32_t t_lo = h.group_off[g] + h.group_hi[g], t_end = h.group_off[g + 1];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const uint64_t i = base | (lo0 + u * kThreads);
-          double ore = 0.0, oim = 0.0;
-          for (uint32_t t = h.group_off[g]; t < h.group_off[g + 1]; ++t) {
+          double ore = oc.x, oim = oc.y;
+          for (uint32_t t = t_lo; t < t_end; ++t) {
             const double sg = parity_sign(i & h.terms[t].yz);
             ore += sg * h.terms[t].cb_re;
             oim += sg * h.terms[t].cb_im;
@@ -528,9 +559,18 @@ void AdjointPlan::init(vqf_statevector* psi_, vqf_statevector* lam_, const Compi
     else mx.push_back(m);
   }
   if (mx.size() > 64) throw_invalid("adjoint gradient: more than 64 diagonal terms straddle the tile boundary");
+  std::vector<uint32_t> ghi;
   for (size_t g = 1; g + 1 < h.group_offset.size(); ++g) {
     flips.push_back(h.group_flip[g]);
-    for (uint32_t t = h.group_offset[g]; t < h.group_offset[g + 1]; ++t) off.push_back(h.terms[t]);
+    uint32_t nh = 0;
+    for (uint32_t t = h.group_offset[g]; t < h.group_offset[g + 1]; ++t)  // tile-constant terms first
+      if ((h.terms[t].yz & lo_mask) == 0) {
+        off.push_back(h.terms[t]);
+        ++nh;
+      }
+    for (uint32_t t = h.group_offset[g]; t < h.group_offset[g + 1]; ++t)
+      if ((h.terms[t].yz & lo_mask) != 0) off.push_back(h.terms[t]);
+    ghi.push_back(nh);
     goff.push_back(static_cast<uint32_t>(off.size()));
   }
   if (flips.size() > kMaxGroups || off.size() > kMaxTerms) throw_invalid("adjoint gradient: Hamiltonian too large");
@@ -547,6 +587,7 @@ void AdjointPlan::init(vqf_statevector* psi_, vqf_statevector* lam_, const Compi
   const size_t o_fl = put(flips.data(), flips.size() * sizeof(uint64_t));
   const size_t o_go = put(goff.data(), goff.size() * sizeof(uint32_t));
   const size_t o_te = put(off.data(), off.size() * sizeof(MaskTerm));
+  const size_t o_gh = put(ghi.data(), ghi.size() * sizeof(uint32_t));
   const size_t o_gp = put(nullptr, 0);
   blob.resize(o_gp);
   const size_t bytes = o_gp + sizeof(double) * ((size_t)P * nb + 2 * (size_t)nb_ham + P + 2);
@@ -559,7 +600,8 @@ void AdjointPlan::init(vqf_statevector* psi_, vqf_statevector* lam_, const Compi
                reinterpret_cast<const MaskTerm*>(d + o_mx), static_cast<uint32_t>(lo.size()),
                static_cast<uint32_t>(hi.size()), static_cast<uint32_t>(mx.size()),
                reinterpret_cast<const uint64_t*>(d + o_fl), reinterpret_cast<const uint32_t*>(d + o_go),
-               reinterpret_cast<const MaskTerm*>(d + o_te), static_cast<uint32_t>(flips.size())};
+               reinterpret_cast<const uint32_t*>(d + o_gh), reinterpret_cast<const MaskTerm*>(d + o_te),
+               static_cast<uint32_t>(flips.size())};
   gpart = reinterpret_cast<double*>(d + o_gp);
   epart = gpart + (size_t)P * nb;
   dout = epart + 2 * (size_t)nb_ham;

@@ -25,6 +25,7 @@ struct HamDevC {
   uint32_t n_lo, n_hi, n_mx;
   const uint64_t* flips;
   const uint32_t* group_off;
+  const uint32_t* group_hi;  // per group: its first group_hi terms have Z/Y only at or above the tile bits
   const MaskTerm* terms;
   uint32_t n_groups;
 };
