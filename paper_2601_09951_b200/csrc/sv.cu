@@ -209,6 +209,19 @@ __device__ __forceinline__ double2 block_sum(double2 v) {
 
 __device__ __forceinline__ double parity_sign(uint64_t x) { return (__popcll(x) & 1) ? -1.0 : 1.0; }
 
+// conj(a) b as (re, im) in double.  fp64 states: fp64 products; fp32 states:
+// the two products per component in fp32 (one FFMA each, no conversions on
+// the operands; ~6e-8 relative, inside the 1e-5 fp32 bar), accumulated by
+// the caller in fp64.
+__device__ __forceinline__ void conj_mul(double2 a, double2 b, double& re, double& im) {
+  re = __fma_rn(a.x, b.x, a.y * b.y);
+  im = __fma_rn(a.x, b.y, -(a.y * b.x));
+}
+__device__ __forceinline__ void conj_mul(float2 a, float2 b, double& re, double& im) {
+  re = static_cast<double>(__fmaf_rn(a.x, b.x, a.y * b.y));
+  im = static_cast<double>(__fmaf_rn(a.x, b.y, -(a.y * b.x)));
+}
+
 // Diagonal group: sum_i |psi_i|^2 * sum_t cb_t (-1)^popc(i & yz_t)
 // (statevector.hpp:227-234, all diagonal terms fused into one pass).
 // grid = (blocks, batch); partials[(entry * G + group) * blocks + block].
@@ -521,8 +534,8 @@ __global__ void __launch_bounds__(kThreads) k_expect_flip(const typename V2<T>::
         if (k0 + u * stride >= half) break;
         const uint64_t i = idx[u];
         // v = conj(x) * y
-        const double vr = (double)x[u].x * (double)y[u].x + (double)x[u].y * (double)y[u].y;
-        const double vi = (double)x[u].x * (double)y[u].y - (double)x[u].y * (double)y[u].x;
+        double vr, vi;
+        conj_mul(x[u], y[u], vr, vi);
         double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
         for (uint32_t t = 0; t < cnt; ++t) {
           const double sg = parity_sign(i & st[t].yz);
@@ -648,8 +661,7 @@ __device__ __forceinline__ void multi_group(const A (&x)[kRegAmps], uint32_t fl,
       y.x = __shfl_xor_sync(0xffffffffu, y.x, fl);
       y.y = __shfl_xor_sync(0xffffffffu, y.y, fl);
     }
-    vr[k] = __fma_rn((double)x[r].x, (double)y.x, (double)x[r].y * (double)y.y);
-    vi[k] = __fma_rn((double)x[r].x, (double)y.y, -((double)x[r].y * (double)y.x));
+    conj_mul(x[r], y, vr[k], vi[k]);
     ++k;
   }
   multi_terms(vr, vi, need_im, base, false, st, sig, t0, t1, acc_re, acc_im);
@@ -672,8 +684,10 @@ __device__ __forceinline__ void multi_group_lane(const A (&x)[kRegAmps], uint32_
     A y = side ? x[k] : x[k + kRegAmps / 2];
     y.x = __shfl_xor_sync(0xffffffffu, y.x, fl);
     y.y = __shfl_xor_sync(0xffffffffu, y.y, fl);
-    vr[k] = __fma_rn((double)own.x, (double)y.x, (double)own.y * (double)y.y);
-    vi[k] = flip_sign(__fma_rn((double)own.x, (double)y.y, -((double)own.y * (double)y.x)), side ? 1u : 0u);
+    double ur, u;
+    conj_mul(own, y, ur, u);
+    vr[k] = ur;
+    vi[k] = flip_sign(u, side ? 1u : 0u);
   }
   multi_terms(vr, vi, need_im, base, side, st, sig, t0, t1, acc_re, acc_im);
 }
