@@ -561,6 +561,83 @@ __global__ void __launch_bounds__(kThreads) k_expect_flip(const typename V2<T>::
   }
 }
 
+// One flip group whose top flip bit hb is >= 11, factorised like the
+// diagonal pass: pair index k = (tile << 11) | lo_u, lo_u = t + 256 u, so the
+// pair's index is i = (I(tile) << 11) | lo_u with I(tile) = tile with a zero
+// inserted at bit hb - 11, and each term's sign splits into
+// parity(((I << 8) | t) & m) (host packs m = (yz >> 11) << 8 | yz[0..8) into
+// .yz) times (-1)^popc(u & v), v = yz[8..11) (in .flip bits 0-2; bit 3 set
+// when sigma = -1, i.e. odd Y count on the flip).  Per tile a thread forms the
+// 8 pair products and their Walsh-Hadamard transforms; each term then costs
+// one parity and one FMA per tile instead of work per pair.  Terms sorted by
+// v, offsets in DiagSplit::mx_off.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_expect_flip_fact(const typename V2<T>::type* __restrict__ a,
+                                                               uint32_t n, uint64_t flip, uint32_t hb,
+                                                               const MaskTerm* __restrict__ terms, const DiagSplit ds,
+                                                               bool need_im, double* __restrict__ partials,
+                                                               uint32_t G, uint32_t group, uint32_t stride) {
+  using A = typename V2<T>::type;
+  __shared__ MaskTerm st[64];
+  for (uint32_t t = threadIdx.x; t < ds.n_mx; t += kThreads) st[t] = terms[t];
+  __syncthreads();
+  const uint32_t b = blockIdx.y;
+  const uint64_t n_tiles = uint64_t{1} << (n - 1 - kDiagB);
+  const A* s = a + ((uint64_t)b << n);
+  const uint32_t hbt = hb - kDiagB;
+  double acc_re = 0.0, acc_im = 0.0;
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint64_t I = insert_zero(tile, hbt);
+    const uint64_t i0 = (I << kDiagB) | threadIdx.x;
+    A x[kDiagU], y[kDiagU];
+#pragma unroll
+    for (int u = 0; u < (int)kDiagU; ++u) {
+      const uint64_t i = i0 + (uint64_t)u * kThreads;
+      x[u] = s[i];
+      y[u] = s[i ^ flip];
+    }
+    double wr[kDiagU], wi[kDiagU];
+#pragma unroll
+    for (int u = 0; u < (int)kDiagU; ++u) conj_mul(x[u], y[u], wr[u], wi[u]);
+#pragma unroll
+    for (int h = 1; h < (int)kDiagU; h <<= 1)
+#pragma unroll
+      for (int u = 0; u < (int)kDiagU; ++u)
+        if ((u & h) == 0) {
+          const double l = wr[u], r = wr[u | h];
+          wr[u] = l + r;
+          wr[u | h] = l - r;
+          if (need_im) {
+            const double li = wi[u], ri = wi[u | h];
+            wi[u] = li + ri;
+            wi[u | h] = li - ri;
+          }
+        }
+    const uint64_t xt = (I << 8) | threadIdx.x;
+#pragma unroll
+    for (int v = 0; v < (int)kDiagU; ++v)
+      for (uint32_t t = ds.mx_off[v]; t < ds.mx_off[v + 1]; ++t) {
+        const MaskTerm m = st[t];
+        const double sg = parity_sign(xt & m.yz);
+        if ((m.flip & 8u) == 0) {  // sigma = +1: cb s 2 Re(v)
+          const double w = 2.0 * sg * wr[v];
+          acc_re += m.cb_re * w;
+          acc_im += m.cb_im * w;
+        } else {  // sigma = -1: cb s 2i Im(v)
+          const double w = 2.0 * sg * wi[v];
+          acc_re -= m.cb_im * w;
+          acc_im += m.cb_re * w;
+        }
+      }
+  }
+  const double2 acc = block_sum(make_double2(acc_re, acc_im));
+  if (threadIdx.x == 0) {
+    const size_t o = ((size_t)b * G + group) * stride + blockIdx.x;
+    partials[2 * o] = acc.x;
+    partials[2 * o + 1] = acc.y;
+  }
+}
+
 // Several flip groups in one pass.  Each thread holds the 16 amplitudes that
 // differ in four "register" index bits R (all >= 5) of one base index whose
 // bits 0..4 are the lane, so warp loads stay 512 B contiguous.  A group whose
@@ -870,8 +947,14 @@ struct ExpPlan {
   uint32_t o_flo = 0, o_fhi = 0, o_fmx = 0;  // factorised split
   std::vector<MultiLaunch> multi;
   std::vector<uint32_t> single;  // flip groups read by their own k_expect_flip pass
+  struct FactFlip {
+    uint32_t group, term_base;
+    DiagSplit ds;
+    bool need_im;
+  };
+  std::vector<FactFlip> fact;  // single groups on k_expect_flip_fact (top flip bit >= 11)
   uint32_t state_passes() const {
-    return (diag != DIAG_NONE ? 1u : 0u) + static_cast<uint32_t>(multi.size() + single.size());
+    return (diag != DIAG_NONE ? 1u : 0u) + static_cast<uint32_t>(multi.size() + single.size() + fact.size());
   }
 };
 
@@ -955,6 +1038,38 @@ ExpPlan plan_expectation(const CompiledHam& h, uint32_t n) {
     }
     dst->rset |= out;
     dst->groups.push_back(g);
+  }
+  // single groups with a high top flip bit: factorised pass
+  if (n >= kDiagB + 2) {
+    std::vector<uint32_t> keep;
+    for (const uint32_t g : pl.single) {
+      const uint64_t f = h.group_flip[g];
+      const uint32_t hb = 63 - __builtin_clzll(f), cnt = h.group_offset[g + 1] - h.group_offset[g];
+      if (hb < kDiagB || cnt > 64) {
+        keep.push_back(g);
+        continue;
+      }
+      ExpPlan::FactFlip ff{};
+      ff.group = g;
+      std::vector<MaskTerm> ts;
+      for (uint32_t t = h.group_offset[g]; t < h.group_offset[g + 1]; ++t) {
+        const MaskTerm& m = h.terms[t];
+        const bool neg = __builtin_popcountll(f & m.yz) & 1;
+        ff.need_im = ff.need_im || neg;
+        ts.push_back(MaskTerm{((m.yz >> 8) & 7) | (neg ? 8u : 0u), ((m.yz >> kDiagB) << 8) | (m.yz & 0xff), m.cb_re,
+                              m.cb_im});
+      }
+      std::stable_sort(ts.begin(), ts.end(), [](const MaskTerm& x, const MaskTerm& y) { return (x.flip & 7) < (y.flip & 7); });
+      ff.ds.n_mx = static_cast<uint32_t>(ts.size());
+      for (uint32_t v = 0, j = 0; v <= 8; ++v) {
+        while (j < ts.size() && (ts[j].flip & 7) < v) ++j;
+        ff.ds.mx_off[v] = j;
+      }
+      ff.term_base = static_cast<uint32_t>(pl.all.size());
+      pl.all.insert(pl.all.end(), ts.begin(), ts.end());
+      pl.fact.push_back(ff);
+    }
+    pl.single = keep;
   }
   for (MultiLaunch& ml : pl.multi) {
     for (uint32_t bit = 5; bit < n && __builtin_popcountll(ml.rset) < kRegBits; ++bit) ml.rset |= uint64_t{1} << bit;
@@ -1051,6 +1166,20 @@ void expectation_t(vqf_statevector* sv, const CompiledHam& h, double* dev_out) {
     const uint32_t hb = 63 - __builtin_clzll(f);
     k_expect_flip<T><<<grid, kThreads, 0, sv->stream>>>(a, n, f, hb, td + t0, cnt, sv->partials, G, g);
     VQF_LAUNCHED();
+  }
+  if (!pl.fact.empty()) {
+    static thread_local uint32_t nbff = 0, nbff_n = 0;
+    if (nbff_n != n) {
+      nbff = resident_grid(k_expect_flip_fact<T>, nb, uint64_t{1} << (n - 1 - kDiagB));
+      nbff_n = n;
+    }
+    for (const ExpPlan::FactFlip& ff : pl.fact) {
+      const uint64_t f = h.group_flip[ff.group];
+      const uint32_t hb = 63 - __builtin_clzll(f);
+      k_expect_flip_fact<T><<<dim3(nbff, sv->batch), kThreads, 0, sv->stream>>>(
+          a, n, f, hb, td + ff.term_base, ff.ds, ff.need_im, sv->partials, G, ff.group, nb);
+      VQF_LAUNCHED();
+    }
   }
   if (!pl.multi.empty()) {
     static thread_local uint32_t nbm = 0, nbm_n = 0;
