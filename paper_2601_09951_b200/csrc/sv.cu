@@ -679,11 +679,23 @@ __device__ __forceinline__ double flip_sign(double x, uint32_t bit) {
   return __hiloint2double(__double2hiint(x) ^ static_cast<int>(bit << 31), __double2loint(x));
 }
 
+__device__ __forceinline__ float flip_sign(float x, uint32_t bit) {
+  return __int_as_float(__float_as_int(x) ^ static_cast<int>(bit << 31));
+}
+
+// conj(a) b in the amplitude precision (the multi-group pass keeps fp32
+// states' pair products and Walsh sums in fp32: 8 terms, ~1e-7 relative)
+__device__ __forceinline__ void conj_mul_native(double2 a, double2 b, double& re, double& im) { conj_mul(a, b, re, im); }
+__device__ __forceinline__ void conj_mul_native(float2 a, float2 b, float& re, float& im) {
+  re = __fmaf_rn(a.x, b.x, a.y * b.y);
+  im = __fmaf_rn(a.x, b.y, -(a.y * b.x));
+}
+
 // W_p = sum_k (-1)^popc(k & p) v_k over NP pairs; p = 0 (no Z/Y on the
 // register bits, e.g. every TFIM term) is a plain sum
-template <int NP>
-__device__ __forceinline__ double walsh(const double (&v)[NP], uint32_t p) {
-  double w = 0.0;
+template <int NP, typename VT>
+__device__ __forceinline__ double walsh(const VT (&v)[NP], uint32_t p) {
+  VT w = VT(0);
   if (p == 0) {
 #pragma unroll
     for (int k = 0; k < NP; ++k) w += v[k];
@@ -691,14 +703,15 @@ __device__ __forceinline__ double walsh(const double (&v)[NP], uint32_t p) {
 #pragma unroll
     for (int k = 0; k < NP; ++k) w += flip_sign(v[k], __popc(k & p) & 1u);
   }
-  return w;
+  return static_cast<double>(w);
 }
 
 // The terms of one group from its 8 pair products v_k: each term adds
 // cb s_base (W + sigma conj W) (k_expect_flip's pair formula summed over k).
 // `neg` flips s_base for the lanes of a lane-pair group that hold the side-1
 // amplitudes (see multi_group_lane).
-__device__ __forceinline__ void multi_terms(const double (&vr)[kRegAmps / 2], const double (&vi)[kRegAmps / 2],
+template <typename VT>
+__device__ __forceinline__ void multi_terms(const VT (&vr)[kRegAmps / 2], const VT (&vi)[kRegAmps / 2],
                                             bool need_im, uint64_t base, bool side, const MaskTerm* st,
                                             const double* sig, uint32_t t0, uint32_t t1, double& acc_re,
                                             double& acc_im) {
@@ -728,7 +741,8 @@ __device__ __forceinline__ void multi_group(const A (&x)[kRegAmps], uint32_t fl,
                                             const MaskTerm* st, const double* sig, uint32_t t0, uint32_t t1,
                                             double& acc_re, double& acc_im) {
   constexpr int top = 31 - __builtin_clz((unsigned)FR);
-  double vr[kRegAmps / 2], vi[kRegAmps / 2];
+  using VT = decltype(A{}.x);
+  VT vr[kRegAmps / 2], vi[kRegAmps / 2];
   int k = 0;
 #pragma unroll
   for (int r = 0; r < kRegAmps; ++r) {
@@ -738,7 +752,7 @@ __device__ __forceinline__ void multi_group(const A (&x)[kRegAmps], uint32_t fl,
       y.x = __shfl_xor_sync(0xffffffffu, y.x, fl);
       y.y = __shfl_xor_sync(0xffffffffu, y.y, fl);
     }
-    conj_mul(x[r], y, vr[k], vi[k]);
+    conj_mul_native(x[r], y, vr[k], vi[k]);
     ++k;
   }
   multi_terms(vr, vi, need_im, base, false, st, sig, t0, t1, acc_re, acc_im);
@@ -754,15 +768,16 @@ template <typename A>
 __device__ __forceinline__ void multi_group_lane(const A (&x)[kRegAmps], uint32_t fl, bool side, bool need_im,
                                                  uint64_t base, const MaskTerm* st, const double* sig, uint32_t t0,
                                                  uint32_t t1, double& acc_re, double& acc_im) {
-  double vr[kRegAmps / 2], vi[kRegAmps / 2];
+  using VT = decltype(A{}.x);
+  VT vr[kRegAmps / 2], vi[kRegAmps / 2];
 #pragma unroll
   for (int k = 0; k < kRegAmps / 2; ++k) {
     const A own = side ? x[k + kRegAmps / 2] : x[k];
     A y = side ? x[k] : x[k + kRegAmps / 2];
     y.x = __shfl_xor_sync(0xffffffffu, y.x, fl);
     y.y = __shfl_xor_sync(0xffffffffu, y.y, fl);
-    double ur, u;
-    conj_mul(own, y, ur, u);
+    VT ur, u;
+    conj_mul_native(own, y, ur, u);
     vr[k] = ur;
     vi[k] = flip_sign(u, side ? 1u : 0u);
   }
