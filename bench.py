@@ -197,11 +197,44 @@ def gate_roofline(V, torch, device, n, steps, warmup):
     for w, t in zip(wires, ms):
         per_wire.setdefault(w, []).append(t)
     avg_ms = statistics.mean(ms)
+
+    # informational (BASELINE configs 3-4, same state): one fused HEA layer
+    # through apply_circuit and TFIM / Z-sum expectations, CUDA events on the
+    # state's stream, median of 3 after one warm-up
+    def timed(fn, reps=3):
+        fn()
+        out = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize(device)
+            out.append(a.elapsed_time(b))
+        return statistics.median(out)
+
+    layer = [V.Gate.ry(0.1 * (q + 1), q) for q in range(n)] + [V.Gate.cnot(q, q + 1) for q in range(n - 1)]
+    tfim, zsum = V.build_tfim(n, 1.0, 1.0), V.build_z_sum(n)
+    with torch.cuda.stream(stream):
+        t_layer = timed(lambda: V.apply_circuit(psi, layer))
+        t_tfim = timed(lambda: V.expectation(psi, tfim))
+        t_zsum = timed(lambda: V.expectation(psi, zsum))
+    plan_layer, plan_tfim = V.circuit_plan(n, layer), V.expectation_plan(tfim)
+    extra = {
+        "workload": f"n={n} fp64 state (2^{n} x 16 B); informational, not the headline",
+        "hea_layer_fused_ms": t_layer, "hea_layer_gates": len(layer), "hea_layer_passes": plan_layer["passes"],
+        "hea_layer_pass_GBps": plan_layer["passes"] * 2 * S / (t_layer * 1e-3) / 1e9,
+        "tfim_expectation_ms": t_tfim, "tfim_flip_groups": plan_tfim["flip_groups"],
+        "tfim_state_passes": plan_tfim["state_passes"],
+        "tfim_pass_GBps": plan_tfim["state_passes"] * S / (t_tfim * 1e-3) / 1e9,
+        "zsum_expectation_ms": t_zsum, "zsum_GBps": S / (t_zsum * 1e-3) / 1e9,
+    }
     del psi
     return {"n_qubits": n, "state_bytes": S, "alg_bytes_per_launch": 2 * S, "avg_ms": avg_ms,
             "gbps": 2 * S / (avg_ms * 1e-3) / 1e9, "launches": launches,
             "worst_wire_gbps": min(2 * S / (statistics.mean(v) * 1e-3) / 1e9 for v in per_wire.values()),
-            "best_wire_gbps": max(2 * S / (statistics.mean(v) * 1e-3) / 1e9 for v in per_wire.values())}
+            "best_wire_gbps": max(2 * S / (statistics.mean(v) * 1e-3) / 1e9 for v in per_wire.values()),
+            "extra": extra}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -307,6 +340,7 @@ def run_ours(args, rank, world, local_rank):
             "wire_range_gbps": [gate["worst_wire_gbps"], gate["best_wire_gbps"]],
         }
         line["config"]["gate_roofline_workload"] = f"RY on an n={gate['n_qubits']} fp64 state (2^{gate['n_qubits']} x 16 B)"
+        line["state_vector_kernels"] = gate["extra"]
     line["pes_kernel"] = {"bound": "latency", "note": "100 bonds x 256 B states live in registers/shared memory; "
                           "one CTA per bond, 200 dependent Adam iterations", "device_ms": pes_s * 1e3}
     if world == 1 and not args.no_cpu_baseline:
