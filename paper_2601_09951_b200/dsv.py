@@ -77,6 +77,10 @@ class GpuBackend:
     def apply(self, psi, kind: int, angle: float, wires: Sequence[int]) -> None:
         self.V.apply_gate(psi, self.V.Gate(kind, angle, tuple(wires)))
 
+    def apply_circuit(self, psi, gates) -> None:
+        """A run of local gates as fused tile passes (vqf_apply_circuit)."""
+        self.V.apply_circuit(psi, [self.V.Gate(k, a, tuple(w)) for k, a, w in gates])
+
     def expectation_complex(self, psi, nl: int, terms) -> complex:
         if not terms:
             return 0j
@@ -221,6 +225,33 @@ class DistributedStateVector:
             self.backend.apply(s, kind, angle, local)
         for w, t in reversed(list(zip(glob, partners))):
             self.swap(w, t)
+
+    def apply_circuit(self, gates: Sequence[Tuple[int, float, Sequence[int]]]) -> None:
+        """apply_circuit (statevector.hpp:205-207) on the sharded state: maximal
+        runs of gates on local wires go to the backend as one fused circuit
+        per shard (tile passes); a gate touching a global wire is swapped in,
+        applied and swapped back (apply_gate)."""
+        fused = getattr(self.backend, "apply_circuit", None)
+        run: List[Tuple[int, float, List[int]]] = []
+
+        def flush():
+            if not run:
+                return
+            for sh in self.shards.values():
+                if fused is not None:
+                    fused(sh, run)
+                else:
+                    for k, a, w in run:
+                        self.backend.apply(sh, k, a, w)
+            run.clear()
+
+        for kind, angle, wires in gates:
+            if all(w >= self.g for w in wires):
+                run.append((kind, angle, [w - self.g for w in wires]))
+            else:
+                flush()
+                self.apply_gate(kind, angle, wires)
+        flush()
 
     # ------------------------------------------------------- expectation
     def _partition(self, ts, f):

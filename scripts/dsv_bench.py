@@ -1,0 +1,66 @@
+"""BASELINE config 5 machinery on one B200: an n-qubit state split over
+`world` virtual shards (paper_2601_09951_b200/dsv.py, LocalComm: shards in
+this process, global-qubit swaps as device copies) vs the single-state
+engine, for one hardware-efficient layer (apply_circuit: fused local runs +
+swaps for the global wires) and a TFIM expectation.  The exchange here is an
+HBM copy, not NVLink; the point is the sharded path's structure and overhead.
+
+  python scripts/dsv_bench.py [n] [world]
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2601_09951_b200 import vqeforge as V  # noqa: E402
+from paper_2601_09951_b200.dsv import DistributedStateVector, GpuBackend, LocalComm  # noqa: E402
+
+
+def wall(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    return sorted(ts)[len(ts) // 2]
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+    world = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    V.init(0)
+    layer = [(1, 0.1 * (q + 1), [q]) for q in range(n)] + [(2, 0.0, [q, q + 1]) for q in range(n - 1)]
+    tfim = V.build_tfim(n, 1.0, 1.0)
+    terms = [(t.coefficient, t.axes) for t in tfim.terms]
+    d = DistributedStateVector(n, world, GpuBackend(0), LocalComm(world))
+    s0 = d.swaps_done
+    t_layer_d = wall(lambda: d.apply_circuit(layer))
+    swaps_layer = (d.swaps_done - s0) // 4
+    s0 = d.swaps_done
+    t_exp_d = wall(lambda: d.expectation(terms))
+    swaps_exp = (d.swaps_done - s0) // 4
+    e_d = d.expectation(terms)
+    del d
+    torch.cuda.empty_cache()
+    single = V.StateVector(n)
+    gates = [V.Gate(k, a, tuple(w)) for k, a, w in layer]
+    t_layer_s = wall(lambda: V.apply_circuit(single, gates))
+    t_exp_s = wall(lambda: V.expectation(single, tfim))
+    print(json.dumps({"n": n, "world": world, "shard_qubits": n - (world.bit_length() - 1),
+                      "hea_layer_s": {"sharded": t_layer_d, "single": t_layer_s, "swaps": swaps_layer},
+                      "tfim_expectation_s": {"sharded": t_exp_d, "single": t_exp_s, "swaps": swaps_exp},
+                      "note": "virtual ranks on one GPU; swaps are device copies; wall clock, median of 3"}))
+
+
+if __name__ == "__main__":
+    main()

@@ -104,3 +104,26 @@ def test_dsv_gloo_world2():
         assert err < 1e-12
         assert abs(e_got - e_want) < 1e-10
         assert swaps > 0
+
+
+@pytest.mark.parametrize("world,n", [(2, 7), (8, 9)])
+def test_dsv_apply_circuit_runs(world, n):
+    # apply_circuit: local runs go through the backend as one circuit (here
+    # the CPU backend has no fused path: per-gate fallback), global-wire
+    # gates through swaps; same amplitudes as the oracle
+    from dsv_cpu_backend import CpuOracleBackend
+    from paper_2601_09951_b200.dsv import DistributedStateVector, LocalComm
+
+    orc = load_orc()
+    pr = random.Random(300 + n)
+    psi = random_state(np.random.default_rng(n), n)
+    d = DistributedStateVector(n, world, CpuOracleBackend(orc), LocalComm(world))
+    d.set_full(psi)
+    gates = [(1, 0.1 * (q + 1), [q]) for q in range(n)] + [(2, 0.0, [q, q + 1]) for q in range(n - 1)]
+    gates += circuit(pr, n, 20)
+    d.apply_circuit(gates)
+    want = orc.apply_gates(n, psi, gates)
+    nl = n - (world.bit_length() - 1)
+    for r, a in d.local_amplitudes().items():
+        assert np.max(np.abs(a - want[r << nl:(r + 1) << nl])) < 1e-12
+    assert d.swaps_done > 0

@@ -52,3 +52,27 @@ def test_dsv_virtual_ranks_on_gpu(gpu, orc, n, world):
     if n <= 12:
         gs4 = [g for g in gs if g[0] != 4]  # the reference has no SingleExcitation
         assert gs4
+
+
+@pytest.mark.parametrize("n,world", [(14, 2), (20, 8)])
+def test_dsv_fused_circuit_on_gpu(gpu, n, world):
+    # DistributedStateVector.apply_circuit: local runs as fused tile passes on
+    # every shard, global-wire gates through swaps; against the single-state
+    # engine on a hardware-efficient layer plus random gates
+    from paper_2601_09951_b200.dsv import DistributedStateVector, GpuBackend, LocalComm
+
+    V = gpu
+    pr = random.Random(100 + n)
+    psi0 = random_state(np.random.default_rng(n + 3), n)
+    gs = [(1, 0.1 * (q + 1), [q]) for q in range(n)] + [(2, 0.0, [q, q + 1]) for q in range(n - 1)]
+    gs += gates_for(pr, n, 40)
+    d = DistributedStateVector(n, world, GpuBackend(0), LocalComm(world))
+    d.set_full(psi0)
+    d.apply_circuit(gs)
+    single = V.StateVector(n)
+    single.amplitudes = psi0
+    V.apply_circuit(single, [V.Gate(k, a, tuple(w)) for k, a, w in gs])
+    want = single.amplitudes
+    nl = n - (world.bit_length() - 1)
+    for r, amps in d.local_amplitudes().items():
+        assert np.max(np.abs(amps - want[r << nl:(r + 1) << nl])) < 1e-12
