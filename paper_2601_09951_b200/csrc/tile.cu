@@ -1,21 +1,25 @@
 // Gate fusion through shared-memory tiles.
 //
 // A pass works on "gathered tiles": 2^B contiguous low-index amplitudes
-// (coalesced HBM transfers) times 2^k chosen high index bits h_0..h_{k-1}
-// (B + k local bits = 64 KB of shared memory).  The CTA loads a tile, applies
-// every gate of the pass whose wires map into its local bits — gates become
-// shared-memory passes between __syncthreads — and writes it back: one HBM
-// read + write of the state per pass instead of per gate.
+// (512 B runs) times 2^k chosen high index bits h_0..h_{k-1} (B + k = 11
+// local bits for fp64, 32 KB).  Runs arrive by TMA tensor loads with the
+// 128 B swizzle; three consumer groups per CTA each own a two-stage ring and
+// a named barrier.  Every gate of the pass whose wires map into the local
+// bits is merged into fused ops of <= 3 bits (4 with a DoubleExcitation);
+// each op is one real 2^m x 2^m matrix composed per CTA and applied to the
+// thread's amplitudes in registers (fp64 3-bit ops on the FP64 tensor cores,
+// mma.sync m8n8k4).  X / CNOT-only passes are an affine map of the local
+// index applied in the write-back.  One HBM read + write of the state per
+// pass instead of per gate.
 //
 // The host scheduler walks the circuit's dependency DAG (gates sharing a wire
-// keep their order; gates on disjoint wires commute) and greedily packs ready
-// gates into a pass while the union of their high bits fits in k.  For the
-// hardware-efficient ansatz every RY on a low wire rides along in every pass,
-// and the CNOT chain advances k - 1 wires per pass.
+// keep their order; gates on disjoint wires commute) and, among ready gates
+// that fit, takes the one adding the fewest new high bits (then sharing the
+// most): for the hardware-efficient ansatz the CNOT chain advances five
+// wires per pass.
 //
-// Per-gate arithmetic is exactly that of the single-gate kernels (sv.cu);
-// commuting gates may be applied in a different order, so amplitudes agree
-// with the unfused path to rounding (~1e-16).
+// Composed matrices (and FMA / MMA accumulation) change rounding only:
+// amplitudes agree with the per-gate kernels to ~1e-16 (tests/).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
