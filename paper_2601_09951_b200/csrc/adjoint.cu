@@ -10,9 +10,12 @@
 //   backward  for k = L..1:  psi <- U_k^dag psi;
 //             if U_k has parameter j:  g_j = 2 Re <lambda| dU_k/dtheta |psi>;
 //             lambda <- U_k^dag lambda
-// Each parameterised backward step is ONE kernel (k_adj_givens): it reads and
+// A parameterised backward step is one kernel (k_adj_givens): it reads and
 // writes both vectors once (4S) and reduces the derivative inner product
-// deterministically into per-block partials.
+// deterministically into per-block partials.  Up to four consecutive RYs on
+// distinct wires share one such pass (k_adj_ry_multi), and runs of X / CNOT
+// gates are un-applied to each vector by the fused tile path (permutation
+// passes, tile.cu).
 #include <algorithm>
 #include <cstring>
 
