@@ -99,6 +99,15 @@ __global__ void __launch_bounds__(kThreads) k_apply_ham(const typename V2<T>::ty
   __syncthreads();
   double2 acc = make_double2(0.0, 0.0);
   __shared__ double2 ohi[kMaxGroups];  // per flip group: its tile-constant operator part
+  __shared__ uint64_t sflip[kMaxGroups];
+  __shared__ uint32_t sgoff[kMaxGroups + 1], sghi[kMaxGroups];
+  for (uint32_t g = threadIdx.x; g <= h.n_groups; g += kThreads) {
+    sgoff[g] = h.group_off[g];
+    if (g < h.n_groups) {
+      sflip[g] = h.flips[g];
+      sghi[g] = h.group_hi[g];
+    }
+  }
   for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     double hre = 0.0, him = 0.0;
     for (uint32_t t = 0; t < h.n_hi; ++t) {
@@ -146,30 +155,16 @@ __global__ void __launch_bounds__(kThreads) k_apply_ham(const typename V2<T>::ty
         }
         l[u] = make_double2(dre * (double)x[u].x - dim * (double)x[u].y, dre * (double)x[u].y + dim * (double)x[u].x);
       }
-      // software-pipelined partner loads: group g + 1's partners are in
-      // flight while group g's terms are applied
-      A y[kU], yn[kU];
-      if (h.n_groups > 0) {
-        const uint64_t f0 = h.flips[0];
+      for (uint32_t g = 0; g < h.n_groups; ++g) {
+        const uint64_t f = sflip[g];
+        A y[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const uint32_t lo = lo0 + u * kThreads;
-          if (lo < tile_amps) yn[u] = psi[(base | lo) ^ f0];
-        }
-      }
-      for (uint32_t g = 0; g < h.n_groups; ++g) {
-#pragma unroll
-        for (int u = 0; u < kU; ++u) y[u] = yn[u];
-        if (g + 1 < h.n_groups) {
-          const uint64_t fn = h.flips[g + 1];
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const uint32_t lo = lo0 + u * kThreads;
-            if (lo < tile_amps) yn[u] = psi[(base | lo) ^ fn];
-          }
+          if (lo < tile_amps) y[u] = psi[(base | lo) ^ f];
         }
         const double2 oc = ohi[g];
-        const uint32_t t_lo = h.group_off[g] + h.group_hi[g], t_end = h.group_off[g + 1];
+        const uint32_t t_lo = sgoff[g] + sghi[g], t_end = sgoff[g + 1];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const uint64_t i = base | (lo0 + u * kThreads);
@@ -179,8 +174,9 @@ __global__ void __launch_bounds__(kThreads) k_apply_ham(const typename V2<T>::ty
             ore += sg * h.terms[t].cb_re;
             oim += sg * h.terms[t].cb_im;
           }
-          l[u].x += ore * (double)y[u].x - oim * (double)y[u].y;
-          l[u].y += ore * (double)y[u].y + oim * (double)y[u].x;
+          // l += O y (fused multiply-adds)
+          l[u].x = __fma_rn(ore, (double)y[u].x, __fma_rn(-oim, (double)y[u].y, l[u].x));
+          l[u].y = __fma_rn(ore, (double)y[u].y, __fma_rn(oim, (double)y[u].x, l[u].y));
         }
       }
 #pragma unroll
