@@ -240,20 +240,21 @@ __global__ void __launch_bounds__(kThreads) k_adj_givens(typename V2<T>::type* _
     for (int u = 0; u < kU; ++u) {
       if (k0 + u * stride >= total) break;
       // psi' = G^dag psi: a' = c a + s b, b' = -s a + c b
-      A pa, pb;
-      pa.x = ct * a[u].x + st * b[u].x;
-      pa.y = ct * a[u].y + st * b[u].y;
-      pb.x = ct * b[u].x - st * a[u].x;
-      pb.y = ct * b[u].y - st * a[u].y;
+      A pa, pb;  // (fused multiply-adds throughout)
+      pa.x = fma(ct, a[u].x, st * b[u].x);
+      pa.y = fma(ct, a[u].y, st * b[u].y);
+      pb.x = fma(ct, b[u].x, -(st * a[u].x));
+      pb.y = fma(ct, b[u].y, -(st * a[u].y));
       // mu = dG psi' = 1/2 (-s a' - c b', c a' - s b')
-      const double mar = 0.5 * (-s * (double)pa.x - c * (double)pb.x), mai = 0.5 * (-s * (double)pa.y - c * (double)pb.y);
-      const double mbr = 0.5 * (c * (double)pa.x - s * (double)pb.x), mbi = 0.5 * (c * (double)pa.y - s * (double)pb.y);
-      acc += (double)la[u].x * mar + (double)la[u].y * mai + (double)lb[u].x * mbr + (double)lb[u].y * mbi;
+      const double mar = fma(-s, (double)pa.x, -(c * (double)pb.x)), mai = fma(-s, (double)pa.y, -(c * (double)pb.y));
+      const double mbr = fma(c, (double)pa.x, -(s * (double)pb.x)), mbi = fma(c, (double)pa.y, -(s * (double)pb.y));
+      acc = fma(0.5 * (double)la[u].x, mar, fma(0.5 * (double)la[u].y, mai,
+            fma(0.5 * (double)lb[u].x, mbr, fma(0.5 * (double)lb[u].y, mbi, acc))));
       A qa, qb;
-      qa.x = ct * la[u].x + st * lb[u].x;
-      qa.y = ct * la[u].y + st * lb[u].y;
-      qb.x = ct * lb[u].x - st * la[u].x;
-      qb.y = ct * lb[u].y - st * la[u].y;
+      qa.x = fma(ct, la[u].x, st * lb[u].x);
+      qa.y = fma(ct, la[u].y, st * lb[u].y);
+      qb.x = fma(ct, lb[u].x, -(st * la[u].x));
+      qb.y = fma(ct, lb[u].y, -(st * la[u].y));
       psi[r[u] | pat_a] = pa;
       psi[r[u] | pat_b] = pb;
       lam[r[u] | pat_a] = qa;
@@ -333,19 +334,21 @@ __global__ void __launch_bounds__(kThreads) k_adj_ry_multi(typename V2<T>::type*
         A& y = a[r | (1 << j)];
         A& lx = l[r];
         A& ly = l[r | (1 << j)];
-        A pa, pb;  // psi' = G^dag psi
-        pa.x = ct * x.x + st * y.x;
-        pa.y = ct * x.y + st * y.y;
-        pb.x = ct * y.x - st * x.x;
-        pb.y = ct * y.y - st * x.y;
-        const double mar = 0.5 * (-sn * (double)pa.x - c * (double)pb.x), mai = 0.5 * (-sn * (double)pa.y - c * (double)pb.y);
-        const double mbr = 0.5 * (c * (double)pa.x - sn * (double)pb.x), mbi = 0.5 * (c * (double)pa.y - sn * (double)pb.y);
-        acc[j] += (double)lx.x * mar + (double)lx.y * mai + (double)ly.x * mbr + (double)ly.y * mbi;
+        A pa, pb;  // psi' = G^dag psi (fused multiply-adds throughout)
+        pa.x = fma(ct, x.x, st * y.x);
+        pa.y = fma(ct, x.y, st * y.y);
+        pb.x = fma(ct, y.x, -(st * x.x));
+        pb.y = fma(ct, y.y, -(st * x.y));
+        // mu = dG psi' = 1/2 (-s a' - c b', c a' - s b'); g += Re<lambda|mu>
+        const double mar = fma(-sn, (double)pa.x, -(c * (double)pb.x)), mai = fma(-sn, (double)pa.y, -(c * (double)pb.y));
+        const double mbr = fma(c, (double)pa.x, -(sn * (double)pb.x)), mbi = fma(c, (double)pa.y, -(sn * (double)pb.y));
+        acc[j] = fma(0.5 * (double)lx.x, mar, fma(0.5 * (double)lx.y, mai,
+                 fma(0.5 * (double)ly.x, mbr, fma(0.5 * (double)ly.y, mbi, acc[j]))));
         A qa, qb;  // lambda' = G^dag lambda
-        qa.x = ct * lx.x + st * ly.x;
-        qa.y = ct * lx.y + st * ly.y;
-        qb.x = ct * ly.x - st * lx.x;
-        qb.y = ct * ly.y - st * lx.y;
+        qa.x = fma(ct, lx.x, st * ly.x);
+        qa.y = fma(ct, lx.y, st * ly.y);
+        qb.x = fma(ct, ly.x, -(st * lx.x));
+        qb.y = fma(ct, ly.y, -(st * lx.y));
         x = pa;
         y = pb;
         lx = qa;
