@@ -165,34 +165,44 @@ __device__ __forceinline__ uint64_t run_start(const TileParams& p, uint64_t tile
 // Every gate here is a real orthogonal map on its pairs, so a fused op is
 // one real 2^m x 2^m matrix U (row-major, in shared memory) composed once
 // per CTA from its gates and the CTA's batch entry angles: start from the
-// identity and apply each gate to the rows of every column.
+// identity and apply each gate to the rows of every column.  The angles are
+// staged in shared memory first (one parallel round of global loads instead
+// of a dependent L2 round trip per gate) and each thread composes one
+// (op, column) pair, so the serial chain is one op's gates: batched states
+// launch a CTA set per entry and pay this once per (CTA, entry).
 template <typename T>
 __device__ void compose_fops(const TileParams& p, T* U) {
-  for (uint32_t o = 0; o < p.n_fops; ++o) {
+  __shared__ double2 sc[kMaxOps];
+  uint32_t n_subs = 0;
+  for (uint32_t o = 0; o < p.n_fops; ++o) n_subs = max(n_subs, p.fops[o].sub0 + p.fops[o].n_sub);
+  for (uint32_t q = threadIdx.x; q < n_subs; q += blockDim.x) {
+    const TileSub& g = p.subs[q];
+    double2 v = make_double2(g.c, g.s);
+    if (g.param >= 0) v = *reinterpret_cast<const double2*>(p.cs + 2 * ((size_t)g.param * p.batch + blockIdx.y));
+    sc[q] = v;
+  }
+  __syncthreads();
+  for (uint32_t w = threadIdx.x;; w += blockDim.x) {
+    uint32_t o = 0, col = w;
+    while (o < p.n_fops && col >= (1u << p.fops[o].m)) col -= 1u << p.fops[o].m, ++o;
+    if (o >= p.n_fops) break;
     const TileFop& f = p.fops[o];
     const uint32_t d = 1u << f.m;
     T* u = U + f.uoff;
-    for (uint32_t col = threadIdx.x; col < d; col += blockDim.x) {
-      for (uint32_t r = 0; r < d; ++r) u[r * d + col] = r == col ? T(1) : T(0);
-      for (uint32_t q = 0; q < f.n_sub; ++q) {
-        const TileSub& g = p.subs[f.sub0 + q];
-        double c = g.c, sn = g.s;
-        if (g.param >= 0) {
-          const double* cs = p.cs + 2 * ((size_t)g.param * p.batch + blockIdx.y);
-          c = cs[0];
-          sn = cs[1];
-        }
-        const uint32_t A = (g.code >> 4) & 15u, B = g.code & 15u, S = A | B;
-        for (uint32_t r = 0; r < d; ++r) {
-          if (r & S) continue;
-          const T x = u[(r | A) * d + col], y = u[(r | B) * d + col];
-          if (g.code >> 8) {  // a' = c a - s b, b' = s a + c b (statevector.hpp:160-163, :195-196)
-            u[(r | A) * d + col] = static_cast<T>(c) * x - static_cast<T>(sn) * y;
-            u[(r | B) * d + col] = static_cast<T>(sn) * x + static_cast<T>(c) * y;
-          } else {
-            u[(r | A) * d + col] = y;
-            u[(r | B) * d + col] = x;
-          }
+    for (uint32_t r = 0; r < d; ++r) u[r * d + col] = r == col ? T(1) : T(0);
+    for (uint32_t q = 0; q < f.n_sub; ++q) {
+      const TileSub& g = p.subs[f.sub0 + q];
+      const double c = sc[f.sub0 + q].x, sn = sc[f.sub0 + q].y;
+      const uint32_t A = (g.code >> 4) & 15u, B = g.code & 15u, S = A | B;
+      for (uint32_t r = 0; r < d; ++r) {
+        if (r & S) continue;
+        const T x = u[(r | A) * d + col], y = u[(r | B) * d + col];
+        if (g.code >> 8) {  // a' = c a - s b, b' = s a + c b (statevector.hpp:160-163, :195-196)
+          u[(r | A) * d + col] = static_cast<T>(c) * x - static_cast<T>(sn) * y;
+          u[(r | B) * d + col] = static_cast<T>(sn) * x + static_cast<T>(c) * y;
+        } else {
+          u[(r | A) * d + col] = y;
+          u[(r | B) * d + col] = x;
         }
       }
     }
@@ -586,6 +596,13 @@ std::vector<Pass> schedule(uint32_t n, uint32_t B, uint32_t kmax, const std::vec
         break;
       }
     }
+    // a pass that needed fewer high bits still moves full tiles: pad with
+    // spectator bits (lowest free ones, so neighbouring runs are adjacent in
+    // HBM) -- a 2^8-amplitude tile spends its time in barriers and TMA
+    // issue, not on its bytes
+    if (pass.hbits.empty() || pass.hbits[0] != 0xffffffffu)
+      for (uint32_t b = B; b < n && pass.hbits.size() < kmax; ++b)
+        if (std::find(pass.hbits.begin(), pass.hbits.end(), b) == pass.hbits.end()) pass.hbits.push_back(b);
     std::sort(pass.hbits.begin(), pass.hbits.end());
     passes.push_back(std::move(pass));
   }
@@ -825,7 +842,12 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
     for (uint32_t o = 0; o < p.n_fops; ++o)
       if (p.fops[o].m == 3) p.fops[o].ipos = choose_item_bits(p.fops[o], LB);
   const uint64_t n_tiles = uint64_t{1} << (n - LB);
-  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n_tiles, kTileBlocks));
+  // persistent over one entry's tiles; a batched state launches a CTA set
+  // per entry, so give each group >= 16 tiles there to amortise the CTA
+  // prologue (matrix composition, ring fill) over enough traffic
+  uint64_t gx = std::min<uint64_t>(n_tiles, kTileBlocks);
+  if (sv->batch > 1) gx = std::max<uint64_t>(1, std::min<uint64_t>(gx, n_tiles / (kGroups * 16)));
+  const unsigned grid = static_cast<unsigned>(gx);
   const uint32_t run_bytes = static_cast<uint32_t>(sizeof(typename V2<T>::type) << B);
   // the encoded map is cached per (state allocation, run size)
   static thread_local std::vector<std::pair<std::pair<const void*, uint64_t>, CUtensorMap>> maps;
@@ -873,8 +895,21 @@ void plan_tile_counts(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>
       ++launches;
       continue;
     }
-    for (size_t first = 0, next = 0; first < p.gates.size(); first = next, ++launches)
-      fops += build_params(n_qubits, 1, B, gates, p, nullptr, dtype == VQF_F64 ? 3 : 4, first, &next).n_fops;
+    for (size_t first = 0, next = 0; first < p.gates.size(); first = next, ++launches) {
+      const TileParams tp = build_params(n_qubits, 1, B, gates, p, nullptr, dtype == VQF_F64 ? 3 : 4, first, &next);
+      fops += tp.n_fops;
+      if (std::getenv("VQF_TILE_DEBUG")) {
+        std::fprintf(stderr, "launch %u: k=%u hb=", launches, tp.k);
+        for (uint32_t j = 0; j < tp.k; ++j) std::fprintf(stderr, "%u,", tp.hb[j]);
+        std::fprintf(stderr, " perm=%u fops=%u:", tp.perm_only, tp.n_fops);
+        for (uint32_t o = 0; o < tp.n_fops; ++o) {
+          const uint32_t ip = tp.fops[o].m == 3 && dtype == VQF_F64 ? choose_item_bits(tp.fops[o], B + tp.k) : 0;
+          std::fprintf(stderr, " m%u/%u[%x]%s", tp.fops[o].m, tp.fops[o].n_sub, tp.fops[o].pos,
+                       ip == kNoMma ? "F" : "");
+        }
+        std::fprintf(stderr, "\n");
+      }
+    }
   }
   *passes = launches;
   *fused_ops = fops;

@@ -513,10 +513,18 @@ struct ShiftEvaluator {
       return t;
     };
     if (batched) {
-      eng->prepare([&](uint32_t j, uint32_t e) { return e < (uint32_t)c_count ? angle_of(j, e) : theta[j]; });
-      std::vector<double> tot(2 * (size_t)NC);
-      sv_expectation(eng->sv, h, tot.data());
-      std::copy(tot.begin(), tot.begin() + 2 * c_count, E.begin());
+      // entries are contiguous: run only the first c_count of them (the
+      // final evaluation after the last Adam step needs one circuit)
+      const uint32_t full = eng->sv->batch;
+      eng->sv->batch = static_cast<uint32_t>(c_count);
+      try {
+        eng->prepare([&](uint32_t j, uint32_t e) { return angle_of(j, e); });
+        sv_expectation(eng->sv, h, E.data());
+      } catch (...) {
+        eng->sv->batch = full;
+        throw;
+      }
+      eng->sv->batch = full;
       return;
     }
     for (int c = 0; c < c_count; ++c) {
@@ -655,7 +663,11 @@ void run_vqe_impl(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const
   check_ansatz_register(kind, n);
   if (method != VQF_GRAD_PARAMETER_SHIFT && method != VQF_GRAD_ADJOINT) throw_invalid("unknown gradient method");
   std::vector<double> init_v(init, init + n_init);
-  if (small_ok(n, P) && method == VQF_GRAD_PARAMETER_SHIFT) {
+  // registers that fit one warp run the whole optimisation in one launch
+  // (k_vqe_warp, parameter-shift gradients); the adjoint method would equal
+  // it to rounding but pays one HBM-engine launch per gate there, so small
+  // registers take this path for either method
+  if (small_ok(n, P)) {
     SmallJob j;
     j.batch = 1;
     j.n_qubits = static_cast<int32_t>(n);

@@ -38,7 +38,7 @@ def main():
         for method in ("shift", "adjoint"):
             # a first run at each width pays one-time costs (state allocations
             # from the pool, kernel attributes); the second run is reported
-            V.run_scaling_study(V.ScalingConfig(qubits=[n], method=method, force=n > 26, iterations=1))
+            V.run_scaling_study(V.ScalingConfig(qubits=[n], method=method, force=n > 26))
             t0 = time.perf_counter()
             rec = V.run_scaling_study(V.ScalingConfig(qubits=[n], method=method, force=n > 26))[0]
             wall = time.perf_counter() - t0
@@ -57,8 +57,7 @@ def main():
         cfg = V.AdamConfig(learning_rate=0.05, max_iterations=5)
         init = [0.1] * (2 * n)
         for method in ("shift", "adjoint"):
-            V.run_vqe(hv, V.AnsatzSpec.hardware_efficient(2), V.AdamConfig(learning_rate=0.05, max_iterations=1), init,
-                      method=method)  # warm-up at this width
+            V.run_vqe(hv, V.AnsatzSpec.hardware_efficient(2), cfg, init, method=method)  # warm-up at this width
             t0 = time.perf_counter()
             r = V.run_vqe(hv, V.AnsatzSpec.hardware_efficient(2), cfg, init, method=method)
             print(json.dumps({"config": "random32-hea2", "engine": f"b200-{method}", "n": n,
