@@ -92,7 +92,6 @@ struct TileParams {
   // the set bits b of L (an affine map over GF(2) on the local index).
   uint32_t perm_only, perm_c;
   uint32_t perm_col[16];
-  uint32_t dense;  // 1: FMA paths multiply every matrix entry (A/B switch, VQF_TILE_DENSE=1)
   TileFop fops[kMaxOps];
   TileSub subs[kMaxOps];
 };
@@ -172,7 +171,7 @@ __device__ __forceinline__ uint64_t run_start(const TileParams& p, uint64_t tile
 // (op, column) pair, so the serial chain is one op's gates: batched states
 // launch a CTA set per entry and pay this once per (CTA, entry).
 template <typename T>
-__device__ void compose_fops(const TileParams& p, T* U, uint16_t* rowmask) {
+__device__ void compose_fops(const TileParams& p, T* U) {
   __shared__ double2 sc[kMaxOps];
   uint32_t n_subs = 0;
   for (uint32_t o = 0; o < p.n_fops; ++o) n_subs = max(n_subs, p.fops[o].sub0 + p.fops[o].n_sub);
@@ -208,21 +207,6 @@ __device__ void compose_fops(const TileParams& p, T* U, uint16_t* rowmask) {
       }
     }
   }
-  // nonzero columns of every row (bit c of rowmask[uoff / 2 + r]): the FMA
-  // paths skip structural zeros (a CNOT / RY product is sparse); a skipped
-  // fma(0, x, acc) would have returned acc, so results are unchanged
-  __syncthreads();
-  for (uint32_t w = threadIdx.x;; w += blockDim.x) {
-    uint32_t o = 0, r = w;
-    while (o < p.n_fops && r >= (1u << p.fops[o].m)) r -= 1u << p.fops[o].m, ++o;
-    if (o >= p.n_fops) break;
-    const TileFop& f = p.fops[o];
-    const uint32_t d = 1u << f.m;
-    uint32_t mk = 0;
-    for (uint32_t c = 0; c < d; ++c)
-      if (p.dense || U[f.uoff + r * d + c] != T(0)) mk |= 1u << c;
-    rowmask[f.uoff / 2 + r] = static_cast<uint16_t>(mk);
-  }
 }
 
 // One fused op over the whole tile: work item w -> base with zeros at the
@@ -231,7 +215,7 @@ __device__ void compose_fops(const TileParams& p, T* U, uint16_t* rowmask) {
 // disjoint bits, so slot addresses are swz(base) ^ swz(offset).
 template <int M, typename T, int NT>
 __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, const TileFop& f, const T* U,
-                                        const uint16_t* rowmask, uint32_t gt) {
+                                        uint32_t gt) {
   using A = typename V2<T>::type;
   constexpr int D = 1 << M;
   uint32_t pos[M];
@@ -365,23 +349,17 @@ __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, co
           b0.y = u[0] * x1[0].y;
         } else {
           const P2* row = reinterpret_cast<const P2*>(u + r * D);
-          const uint32_t mk = rowmask[f.uoff / 2 + r];
 #pragma unroll
           for (int c = 0; c < D; c += 2) {
-            if (!(mk & (3u << c))) continue;
             const P2 m = row[c / 2];
-            if (mk & (1u << c)) {
-              a0.x = fma(m.x, x0[c].x, a0.x);
-              a0.y = fma(m.x, x0[c].y, a0.y);
-              b0.x = fma(m.x, x1[c].x, b0.x);
-              b0.y = fma(m.x, x1[c].y, b0.y);
-            }
-            if (mk & (2u << c)) {
-              a1.x = fma(m.y, x0[c + 1].x, a1.x);
-              a1.y = fma(m.y, x0[c + 1].y, a1.y);
-              b1.x = fma(m.y, x1[c + 1].x, b1.x);
-              b1.y = fma(m.y, x1[c + 1].y, b1.y);
-            }
+            a0.x = fma(m.x, x0[c].x, a0.x);
+            a0.y = fma(m.x, x0[c].y, a0.y);
+            a1.x = fma(m.y, x0[c + 1].x, a1.x);
+            a1.y = fma(m.y, x0[c + 1].y, a1.y);
+            b0.x = fma(m.x, x1[c].x, b0.x);
+            b0.y = fma(m.x, x1[c].y, b0.y);
+            b1.x = fma(m.y, x1[c + 1].x, b1.x);
+            b1.y = fma(m.y, x1[c + 1].y, b1.y);
           }
         }
         A y0, y1;
@@ -406,19 +384,13 @@ __device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, co
         A y0, y1;
         y0.x = y0.y = y1.x = y1.y = T(0);
         const P2* row = reinterpret_cast<const P2*>(u + r * D);
-        const uint32_t mk = rowmask[f.uoff / 2 + r];
 #pragma unroll
         for (int c = 0; c < D; c += 2) {
-          if (!(mk & (3u << c))) continue;
           const P2 m = row[c / 2];
-          if (mk & (1u << c)) {
-            y0.x = fma(m.x, x[c].x, y0.x);
-            y0.y = fma(m.x, x[c].y, y0.y);
-          }
-          if (mk & (2u << c)) {
-            y1.x = fma(m.y, x[c + 1].x, y1.x);
-            y1.y = fma(m.y, x[c + 1].y, y1.y);
-          }
+          y0.x = fma(m.x, x[c].x, y0.x);
+          y0.y = fma(m.x, x[c].y, y0.y);
+          y1.x = fma(m.y, x[c + 1].x, y1.x);
+          y1.y = fma(m.y, x[c + 1].y, y1.y);
         }
         A y;
         y.x = y0.x + y1.x;
@@ -469,8 +441,7 @@ __global__ void __launch_bounds__(kGroups * NT, 1)
     for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __shared__ uint16_t rowmask[PERM ? 1 : kMatElems / 2];
-  if constexpr (!PERM) compose_fops<T>(p, U, rowmask);
+  if constexpr (!PERM) compose_fops<T>(p, U);
   // permutation-only pass: F as two 64-entry tables (bits 0-5, bits 6-11)
   __shared__ uint16_t ftab[PERM ? 2 : 1][64];
   if constexpr (PERM)
@@ -511,11 +482,11 @@ __global__ void __launch_bounds__(kGroups * NT, 1)
     for (uint32_t o = 0; o < (PERM ? 0u : p.n_fops); ++o) {
       const TileFop f = p.fops[o];
       switch (f.m) {
-        case 1: run_fop<1, T, NT>(t, NL, f, U, rowmask, gt); break;
-        case 2: run_fop<2, T, NT>(t, NL, f, U, rowmask, gt); break;
-        case 3: run_fop<3, T, NT>(t, NL, f, U, rowmask, gt); break;
+        case 1: run_fop<1, T, NT>(t, NL, f, U, gt); break;
+        case 2: run_fop<2, T, NT>(t, NL, f, U, gt); break;
+        case 3: run_fop<3, T, NT>(t, NL, f, U, gt); break;
         default:
-          if constexpr (MAXM >= 4) run_fop<4, T, NT>(t, NL, f, U, rowmask, gt);
+          if constexpr (MAXM >= 4) run_fop<4, T, NT>(t, NL, f, U, gt);
           break;
       }
       group_sync<NT>(group);
@@ -864,8 +835,6 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
   const uint32_t n = sv->n_qubits;
   for (size_t first = 0, next = 0; first < pass.gates.size(); first = next) {
   TileParams p = build_params(n, sv->batch, B, gates, pass, cs_dev, sizeof(T) == 8 ? 3 : 4, first, &next);
-  static const bool dense = std::getenv("VQF_TILE_DENSE") != nullptr;
-  p.dense = dense ? 1u : 0u;
   bool wide = false;
   for (uint32_t o = 0; o < p.n_fops; ++o) wide = wide || p.fops[o].m == 4;
   const uint32_t LB = B + p.k;

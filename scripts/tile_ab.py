@@ -10,7 +10,7 @@ V.init(0)
 s = torch.cuda.Stream()
 for n in [int(a) for a in sys.argv[1:]] or [24, 26, 28]:
     gates = []
-    for layer in range(2):
+    for layer in range(int(os.environ.get("LAYERS", "2"))):
         gates += [V.Gate.ry(0.1 * (q + 1) + layer, q) for q in range(n)] + [V.Gate.cnot(q, q + 1) for q in range(n - 1)]
     a = V.StateVector(n)
     a.set_stream(s.cuda_stream)
@@ -22,7 +22,7 @@ for n in [int(a) for a in sys.argv[1:]] or [24, 26, 28]:
     plan = V.circuit_plan(n, gates)
     S = (1 << n) * 16
     med = statistics.median(ts[2:])
-    print(f"{os.environ.get('VQF_TILE_DENSE') and 'dense ' or 'sparse'} n={n}: {med:.3f} ms (min {min(ts[2:]):.3f}) "
+    print(f"{os.environ.get('TAG', '')} L{os.environ.get('LAYERS', '2')} n={n}: {med:.3f} ms (min {min(ts[2:]):.3f}) "
           f"{plan['passes']} passes, {2 * S * plan['passes'] / (med * 1e-3) / 1e9:.0f} GB/s", flush=True)
     del a
     torch.cuda.empty_cache()
