@@ -553,3 +553,32 @@ def test_adjoint_equals_shift_at_width_20(gpu):
     ga = V.gradient(th, h, hea, method="adjoint")
     gs = V.gradient(th, h, hea, method="shift")
     assert np.max(np.abs(ga - gs)) < 1e-10
+
+
+def test_small_register_adjoint_runs_match_oracle(gpu, orc):
+    """n <= 5 run_vqe with method="adjoint" takes the one-launch register
+    engine; its trajectory still matches the reference's run_vqe."""
+    V = gpu
+    for n in [3, 4, 5]:
+        h = orc.build_tfim(n, 1.0, 0.7)
+        want = orc.run_vqe(h, kind=1, layers=2, lr=0.05, max_iter=5, init=[0.1] * (2 * n))
+        for method in ("adjoint", "shift"):
+            r = V.run_vqe(to_v(V, h), V.AnsatzSpec.hardware_efficient(2), V.AdamConfig(learning_rate=0.05, max_iterations=5),
+                          [0.1] * (2 * n), method=method)
+            assert abs(r.energy - want["energy"]) < E_TOL
+
+
+def test_batched_shift_run_matches_adjoint_at_width_16(gpu):
+    """Parameter shift at n = 16 runs the 2P + 1 circuits as one batch
+    (padded full-height tile passes; the final energy evaluates one entry):
+    same trajectory as the adjoint engine."""
+    V = gpu
+    n = 16
+    h = V.build_tfim(n, 1.0, 1.0)
+    hea = V.AnsatzSpec.hardware_efficient(2)
+    cfg = V.AdamConfig(learning_rate=0.05, max_iterations=3)
+    rs = V.run_vqe(h, hea, cfg, [0.1] * (2 * n), method="shift")
+    ra = V.run_vqe(h, hea, cfg, [0.1] * (2 * n), method="adjoint")
+    assert len(rs.trajectory) == len(ra.trajectory) == 4
+    assert np.max(np.abs(np.array(rs.trajectory) - np.array(ra.trajectory))) < 1e-10
+    assert np.max(np.abs(np.array(rs.theta) - np.array(ra.theta))) < 1e-10
