@@ -509,6 +509,16 @@ __global__ void __launch_bounds__(kGroups * NT, 1)
   }
 }
 
+// dst[e] = src for e < m (one read of the source, m writes): entries of a
+// batch joining the shared prefix of a circuit family.
+template <typename A>
+__global__ void k_broadcast(const A* __restrict__ src, A* __restrict__ dst, uint32_t m, uint64_t dim) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < dim; i += (uint64_t)gridDim.x * blockDim.x) {
+    const A v = src[i];
+    for (uint32_t e = 0; e < m; ++e) dst[e * dim + i] = v;
+  }
+}
+
 struct Pass {
   std::vector<uint32_t> hbits;  // ascending global bits
   std::vector<int> gates;
@@ -831,7 +841,9 @@ uint32_t choose_item_bits(const TileFop& f, uint32_t LB) {
 
 template <typename T>
 void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pass& pass, uint32_t B,
-                 const double* cs_dev) {
+                 const double* cs_dev, uint32_t active = 0) {
+  // active: batch entries [0, active) take the pass (0 = all)
+  if (active == 0) active = sv->batch;
   const uint32_t n = sv->n_qubits;
   for (size_t first = 0, next = 0; first < pass.gates.size(); first = next) {
   TileParams p = build_params(n, sv->batch, B, gates, pass, cs_dev, sizeof(T) == 8 ? 3 : 4, first, &next);
@@ -846,7 +858,7 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
   // per entry, so give each group >= 16 tiles there to amortise the CTA
   // prologue (matrix composition, ring fill) over enough traffic
   uint64_t gx = std::min<uint64_t>(n_tiles, kTileBlocks);
-  if (sv->batch > 1) gx = std::max<uint64_t>(1, std::min<uint64_t>(gx, n_tiles / (kGroups * 16)));
+  if (active > 1) gx = std::max<uint64_t>(1, std::min<uint64_t>(gx, n_tiles / (kGroups * 16)));
   const unsigned grid = static_cast<unsigned>(gx);
   const uint32_t run_bytes = static_cast<uint32_t>(sizeof(typename V2<T>::type) << B);
   // the encoded map is cached per (state allocation, run size)
@@ -865,11 +877,11 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
   const size_t smem = kGroups * kStages * (sizeof(typename V2<T>::type) << LB) + 256 + kMatElems * sizeof(T) + 1024;  // rings + mbarriers + matrices + align
   auto* amps = static_cast<typename V2<T>::type*>(sv->amps);
   if (p.perm_only)
-    k_tile<T, kNT, 1, true><<<dim3(grid, sv->batch), kGroups * kNT, smem, sv->stream>>>(amps, *map, p);
+    k_tile<T, kNT, 1, true><<<dim3(grid, active), kGroups * kNT, smem, sv->stream>>>(amps, *map, p);
   else if (sizeof(T) == 4 || !wide)
-    k_tile<T, kNT, sizeof(T) == 4 ? 4 : 3, false><<<dim3(grid, sv->batch), kGroups * kNT, smem, sv->stream>>>(amps, *map, p);
+    k_tile<T, kNT, sizeof(T) == 4 ? 4 : 3, false><<<dim3(grid, active), kGroups * kNT, smem, sv->stream>>>(amps, *map, p);
   else
-    k_tile<T, kNT / 2, 4, false><<<dim3(grid, sv->batch), kGroups * kNT / 2, smem, sv->stream>>>(amps, *map, p);
+    k_tile<T, kNT / 2, 4, false><<<dim3(grid, active), kGroups * kNT / 2, smem, sv->stream>>>(amps, *map, p);
   VQF_LAUNCHED();
   }
 }
@@ -915,11 +927,8 @@ void plan_tile_counts(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>
   *fused_ops = fops;
 }
 
-int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, const double* cs_dev) {
-  if (gates.empty()) return 0;
-  const uint32_t n = sv->n_qubits;
-  uint32_t B, kmax;
-  tile_shape(n, sv->dtype, B, kmax);
+namespace {
+void ensure_tile_attrs(const vqf_statevector* sv) {
   static thread_local int opted = -1;
   if (opted != sv->device) {
     const int bytes = kGroups * kStages * (16 << VQF_TILE_LB) + 256 + kMatElems * 8 + 1024;
@@ -930,6 +939,15 @@ int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, cons
     VQF_CUDA(cudaFuncSetAttribute(k_tile<float, kNT, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     opted = sv->device;
   }
+}
+}  // namespace
+
+int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, const double* cs_dev) {
+  if (gates.empty()) return 0;
+  const uint32_t n = sv->n_qubits;
+  uint32_t B, kmax;
+  tile_shape(n, sv->dtype, B, kmax);
+  ensure_tile_attrs(sv);
   const std::vector<Pass> passes = schedule(n, B, kmax, gates);
   const bool tiny = (sv->amp_bytes() << B) < 128;  // 2-3 qubits: a run is below one 128 B row
   for (const Pass& pass : passes) {
@@ -954,6 +972,65 @@ int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, cons
     else
       launch_pass<float>(sv, gates, pass, B, cs_dev);
   }
+  VQF_CUDA(cudaGetLastError());
+  return static_cast<int>(passes.size());
+}
+
+std::vector<int> tile_param_first_pass(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>& gates,
+                                       uint32_t n_params) {
+  uint32_t B, kmax;
+  tile_shape(n_qubits, dtype, B, kmax);
+  const uint32_t amp = dtype == VQF_F64 ? 16 : 8;
+  if ((amp << B) < 128 || gates.empty()) return {};  // tiny registers: per-gate path
+  const std::vector<Pass> passes = schedule(n_qubits, B, kmax, gates);
+  std::vector<int> first(n_params, -1);
+  for (size_t p = 0; p < passes.size(); ++p) {
+    if (!passes[p].hbits.empty() && passes[p].hbits[0] == 0xffffffffu) return {};  // single-gate fallback pass
+    for (int gi : passes[p].gates) {
+      const int32_t j = gates[gi].param;
+      if (j >= 0 && (uint32_t)j < n_params && first[j] < 0) first[j] = static_cast<int>(p);
+    }
+  }
+  return first;
+}
+
+int run_circuit_tiled_shared(vqf_statevector* sv, const std::vector<TGate>& gates, const double* cs_dev,
+                             const std::vector<uint32_t>& join) {
+  const uint32_t n = sv->n_qubits;
+  uint32_t B, kmax;
+  tile_shape(n, sv->dtype, B, kmax);
+  if (join.size() != sv->batch) throw Error(VQF_LOGIC_ERROR, "shared-prefix circuit: one join pass per entry");
+  for (size_t e = 1; e < join.size(); ++e)
+    if (join[e] < join[e - 1]) throw Error(VQF_LOGIC_ERROR, "shared-prefix circuit: join passes must not decrease");
+  ensure_tile_attrs(sv);
+  const std::vector<Pass> passes = schedule(n, B, kmax, gates);
+  const uint64_t dim = sv->dim();
+  uint32_t active = 0;
+  while (active < sv->batch && join[active] == 0) ++active;
+  // entries [active, upto) take entry 0's state after the passes so far
+  const auto join_up_to = [&](uint64_t upto) {
+    if (upto <= active) return;
+    const uint32_t m = static_cast<uint32_t>(upto - active);
+    if (sv->dtype == VQF_F64) {
+      auto* a = static_cast<double2*>(sv->amps);
+      k_broadcast<double2><<<kTileBlocks * 8, 256, 0, sv->stream>>>(a, a + active * dim, m, dim);
+    } else {
+      auto* a = static_cast<float2*>(sv->amps);
+      k_broadcast<float2><<<kTileBlocks * 8, 256, 0, sv->stream>>>(a, a + active * dim, m, dim);
+    }
+    VQF_LAUNCHED();
+    active = static_cast<uint32_t>(upto);
+  };
+  for (size_t p = 0; p < passes.size(); ++p) {
+    uint32_t next = active;
+    while (next < sv->batch && join[next] <= p) ++next;
+    join_up_to(next);
+    if (sv->dtype == VQF_F64)
+      launch_pass<double>(sv, gates, passes[p], B, cs_dev, active);
+    else
+      launch_pass<float>(sv, gates, passes[p], B, cs_dev, active);
+  }
+  join_up_to(sv->batch);  // entries differing in no gate: entry 0's final state
   VQF_CUDA(cudaGetLastError());
   return static_cast<int>(passes.size());
 }

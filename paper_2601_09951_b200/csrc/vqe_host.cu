@@ -8,6 +8,7 @@
 //     gate position is one launch over every circuit.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <iostream>
 #include <limits>
@@ -478,6 +479,35 @@ struct HbmEngine {
     sv_reset(sv, kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION ? 12 : 0);  // basis_state(4, {1,1,0,0}) / |0..0>
     run_circuit_tiled(sv, ansatz_tgates(kind, layers, n), sv->cs_dev);
   }
+
+  // Same states as prepare() for a circuit family whose entry e agrees with
+  // entry 0 before tile pass join[e] (run_circuit_tiled_shared): only the
+  // entries with join 0 are reset; the rest are copied from entry 0.
+  template <typename F>
+  void prepare_shared(F&& angle, const std::vector<uint32_t>& join) {
+    const uint32_t B = sv->batch;
+    cs.resize((size_t)std::max(P, 1u) * B * 2);
+    for (uint32_t j = 0; j < P; ++j)
+      for (uint32_t e = 0; e < B; ++e) {
+        const double a = angle(j, e);
+        cs[2 * ((size_t)j * B + e)] = std::cos(0.5 * a);
+        cs[2 * ((size_t)j * B + e) + 1] = std::sin(0.5 * a);
+      }
+    sv_ensure_cs(sv, cs.size());
+    VQF_CUDA(cudaMemcpyAsync(sv->cs_dev, cs.data(), cs.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             sv->stream));
+    uint32_t k0 = 0;
+    while (k0 < B && join[k0] == 0) ++k0;
+    sv->batch = std::max(k0, 1u);
+    try {
+      sv_reset(sv, kind == VQF_ANSATZ_H2_DOUBLE_EXCITATION ? 12 : 0);
+    } catch (...) {
+      sv->batch = B;
+      throw;
+    }
+    sv->batch = B;
+    run_circuit_tiled_shared(sv, ansatz_tgates(kind, layers, n), sv->cs_dev, join);
+  }
 };
 
 size_t free_device_bytes(int device) {
@@ -497,11 +527,28 @@ struct ShiftEvaluator {
   int device;
   std::unique_ptr<HbmEngine> eng;
   bool batched;
+  // shared-prefix layout of the batched family: entry e holds circuit
+  // order[e]; join[e] = first tile pass that uses the shifted parameter
+  std::vector<uint32_t> order, join;
   ShiftEvaluator(uint32_t n_, int32_t kind_, uint32_t layers_, int device_)
       : n(n_), P(ansatz_params(kind_, layers_, n_)), NC(2 * P + 1), kind(kind_), layers(layers_), device(device_) {
     const double need = (double)NC * (double)(uint64_t{1} << n) * 16.0;
     batched = need < 0.6 * (double)free_device_bytes(device);
     eng = std::make_unique<HbmEngine>(n, kind, layers, batched ? NC : 1, device);
+    const std::vector<int> first =
+        batched ? tile_param_first_pass(n, VQF_F64, ansatz_tgates(kind, layers, n), P) : std::vector<int>{};
+    if (!first.empty() && !std::getenv("VQF_NO_SHARED_PREFIX")) {
+      const auto join_of = [&](uint32_t c) -> uint32_t {
+        if (c == 0) return 0;
+        const int f = first[(c - 1) / 2];
+        return f < 0 ? UINT32_MAX : static_cast<uint32_t>(f);
+      };
+      order.resize(NC);
+      for (uint32_t c = 0; c < NC; ++c) order[c] = c;
+      std::stable_sort(order.begin() + 1, order.end(),
+                       [&](uint32_t a, uint32_t b) { return join_of(a) < join_of(b); });
+      for (uint32_t e = 0; e < NC; ++e) join.push_back(join_of(order[e]));
+    }
   }
   // circuits [c_begin, c_end) of the shift family around theta
   void run(const std::vector<double>& theta, const CompiledHam& h, int c_count, std::vector<double>& E) {
@@ -512,6 +559,16 @@ struct ShiftEvaluator {
       if (c == 2 * j + 2) t = theta[j] - kShift;
       return t;
     };
+    if (batched && c_count == (int)NC && !order.empty()) {
+      eng->prepare_shared([&](uint32_t j, uint32_t e) { return angle_of(j, order[e]); }, join);
+      std::vector<double> tot(2 * (size_t)NC);
+      sv_expectation(eng->sv, h, tot.data());
+      for (uint32_t e = 0; e < NC; ++e) {
+        E[2 * (size_t)order[e]] = tot[2 * (size_t)e];
+        E[2 * (size_t)order[e] + 1] = tot[2 * (size_t)e + 1];
+      }
+      return;
+    }
     if (batched) {
       // entries are contiguous: run only the first c_count of them (the
       // final evaluation after the last Adam step needs one circuit)

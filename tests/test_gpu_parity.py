@@ -582,3 +582,23 @@ def test_batched_shift_run_matches_adjoint_at_width_16(gpu):
     assert len(rs.trajectory) == len(ra.trajectory) == 4
     assert np.max(np.abs(np.array(rs.trajectory) - np.array(ra.trajectory))) < 1e-10
     assert np.max(np.abs(np.array(rs.theta) - np.array(ra.theta))) < 1e-10
+
+
+@pytest.mark.parametrize("n", [12, 17])
+def test_shared_prefix_shift_batch_is_bitwise(gpu, n, monkeypatch):
+    """The batched parameter-shift family copies entry 0's state into each
+    shifted entry before the first tile pass that uses its parameter; the
+    energies and gradients are bitwise those of running every entry from
+    |0..0> (VQF_NO_SHARED_PREFIX=1)."""
+    V = gpu
+    h = V.build_tfim(n, 1.0, 0.9)
+    hea = V.AnsatzSpec.hardware_efficient(2)
+    th = list(np.random.default_rng(n).uniform(-1.5, 1.5, 2 * n))
+    cfg = V.AdamConfig(learning_rate=0.05, max_iterations=2)
+    g1 = V.gradient(th, h, hea, method="shift")
+    r1 = V.run_vqe(h, hea, cfg, th, method="shift")
+    monkeypatch.setenv("VQF_NO_SHARED_PREFIX", "1")
+    g0 = V.gradient(th, h, hea, method="shift")
+    r0 = V.run_vqe(h, hea, cfg, th, method="shift")
+    assert np.array_equal(np.asarray(g1), np.asarray(g0))
+    assert r1.trajectory == r0.trajectory and list(r1.theta) == list(r0.theta)
