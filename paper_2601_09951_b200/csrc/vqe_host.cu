@@ -526,17 +526,23 @@ struct ShiftEvaluator {
   uint32_t layers;
   int device;
   std::unique_ptr<HbmEngine> eng;
-  bool batched;
-  // shared-prefix layout of the batched family: entry e holds circuit
-  // order[e]; join[e] = first tile pass that uses the shifted parameter
+  uint32_t K;    // batch entries of the engine (<= NC; what fits 60% of free memory)
+  bool batched;  // K == NC
+  // shared-prefix layout of the family: position e holds circuit order[e]
+  // (order[0] = 0, the base); join[e] = first tile pass using the shifted
+  // parameter.  Chunks of K - 1 shifted circuits run with the base as entry 0.
   std::vector<uint32_t> order, join;
   ShiftEvaluator(uint32_t n_, int32_t kind_, uint32_t layers_, int device_)
       : n(n_), P(ansatz_params(kind_, layers_, n_)), NC(2 * P + 1), kind(kind_), layers(layers_), device(device_) {
-    const double need = (double)NC * (double)(uint64_t{1} << n) * 16.0;
-    batched = need < 0.6 * (double)free_device_bytes(device);
-    eng = std::make_unique<HbmEngine>(n, kind, layers, batched ? NC : 1, device);
+    const double entry = (double)(uint64_t{1} << n) * 16.0;
+    K = static_cast<uint32_t>(std::max(1.0, std::min<double>(NC, std::floor(0.6 * (double)free_device_bytes(device) / entry))));
+    if (const char* cap = std::getenv("VQF_SHIFT_MAX_BATCH")) K = std::max(1u, std::min<uint32_t>(K, std::atoi(cap)));
+    batched = K == NC;
+    // a chunk recomputes the base circuit: below 8 entries per chunk one
+    // circuit at a time is cheaper
+    if (!batched && K < 8) K = 1;
     const std::vector<int> first =
-        batched ? tile_param_first_pass(n, VQF_F64, ansatz_tgates(kind, layers, n), P) : std::vector<int>{};
+        K >= 2 ? tile_param_first_pass(n, VQF_F64, ansatz_tgates(kind, layers, n), P) : std::vector<int>{};
     if (!first.empty() && !std::getenv("VQF_NO_SHARED_PREFIX")) {
       const auto join_of = [&](uint32_t c) -> uint32_t {
         if (c == 0) return 0;
@@ -548,9 +554,25 @@ struct ShiftEvaluator {
       std::stable_sort(order.begin() + 1, order.end(),
                        [&](uint32_t a, uint32_t b) { return join_of(a) < join_of(b); });
       for (uint32_t e = 0; e < NC; ++e) join.push_back(join_of(order[e]));
+    } else if (!batched) {
+      K = 1;  // no prefix sharing: one circuit at a time
     }
+    eng = std::make_unique<HbmEngine>(n, kind, layers, K, device);
   }
-  // circuits [c_begin, c_end) of the shift family around theta
+  // runs f with the engine's batch temporarily set to b entries
+  template <typename F>
+  void with_batch(uint32_t b, F&& f) {
+    const uint32_t full = eng->sv->batch;
+    eng->sv->batch = b;
+    try {
+      f();
+    } catch (...) {
+      eng->sv->batch = full;
+      throw;
+    }
+    eng->sv->batch = full;
+  }
+  // circuits [0, c_count) of the shift family around theta
   void run(const std::vector<double>& theta, const CompiledHam& h, int c_count, std::vector<double>& E) {
     E.assign(2 * (size_t)c_count, 0.0);
     const auto angle_of = [&](uint32_t j, uint32_t c) {
@@ -559,37 +581,46 @@ struct ShiftEvaluator {
       if (c == 2 * j + 2) t = theta[j] - kShift;
       return t;
     };
-    if (batched && c_count == (int)NC && !order.empty()) {
-      eng->prepare_shared([&](uint32_t j, uint32_t e) { return angle_of(j, order[e]); }, join);
-      std::vector<double> tot(2 * (size_t)NC);
-      sv_expectation(eng->sv, h, tot.data());
-      for (uint32_t e = 0; e < NC; ++e) {
-        E[2 * (size_t)order[e]] = tot[2 * (size_t)e];
-        E[2 * (size_t)order[e] + 1] = tot[2 * (size_t)e + 1];
+    if (c_count == (int)NC && !order.empty()) {
+      std::vector<uint32_t> co, cj;
+      std::vector<double> tot;
+      for (uint32_t i = 1; i < NC; i += K - 1) {
+        const uint32_t m = std::min(K - 1, NC - i);
+        co.assign(1, 0u);
+        cj.assign(1, 0u);
+        for (uint32_t t = 0; t < m; ++t) {
+          co.push_back(order[i + t]);
+          cj.push_back(join[i + t]);
+        }
+        tot.assign(2 * (size_t)(m + 1), 0.0);
+        with_batch(m + 1, [&] {
+          eng->prepare_shared([&](uint32_t j, uint32_t e) { return angle_of(j, co[e]); }, cj);
+          sv_expectation(eng->sv, h, tot.data());
+        });
+        for (uint32_t e = i == 1 ? 0 : 1; e <= m; ++e) {
+          E[2 * (size_t)co[e]] = tot[2 * (size_t)e];
+          E[2 * (size_t)co[e] + 1] = tot[2 * (size_t)e + 1];
+        }
       }
       return;
     }
-    if (batched) {
+    if (batched || (K > 1 && c_count <= (int)K)) {
       // entries are contiguous: run only the first c_count of them (the
       // final evaluation after the last Adam step needs one circuit)
-      const uint32_t full = eng->sv->batch;
-      eng->sv->batch = static_cast<uint32_t>(c_count);
-      try {
+      with_batch(static_cast<uint32_t>(c_count), [&] {
         eng->prepare([&](uint32_t j, uint32_t e) { return angle_of(j, e); });
         sv_expectation(eng->sv, h, E.data());
-      } catch (...) {
-        eng->sv->batch = full;
-        throw;
-      }
-      eng->sv->batch = full;
+      });
       return;
     }
     for (int c = 0; c < c_count; ++c) {
-      eng->prepare([&](uint32_t j, uint32_t) { return angle_of(j, c); });
-      double tot[2];
-      sv_expectation(eng->sv, h, tot);
-      E[2 * c] = tot[0];
-      E[2 * c + 1] = tot[1];
+      with_batch(1, [&] {
+        eng->prepare([&](uint32_t j, uint32_t) { return angle_of(j, c); });
+        double tot[2];
+        sv_expectation(eng->sv, h, tot);
+        E[2 * c] = tot[0];
+        E[2 * c + 1] = tot[1];
+      });
     }
   }
 };

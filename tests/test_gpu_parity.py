@@ -602,3 +602,22 @@ def test_shared_prefix_shift_batch_is_bitwise(gpu, n, monkeypatch):
     r0 = V.run_vqe(h, hea, cfg, th, method="shift")
     assert np.array_equal(np.asarray(g1), np.asarray(g0))
     assert r1.trajectory == r0.trajectory and list(r1.theta) == list(r0.theta)
+
+
+def test_chunked_shift_batches_are_bitwise(gpu, monkeypatch):
+    """A family larger than the memory budget runs in chunks (base + up to
+    K - 1 shifted circuits each; VQF_SHIFT_MAX_BATCH caps K here): bitwise
+    the energies of the one-circuit-at-a-time path."""
+    V = gpu
+    n = 12
+    h = V.build_tfim(n, 1.0, 0.6)
+    hea = V.AnsatzSpec.hardware_efficient(2)
+    th = list(np.random.default_rng(3).uniform(-1.5, 1.5, 2 * n))
+    monkeypatch.setenv("VQF_SHIFT_MAX_BATCH", "9")
+    g_chunk = V.gradient(th, h, hea, method="shift")
+    monkeypatch.setenv("VQF_SHIFT_MAX_BATCH", "1")
+    g_seq = V.gradient(th, h, hea, method="shift")
+    monkeypatch.delenv("VQF_SHIFT_MAX_BATCH")
+    g_full = V.gradient(th, h, hea, method="shift")
+    assert np.array_equal(np.asarray(g_chunk), np.asarray(g_seq))
+    assert np.array_equal(np.asarray(g_full), np.asarray(g_seq))
