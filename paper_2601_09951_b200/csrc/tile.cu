@@ -35,11 +35,16 @@ namespace {
 constexpr int kMaxOps = 64;        // TileParams stays under the 4 KB kernel-parameter limit
 constexpr int kMaxHigh = 6;
 constexpr int kTileBlocks = 148;   // persistent: one CTA per SM
+// four single-buffered consumer groups (128 KB of tiles): a group loads its
+// next tile after writing back the current one while the other three
+// compute; measured against 3 groups x 2 stages (the previous default, 192
+// KB), 5 x 1 and 6 x 1 (scripts/ab_variants.sh: HEA(2) n = 30 80.5 vs 84.2,
+// 89.2, 121.5 ms)
 #ifndef VQF_TILE_GROUPS
-#define VQF_TILE_GROUPS 3
+#define VQF_TILE_GROUPS 4
 #endif
 #ifndef VQF_TILE_STAGES
-#define VQF_TILE_STAGES 2
+#define VQF_TILE_STAGES 1
 #endif
 #ifndef VQF_TILE_LB
 #define VQF_TILE_LB 11  // fp64 tile = 2^11 amplitudes (32 KB); fp32 one bit more
