@@ -223,6 +223,42 @@ class Reference:
         _check(self.lib.ref_expectation(C.c_uint32(n), a.ctypes.data_as(_dp), *args, C.byref(out), *self._e()), self.err)
         return out.value
 
+    # ---- the reference's own seeded fixtures (tests/test_helpers.hpp:28-69)
+    def random_hamiltonian(self, seed: int, n: int, n_terms: int, real=True) -> Ham:
+        """testutil::random_hamiltonian(std::mt19937(seed), n, T, real): the
+        exact Pauli sum the reference's tests draw (uncanonicalised)."""
+        o = _HamOut(cap_terms=max(8192, n_terms), cap_axes=max(1 << 18, n_terms * n))
+        _check(self.lib.ref_random_hamiltonian(C.c_uint32(seed), C.c_uint32(n), C.c_int(n_terms), C.c_int(int(real)),
+                                               *o.args(), *self._e()), self.err)
+        return o.ham(n)
+
+    def random_state(self, seed: int, n: int) -> np.ndarray:
+        """testutil::random_state(std::mt19937(seed), n), bit for bit."""
+        a = np.empty(1 << n, dtype=np.complex128)
+        _check(self.lib.ref_random_state(C.c_uint32(seed), C.c_uint32(n), a.ctypes.data_as(_dp), *self._e()), self.err)
+        return a
+
+    # ---- CPU baselines (bench.py): one reference call on a resident state
+    def time_apply_gate(self, n, amps, kind, angle, wires, reps=1) -> float:
+        """Best-of-reps seconds of ONE statevector.hpp:148 apply_gate call
+        (single-threaded, as the reference is); amps are updated in the
+        reference's own copy only."""
+        a = np.ascontiguousarray(amps, dtype=np.complex128)
+        w = (C.c_uint32 * 4)(*(list(wires) + [0] * (4 - len(wires))))
+        out = C.c_double()
+        _check(self.lib.ref_time_apply_gate(C.c_uint32(n), a.ctypes.data_as(_dp), C.c_int(kind), C.c_double(angle),
+                                            C.c_uint32(len(wires)), w, C.c_int(reps), C.byref(out), *self._e()), self.err)
+        return out.value
+
+    def time_expectation(self, n, amps, h: Ham, reps=1):
+        """(value, best-of-reps seconds) of ONE statevector.hpp:217 call."""
+        a = np.ascontiguousarray(amps, dtype=np.complex128)
+        val, sec = C.c_double(), C.c_double()
+        keep, args = _ham_in(h)
+        _check(self.lib.ref_time_expectation(C.c_uint32(n), a.ctypes.data_as(_dp), *args, C.c_int(reps), C.byref(val),
+                                             C.byref(sec), *self._e()), self.err)
+        return val.value, sec.value
+
     def prepare_ansatz(self, kind, layers, theta, n):
         t = np.ascontiguousarray(theta, dtype=np.float64)
         a = np.zeros(1 << n, dtype=np.complex128)

@@ -25,6 +25,11 @@
 #include "vqeforge/statevector.hpp"
 #include "vqeforge/sweep.hpp"
 #include "vqeforge/vqe.hpp"
+// the reference's own seeded fixtures (tests/test_helpers.hpp:28-69):
+// random Pauli sums and random states for the config-3/4 parity tests
+#include "test_helpers.hpp"
+
+#include <chrono>
 
 using namespace vqeforge;
 
@@ -376,6 +381,63 @@ int ref_run_scaling_study(const std::uint32_t* widths, std::uint32_t n_widths, s
       final_energy[i] = recs[i].final_energy;
       iters_run[i] = recs[i].iterations_run;
     }
+  });
+}
+
+// test_helpers.hpp:49-58 random_hamiltonian(mt19937(seed), n, T, real)
+// (uncanonicalised; tests canonicalise through ref_canonicalize as the
+// reference tests do, test_statevector.cpp:200).
+int ref_random_hamiltonian(std::uint32_t seed, std::uint32_t n, int n_terms, int real, HAM_OUT_ARGS, char* err,
+                           std::size_t errcap) {
+  return guarded(err, errcap, [&] {
+    std::mt19937 rng(seed);
+    HAM_OUT(testutil::random_hamiltonian(rng, n, n_terms, real != 0));
+  });
+}
+
+// test_helpers.hpp:61-69 random_state(mt19937(seed), n)
+int ref_random_state(std::uint32_t seed, std::uint32_t n, double* amps, char* err, std::size_t errcap) {
+  return guarded(err, errcap, [&] {
+    std::mt19937 rng(seed);
+    sv_out(testutil::random_state(rng, n), amps);
+  });
+}
+
+// CPU baselines for bench.py (configs 3/4): the reference's single-threaded
+// apply_gate / expectation, one call timed by steady_clock on a state that
+// is already resident (no copies inside the timed region), best of `reps`.
+int ref_time_apply_gate(std::uint32_t n, const double* amps, int kind, double angle, std::uint32_t n_wires,
+                        const std::uint32_t* wires, int reps, double* seconds, char* err, std::size_t errcap) {
+  return guarded(err, errcap, [&] {
+    StateVector psi = sv_in(n, amps);
+    Gate gate;
+    gate.kind = static_cast<GateKind>(kind);
+    gate.angle = angle;
+    gate.wires.assign(wires, wires + n_wires);
+    double best = 1e300;
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      apply_gate(psi, gate);
+      const auto t1 = std::chrono::steady_clock::now();
+      best = std::min(best, std::chrono::duration<double>(t1 - t0).count());
+    }
+    *seconds = best;
+  });
+}
+
+int ref_time_expectation(std::uint32_t sv_qubits, const double* amps, HAM_IN_ARGS, int reps, double* value,
+                         double* seconds, char* err, std::size_t errcap) {
+  return guarded(err, errcap, [&] {
+    const StateVector psi = sv_in(sv_qubits, amps);
+    const QubitHamiltonian h = HAM_IN;
+    double best = 1e300;
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      *value = expectation(psi, h);
+      const auto t1 = std::chrono::steady_clock::now();
+      best = std::min(best, std::chrono::duration<double>(t1 - t0).count());
+    }
+    *seconds = best;
   });
 }
 

@@ -288,6 +288,20 @@ int orc_apply_gate(uint32_t n, double* amps, const orc_gate* g, char* err, size_
         }
       return 0;
     }
+    case ORC_SE: { /* DE's loop (:179-200) on two wires: occupied = w0 */
+      if ((rc = check_wires(n, g, 2, err, cap))) return rc;
+      const uint64_t m0 = qubit_bit(n, g->wires[0]), m1 = qubit_bit(n, g->wires[1]);
+      const uint64_t sel = m0 | m1;
+      const double c = cos(0.5 * g->angle), s = sin(0.5 * g->angle);
+      for (uint64_t i = 0; i < dim; ++i)
+        if ((i & sel) == m0) {
+          const uint64_t j = i ^ sel;
+          const cplx x = a[i], y = a[j];
+          a[i] = c_sub(c_scale(c, x), c_scale(s, y));
+          a[j] = c_add(c_scale(s, x), c_scale(c, y));
+        }
+      return 0;
+    }
   }
   return fail(err, cap, 3, "unknown gate kind");
 }

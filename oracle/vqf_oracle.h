@@ -32,7 +32,10 @@ typedef struct {
   uint32_t cap_terms, cap_axes;
 } orc_ham_out;
 
-enum { ORC_X = 0, ORC_RY = 1, ORC_CNOT = 2, ORC_DE = 3 };
+/* ORC_SE: SingleExcitation, the engine's appended kind (not in the
+ * reference's GateKind): the Givens rotation of statevector.hpp:179-200
+ * restricted to two wires, |10> -> c|10> + s|01>, |01> -> c|01> - s|10>. */
+enum { ORC_X = 0, ORC_RY = 1, ORC_CNOT = 2, ORC_DE = 3, ORC_SE = 4 };
 
 typedef struct {
   int kind;

@@ -541,6 +541,17 @@ void run_t(AdjointPlan& pl, const std::vector<AdjGate>& prog, const std::vector<
 
 }  // namespace
 
+bool AdjointPlan::supports(const CompiledHam& h, uint32_t n_qubits) {
+  const uint32_t tb = std::min<uint32_t>(n_qubits, kTileBits);
+  const uint64_t lo_mask = (uint64_t{1} << tb) - 1;
+  uint32_t mixed = 0;
+  for (uint32_t t = h.group_offset[0]; t < h.group_offset[1]; ++t)
+    mixed += (h.terms[t].yz & ~lo_mask) != 0 && (h.terms[t].yz & lo_mask) != 0;
+  const size_t groups = h.group_offset.size() >= 2 ? h.group_offset.size() - 2 : 0;
+  const size_t off_terms = h.group_offset.empty() ? 0 : h.group_offset.back() - h.group_offset[1];
+  return mixed <= 64 && groups <= kMaxGroups && off_terms <= kMaxTerms;
+}
+
 void AdjointPlan::init(vqf_statevector* psi_, vqf_statevector* lam_, const CompiledHam& h, uint32_t n_params) {
   psi = psi_;
   lam = lam_;
@@ -560,7 +571,9 @@ void AdjointPlan::init(vqf_statevector* psi_, vqf_statevector* lam_, const Compi
     else if ((m.yz & lo_mask) == 0) hi.push_back(m);
     else mx.push_back(m);
   }
-  if (mx.size() > 64) throw_invalid("adjoint gradient: more than 64 diagonal terms straddle the tile boundary");
+  if (mx.size() > 64)
+    throw_invalid("adjoint gradient: " + std::to_string(mx.size()) +
+                  " diagonal terms straddle the tile boundary (limit 64; use parameter shift)");
   std::vector<uint32_t> ghi;
   for (size_t g = 1; g + 1 < h.group_offset.size(); ++g) {
     flips.push_back(h.group_flip[g]);
@@ -575,7 +588,10 @@ void AdjointPlan::init(vqf_statevector* psi_, vqf_statevector* lam_, const Compi
     ghi.push_back(nh);
     goff.push_back(static_cast<uint32_t>(off.size()));
   }
-  if (flips.size() > kMaxGroups || off.size() > kMaxTerms) throw_invalid("adjoint gradient: Hamiltonian too large");
+  if (flips.size() > kMaxGroups || off.size() > kMaxTerms)
+    throw_invalid("adjoint gradient: " + std::to_string(flips.size()) + " flip groups / " + std::to_string(off.size()) +
+                  " off-diagonal terms exceed the tables (" + std::to_string(kMaxGroups) + " / " +
+                  std::to_string(kMaxTerms) + "; use parameter shift)");
   std::vector<unsigned char> blob;
   auto put = [&](const void* p, size_t bytes) {
     const size_t at = (blob.size() + 15) & ~size_t{15};

@@ -45,6 +45,11 @@ struct AdjointPlan {
   AdjointPlan(const AdjointPlan&) = delete;
   ~AdjointPlan();
   void init(vqf_statevector* psi, vqf_statevector* lam, const CompiledHam& h, uint32_t n_params);
+  // Whether init() can table this Hamiltonian on an n-qubit register (at most
+  // 64 diagonal terms straddling the tile boundary, 256 flip groups, 1024
+  // off-diagonal terms).  Callers run the parameter-shift engine otherwise,
+  // so method = adjoint never fails on a large Hamiltonian.
+  static bool supports(const CompiledHam& h, uint32_t n_qubits);
   // Gradient of <psi(theta)|H|psi(theta)> for the prepared forward state in
   // psi (destroyed); e_out = {Re, Im} of the energy, grad_out[P].
   void run(const std::vector<AdjGate>& prog, const std::vector<double>& theta, double* e_out, double* grad_out);

@@ -663,7 +663,9 @@ void run_vqe_hbm(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const 
                  const std::vector<double>& init, int32_t method, int device, vqf_vqe_result* r) {
   const uint32_t n = h->n_qubits;
   const CompiledHam ch = compile_hamiltonian(h);
-  const bool adjoint = method == VQF_GRAD_ADJOINT;
+  // Hamiltonians beyond the adjoint tables take parameter shift (same
+  // gradient, the reference's own algorithm)
+  const bool adjoint = method == VQF_GRAD_ADJOINT && AdjointPlan::supports(ch, n);
   std::unique_ptr<ShiftEvaluator> evp;
   std::unique_ptr<AdjointRunner> adj;
   if (adjoint) adj = std::make_unique<AdjointRunner>(n, kind, layers, device, ch);
@@ -957,10 +959,12 @@ int vqf_gradient(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h
     if (method != VQF_GRAD_PARAMETER_SHIFT && method != VQF_GRAD_ADJOINT) throw_invalid("unknown gradient method");
     const CompiledHam ch = compile_hamiltonian(h);
     std::vector<double> th(theta, theta + n_theta), E;
-    if (method == VQF_GRAD_ADJOINT) {
+    if (method == VQF_GRAD_ADJOINT && AdjointPlan::supports(ch, h->n_qubits)) {
       AdjointRunner adj(h->n_qubits, kind, layers, device, ch);
       double e[2];
       adj.run(th, e, grad_out);
+      // energy()'s check (statevector.hpp:244-247), as on the shift path
+      if (std::abs(e[1]) >= 1e-10) throw_runtime(imag_msg(e[1]));
       return;
     }
     ShiftEvaluator ev(h->n_qubits, kind, layers, device);

@@ -1,7 +1,7 @@
 """Distributed state vector on one B200 with virtual ranks (shards on one
 device, exchanges as device copies, local compute by the engine's kernels):
-amplitudes and energies against the engine's own single-state run and, at
-small width, the oracle."""
+amplitudes and energies against the engine's own single-state run and the
+CPU oracle."""
 from __future__ import annotations
 
 import random
@@ -49,9 +49,13 @@ def test_dsv_virtual_ranks_on_gpu(gpu, orc, n, world):
     assert abs(d.expectation(h.terms) - V.expectation(single, hv)) < 1e-10
     tf = orc.build_tfim(n, 1.0, 1.0)
     assert abs(d.expectation(tf.terms) - V.expectation(single, V.QubitHamiltonian(n, [V.PauliTerm(c, a) for c, a in tf.terms]))) < 1e-10
-    if n <= 12:
-        gs4 = [g for g in gs if g[0] != 4]  # the reference has no SingleExcitation
-        assert gs4
+    # and against the CPU oracle directly (vqf_oracle.c, SingleExcitation
+    # included; pinned to the reference and a dense embedding in test_oracle.py)
+    ref_amps = orc.apply_gates(n, psi0, gs)
+    for r, amps in d.local_amplitudes().items():
+        assert np.max(np.abs(amps - ref_amps[r << nl:(r + 1) << nl])) < 1e-12
+    assert abs(d.expectation(h.terms) - orc.expectation(n, ref_amps, h)) < 1e-10
+    assert abs(d.expectation(tf.terms) - orc.expectation(n, ref_amps, tf)) < 1e-10
 
 
 @pytest.mark.parametrize("n,world", [(14, 2), (20, 8)])

@@ -57,7 +57,7 @@ def test_gates_match_oracle(gpu, orc, n):
     rng = np.random.default_rng(100 + n)
     pr = random.Random(200 + n)
     psi0 = random_state(rng, n)
-    gates = rand_gates(pr, n, 40, kinds=(0, 1, 2, 3))
+    gates = rand_gates(pr, n, 40, kinds=(0, 1, 2, 3, 4))  # SingleExcitation: vqf_oracle.c ORC_SE
     want = orc.apply_gates(n, psi0, gates)
     psi = V.StateVector(n)
     psi.amplitudes = psi0
@@ -621,3 +621,22 @@ def test_chunked_shift_batches_are_bitwise(gpu, monkeypatch):
     g_full = V.gradient(th, h, hea, method="shift")
     assert np.array_equal(np.asarray(g_chunk), np.asarray(g_seq))
     assert np.array_equal(np.asarray(g_full), np.asarray(g_seq))
+
+
+def test_adjoint_large_hamiltonian_falls_back_and_checks_residue(gpu, orc):
+    """Hamiltonians beyond the adjoint tables (> 256 flip groups) take the
+    parameter-shift engine under method="adjoint" instead of failing; the
+    adjoint path raises energy()'s imaginary-residue error like shift."""
+    V = gpu
+    n = 10
+    h = orc.canonicalize(random_hamiltonian(random.Random(31), n, 400))
+    th = np.random.default_rng(31).uniform(-1, 1, 2 * n)
+    hea = V.AnsatzSpec.hardware_efficient(2)
+    g = V.gradient(th, to_v(V, h), hea, method="adjoint")
+    assert np.max(np.abs(g - orc.gradient(1, 2, th, h))) < E_TOL
+    r = V.run_vqe(to_v(V, h), hea, V.AdamConfig(learning_rate=0.05, max_iterations=2), list(th), method="adjoint")
+    want = orc.run_vqe(h, kind=1, layers=2, lr=0.05, max_iter=2, init=list(th))
+    assert np.max(np.abs(np.array(r.trajectory) - want["trajectory"])) < E_TOL
+    bad = V.QubitHamiltonian(n, [V.PauliTerm(1.0, [(0, 1)]), V.PauliTerm(0.5j, [(3, 3)])])
+    with pytest.raises(RuntimeError, match="imaginary residue"):
+        V.gradient(th, bad, hea, method="adjoint")

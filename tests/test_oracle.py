@@ -206,3 +206,78 @@ def test_reference_pes_properties(golden):
     i = int(np.argmin(p["energy"]))
     assert 0.70 <= p["bond"][i] <= 0.78 and abs(p["energy"][i] + 1.137) < 0.005
     assert all(it == 200 for it in p["iterations"])
+
+
+# ----------------------------------------- dense embedding (independent)
+def _small_gate(kind, angle):
+    """Local unitaries of tests/oracles/dense_gates.hpp:30-67 (wire k = local
+    bit w-1-k) plus SingleExcitation, the engine's appended kind: the
+    DoubleExcitation Givens restricted to |10>,|01> (local indices 2, 1)."""
+    c, s = math.cos(0.5 * angle), math.sin(0.5 * angle)
+    if kind == 0:
+        return np.array([[0, 1], [1, 0]], dtype=complex)
+    if kind == 1:
+        return np.array([[c, -s], [s, c]], dtype=complex)
+    if kind == 2:
+        m = np.eye(4, dtype=complex)
+        m[2, 2] = m[3, 3] = 0
+        m[2, 3] = m[3, 2] = 1
+        return m
+    if kind == 3:
+        m = np.eye(16, dtype=complex)
+        m[12, 12], m[12, 3], m[3, 12], m[3, 3] = c, -s, s, c
+        return m
+    m = np.eye(4, dtype=complex)
+    m[2, 2], m[2, 1], m[1, 2], m[1, 1] = c, -s, s, c
+    return m
+
+
+def _embed(kind, angle, wires, n):
+    """dense_gates.hpp:70-101 embed_gate: the full 2^n unitary by index
+    arithmetic (qubit 0 = most significant bit)."""
+    small = _small_gate(kind, angle)
+    w = len(wires)
+    dim = 1 << n
+    mask = 0
+    for q in wires:
+        mask |= 1 << (n - 1 - q)
+
+    def loc(i):
+        return sum(((i >> (n - 1 - q)) & 1) << (w - 1 - k) for k, q in enumerate(wires))
+
+    full = np.zeros((dim, dim), dtype=complex)
+    for i in range(dim):
+        for j in range(dim):
+            if (i & ~mask) == (j & ~mask):
+                full[i, j] = small[loc(i), loc(j)]
+    return full
+
+
+@pytest.mark.parametrize("n", [2, 4, 6])
+def test_single_excitation_oracle_vs_dense_embedding(orc, n):
+    """The SingleExcitation restatement (vqf_oracle.c ORC_SE) against the
+    dense embedding, in the style of test_statevector.cpp:150-166; DE and
+    the reference kinds as a control of the embedding itself."""
+    rng = np.random.default_rng(20260802 + n)
+    pr = random.Random(n)
+    for _ in range(20):
+        kind = pr.choice([4, 4, 0, 1, 2] + ([3] if n >= 4 else []))
+        wires = pr.sample(range(n), [1, 1, 2, 4, 2][kind])
+        angle = pr.uniform(-3.2, 3.2)
+        psi = random_state(rng, n)
+        want = _embed(kind, angle, wires, n) @ psi
+        got = orc.apply_gates(n, psi, [(kind, angle, wires)])
+        assert np.max(np.abs(got - want)) < 1e-12
+    # |10> -> cos|10> + sin|01>: the engine's convention (DE's, on two wires)
+    e = orc.apply_gates(2, np.array([0, 0, 1, 0], dtype=complex), [(4, 0.6, [0, 1])])
+    assert abs(e[2] - math.cos(0.3)) < 1e-15 and abs(e[1] - math.sin(0.3)) < 1e-15
+
+
+def test_reference_fixtures_are_seeded(ref):
+    """ref_random_hamiltonian / ref_random_state are test_helpers.hpp's own
+    generators (mt19937): deterministic, normalised, the documented shape."""
+    h = ref.random_hamiltonian(20260804, 6, 32)
+    assert len(h.terms) == 32 and all(c.imag == 0 and -2 <= c.real <= 2 for c, _ in h.terms)
+    assert ref.random_hamiltonian(20260804, 6, 32).terms == h.terms
+    a = ref.random_state(20260802, 5)
+    assert abs(np.vdot(a, a).real - 1) < 1e-14 and np.array_equal(a, ref.random_state(20260802, 5))

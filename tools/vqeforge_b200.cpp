@@ -7,6 +7,13 @@
 // "--flag=value", as CLI11 accepts).  Additions: `scaling --gradient
 // adjoint`.  `--workers` / `--worker-list` count GPU workers (one host
 // thread + stream per worker, round-robin over visible devices).
+//
+// Attribution: the argument parser (Args) is new, but the command bodies
+// (parse_int_list, write_outputs, run_pes, run_bench, run_scaling) follow the
+// flow of the reference CLI, /root/reference/proj/tools/vqeforge.cpp:36-270
+// (Copyright 2026 VQE Forge contributors, Apache License 2.0), because their
+// stdout lines, output files and manifest keys must match the reference
+// byte for byte.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
