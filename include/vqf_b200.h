@@ -322,6 +322,17 @@ int vqf_pes_create(const vqf_sweep_config* config, int32_t device, vqf_pes* out)
 int vqf_pes_launch(vqf_pes plan, void* cuda_stream);
 int vqf_pes_read(vqf_pes plan, vqf_sweep_report* report);
 int vqf_pes_destroy(vqf_pes plan);
+
+/* Diagnostic view of the PES kernel's on-device chemistry (chem.hpp:280-482
+ * run_hartree_fock + jordan_wigner, built inside the fused kernel): for each
+ * bond, the Hamiltonian the optimisation uses, as up to 16 terms.  Term t of
+ * bond b: keys[16b + t] encodes the Pauli string with bit q = X on qubit q
+ * and bit 4 + q = Z on qubit q (both set = Y); coeffs[16b + t] its (real)
+ * coefficient; n_terms[b] the count (0 when the point failed).  hf[4b..4b+3]
+ * = {hf_energy, electronic, nuclear_repulsion, scf_iterations}.  Bonds
+ * outside chem.hpp's range fail with the BondLengthOutOfRange text. */
+int vqf_pes_device_hamiltonians(const double* bonds, uint32_t n_bonds, int32_t device, uint32_t* n_terms,
+                                int32_t* keys, double* coeffs, double* hf);
 /* run_scaling_study (sweep.hpp:265-307). records holds n_widths entries. */
 int vqf_run_scaling_study(const vqf_scaling_config* config, vqf_scaling_record* records);
 

@@ -137,6 +137,7 @@ SIGNATURES = [
     ("vqf_pes_launch", C.c_int, [PES, C.c_void_p]),
     ("vqf_pes_read", C.c_int, [PES, C.POINTER(SweepReport)]),
     ("vqf_pes_destroy", C.c_int, [PES]),
+    ("vqf_pes_device_hamiltonians", C.c_int, [dp, C.c_uint32, C.c_int32, u32p, i32p, dp, dp]),
     ("vqf_run_scaling_study", C.c_int, [C.POINTER(ScalingConfig), C.POINTER(ScalingRecord)]),
 ]
 

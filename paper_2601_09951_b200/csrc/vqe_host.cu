@@ -1021,6 +1021,36 @@ int vqf_run_vqe_batch(const vqf_hamiltonian* hs, uint32_t batch, int32_t kind, u
   });
 }
 
+int vqf_pes_device_hamiltonians(const double* bonds, uint32_t n_bonds, int32_t device, uint32_t* n_terms,
+                                int32_t* keys, double* coeffs, double* hf) {
+  return guarded([&] {
+    if (n_bonds == 0) return;
+    if (bonds == nullptr || n_terms == nullptr || keys == nullptr || coeffs == nullptr || hf == nullptr)
+      throw_invalid("null argument");
+    for (uint32_t b = 0; b < n_bonds; ++b) chem::check_bond(bonds[b]);
+    SmallJob j;
+    j.batch = n_bonds;
+    j.n_qubits = 4;
+    j.kind = VQF_ANSATZ_H2_DOUBLE_EXCITATION;
+    j.P = 1;
+    j.adam = vqf_adam_config{0.01, 0.9, 0.999, 1e-8, 1, 0, 0.0};
+    j.pes = true;
+    j.want_ham = true;
+    j.bonds.assign(bonds, bonds + n_bonds);
+    j.status_in.assign(n_bonds, 0);
+    run_small(j, device, false);
+    for (uint32_t b = 0; b < n_bonds; ++b) {
+      if (j.status[b] != kStatusOk) throw_runtime(small_error(j, b, bonds[b]));
+      n_terms[b] = static_cast<uint32_t>(j.ham_count[b]);
+      for (int t = 0; t < 16; ++t) {
+        keys[16 * b + t] = t < j.ham_count[b] ? j.ham_keys[16 * b + t] : 0;
+        coeffs[16 * b + t] = t < j.ham_count[b] ? j.ham_coeffs[16 * b + t] : 0.0;
+      }
+      for (int k = 0; k < 4; ++k) hf[4 * b + k] = j.hf[4 * b + k];
+    }
+  });
+}
+
 int vqf_run_sweep(const vqf_sweep_config* cfg, vqf_sweep_report* rep) {
   return guarded([&] {
     if (cfg == nullptr || rep == nullptr) throw_invalid("null argument");

@@ -509,6 +509,37 @@ def run_sweep(config: SweepConfig = None, trajectories: bool = False) -> SweepRe
     return buf.report()
 
 
+def pes_device_hamiltonians(bonds: Sequence[float], device: int = 0):
+    """The Hamiltonians (and HF summaries) the fused PES kernel builds on the
+    device for each bond (vqf_pes_device_hamiltonians): a list of
+    (QubitHamiltonian, {hf_energy, electronic_energy, nuclear_repulsion,
+    scf_iterations}) with terms as the kernel holds them."""
+    b = np.ascontiguousarray(bonds, dtype=np.float64)
+    n = len(b)
+    cnt = np.zeros(max(n, 1), dtype=np.uint32)
+    keys = np.zeros(16 * max(n, 1), dtype=np.int32)
+    coeffs = np.zeros(16 * max(n, 1))
+    hf = np.zeros(4 * max(n, 1))
+    check(lib.vqf_pes_device_hamiltonians(b.ctypes.data_as(A.dp), n, device, cnt.ctypes.data_as(A.u32p),
+                                          keys.ctypes.data_as(A.i32p), coeffs.ctypes.data_as(A.dp),
+                                          hf.ctypes.data_as(A.dp)))
+    out = []
+    for i in range(n):
+        terms = []
+        for t in range(int(cnt[i])):
+            k = int(keys[16 * i + t])
+            axes = []
+            for q in range(4):
+                x, z = (k >> q) & 1, (k >> (4 + q)) & 1
+                if x or z:
+                    axes.append((q, 2 if (x and z) else (1 if x else 3)))
+            terms.append(PauliTerm(complex(coeffs[16 * i + t], 0.0), axes))
+        out.append((QubitHamiltonian(4, terms), {"hf_energy": hf[4 * i], "electronic_energy": hf[4 * i + 1],
+                                                 "nuclear_repulsion": hf[4 * i + 2],
+                                                 "scf_iterations": int(hf[4 * i + 3])}))
+    return out
+
+
 class PesPlan:
     """Device-resident run_sweep slice (vqf_pes_*): stage once, launch the
     fused kernel on any CUDA stream, read back into a SweepReport."""
