@@ -237,6 +237,153 @@ def gate_roofline(V, torch, device, n, steps, warmup):
             "extra": extra}
 
 
+# ------------------------------------------------- configs 3 / 4 (one GPU)
+def configs_3_4(V, torch, device, n_big, steps, warmup, peak, cpu_ok, cpu_seconds):
+    """BASELINE configs 3 and 4 on one GPU (each rank a replica), with the
+    reference's own single-threaded CPU path timed beside them (rank 0, N = 1).
+
+    Config 4 (n_big = 30 fp64, 16 GiB state >> L2): one launch of each
+    kernel class on a state already in HBM, CUDA events on the state's
+    stream, median over `steps`; algorithmic bytes per launch as in DESIGN.md
+    section 3 (S = 2^n * 16: RY / X 2S, CNOT S, DE S/4, SE S, fused HEA layer
+    2S per pass, expectation S per state pass); frac = achieved / peak.
+    Config 3: one HEA(2) Adam iteration (energy + gradient + step) of
+    run_vqe with TFIM and with the reference's random 32-term sum
+    (mt19937(20260804)), parameter shift (the reference's algorithm) and
+    adjoint, at n = 20 / 24 / 26.  CPU: the reference's apply_gate /
+    expectation (one call, single-threaded) at n = 20 and 24 and one
+    run_vqe iteration at n = 20, timed concurrently in a thread pool (each
+    call single-threaded; ctypes drops the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    out = {"config4": {}, "config3": {}}
+    n = n_big
+    S = (1 << n) * 16
+    stream = torch.cuda.Stream(device=device)
+    ref = None
+    if cpu_ok:
+        from oracle.oracle import load_ref
+
+        ref = load_ref()
+    pool = ThreadPoolExecutor(6) if ref is not None else None
+    cpu_jobs = {}
+    if pool is not None:
+        # reference CPU baselines run while the GPU measures (single-threaded
+        # calls; the sample sizes below keep the whole leg within ~30 s)
+        def cpu_kernels(nq):
+            psi0 = ref.random_state(20260802, nq)
+            r = {"n": nq, "ry_s": ref.time_apply_gate(nq, psi0, 1, 0.3, [nq // 2]),
+                 "cnot_s": ref.time_apply_gate(nq, psi0, 2, 0.0, [nq // 2, nq // 2 + 1]),
+                 "de_s": ref.time_apply_gate(nq, psi0, 3, 0.7, [0, 1, 2, 3])}
+            tfim = ref.build_tfim(nq, 1.0, 1.0)
+            rnd = ref.canonicalize(ref.random_hamiltonian(20260804, nq, 32))
+            r["tfim_expectation_s"] = ref.time_expectation(nq, psi0, tfim)[1]
+            r["random32_expectation_s"] = ref.time_expectation(nq, psi0, rnd)[1]
+            return r
+
+        def cpu_iteration(nq, ham):
+            h = ref.build_tfim(nq, 1.0, 1.0) if ham == "tfim" else ref.canonicalize(ref.random_hamiltonian(20260804, nq, 32))
+            t0 = time.perf_counter()
+            ref.run_vqe(h, kind=1, layers=2, lr=0.05, max_iter=1, init=[0.1] * (2 * nq))
+            return time.perf_counter() - t0
+
+        cpu_jobs["kernels20"] = pool.submit(cpu_kernels, 20)
+        cpu_jobs["kernels24"] = pool.submit(cpu_kernels, 24)
+        cpu_jobs["iter20_tfim"] = pool.submit(cpu_iteration, 20, "tfim")
+        cpu_jobs["iter20_random32"] = pool.submit(cpu_iteration, 20, "random32")
+
+    def timed(fn, reps):
+        with torch.cuda.stream(stream):
+            fn()
+            ts = []
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize(device)
+                ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    reps = max(3, min(steps, 10))
+    for dtype, amp in (("f64", 16), ("f32", 8)):
+        Sd = (1 << n) * amp
+        psi = V.StateVector(n, dtype=dtype, device=device)
+        psi.set_stream(stream.cuda_stream)
+        V.apply_circuit(psi, [V.Gate.ry(0.3 + 0.01 * q, q) for q in range(n)])  # dense state
+        m = n // 2
+        kernels = {
+            "ry_mid": (lambda: V.apply_gate(psi, V.Gate.ry(0.01, m)), 2 * Sd),
+            "ry_low_wire": (lambda: V.apply_gate(psi, V.Gate.ry(0.01, n - 1)), 2 * Sd),
+            "cnot_mid": (lambda: V.apply_gate(psi, V.Gate.cnot(m, m + 1)), Sd),
+            "de_top": (lambda: V.apply_gate(psi, V.Gate.double_excitation(0.2, 0, 1, 2, 3)), Sd // 4),
+            "se_mid": (lambda: V.apply_gate(psi, V.Gate.single_excitation(0.2, m, m + 2)), Sd),
+        }
+        layer = [V.Gate.ry(0.1 * (q + 1), q) for q in range(n)] + [V.Gate.cnot(q, q + 1) for q in range(n - 1)]
+        passes = V.circuit_plan(n, layer, dtype)["passes"]
+        kernels["hea_layer_fused"] = (lambda: V.apply_circuit(psi, layer), 2 * Sd * passes)
+        tfim = V.build_tfim(n, 1.0, 1.0)
+        rnd = None
+        if ref is not None:
+            rh = ref.canonicalize(ref.random_hamiltonian(20260804, n, 32))
+            rnd = V.QubitHamiltonian(n, [V.PauliTerm(c, a) for c, a in rh.terms])
+        tp = V.expectation_plan(tfim)["state_passes"]
+        kernels["tfim_expectation"] = (lambda: V.expectation(psi, tfim), Sd * tp)
+        if rnd is not None:
+            rp = V.expectation_plan(rnd)["state_passes"]
+            kernels["random32_expectation"] = (lambda: V.expectation(psi, rnd), Sd * rp)
+        res = {"n_qubits": n, "state_bytes": Sd}
+        for name, (fn, alg) in kernels.items():
+            ms = timed(fn, reps)
+            res[name] = {"ms": ms, "alg_bytes": alg, "GBps": alg / (ms * 1e-3) / 1e9,
+                         "frac": alg / (ms * 1e-3) / 1e9 / peak}
+        res["hea_layer_fused"]["passes"] = passes
+        res["tfim_expectation"]["state_passes"] = tp
+        if rnd is not None:
+            res["random32_expectation"]["state_passes"] = rp
+        out["config4"][dtype] = res
+        del psi
+        torch.cuda.empty_cache()
+
+    # config 3: one Adam iteration of run_vqe (HEA(2), theta0 = 0.1, lr 0.05)
+    for nq in (20, 24, 26):
+        tf = V.build_tfim(nq, 1.0, 1.0)
+        hams = {"tfim": tf}
+        if ref is not None:
+            rh = ref.canonicalize(ref.random_hamiltonian(20260804, nq, 32))
+            hams["random32"] = V.QubitHamiltonian(nq, [V.PauliTerm(c, a) for c, a in rh.terms])
+        row = {}
+        for hname, h in hams.items():
+            for method in ("shift", "adjoint"):
+                cfg = V.AdamConfig(learning_rate=0.05, max_iterations=1)
+                V.run_vqe(h, V.AnsatzSpec.hardware_efficient(2), cfg, [0.1] * (2 * nq), method=method)  # warm
+                t0 = time.perf_counter()
+                r = V.run_vqe(h, V.AnsatzSpec.hardware_efficient(2), cfg, [0.1] * (2 * nq), method=method)
+                row[f"{hname}_{method}_s"] = time.perf_counter() - t0
+                row[f"{hname}_{method}_energy"] = r.energy
+        out["config3"][f"n{nq}"] = row
+    if pool is not None:
+        cpu = {k: f.result() for k, f in cpu_jobs.items()}
+        pool.shutdown()
+        out["cpu_baseline"] = {
+            "kind": "reference", "cores": 1,
+            "sample": "reference statevector.hpp apply_gate / expectation: one call each on a resident "
+                      "random_state (n = 20 and 24); run_vqe (HEA(2), 1 Adam iteration = 82 circuits) at n = 20; "
+                      "single-threaded calls run concurrently in a 6-thread pool",
+            "n20": cpu["kernels20"], "n24": cpu["kernels24"],
+            "iteration_n20_tfim_s": cpu["iter20_tfim"], "iteration_n20_random32_s": cpu["iter20_random32"],
+        }
+        c3 = out["config3"]["n20"]
+        out["config3"]["speedup_vs_reference_n20"] = {
+            "tfim_shift": cpu["iter20_tfim"] / c3["tfim_shift_s"],
+            "tfim_adjoint": cpu["iter20_tfim"] / c3["tfim_adjoint_s"],
+        }
+        if "random32_shift_s" in c3:
+            out["config3"]["speedup_vs_reference_n20"]["random32_shift"] = cpu["iter20_random32"] / c3["random32_shift_s"]
+            out["config3"]["speedup_vs_reference_n20"]["random32_adjoint"] = cpu["iter20_random32"] / c3["random32_adjoint_s"]
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -301,6 +448,11 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- gate-apply roofline (each rank a replica; rank 0 reported)
     gate = gate_roofline(V, torch, local_rank, args.gate_qubits, args.steps, args.warmup) if args.gate_qubits else None
+    peak, peak_src = load_peaks()
+    c34 = None
+    if args.gate_qubits and not args.no_configs34:
+        c34 = configs_3_4(V, torch, local_rank, args.gate_qubits, args.steps, args.warmup, peak,
+                          world == 1 and rank == 0 and not args.no_cpu_baseline, args.cpu_seconds)
     clk = clocks.stop()
 
     # ---- gather results, check parity against the reference's fixture
@@ -319,7 +471,6 @@ def run_ours(args, rank, world, local_rank):
         "e2e_equals_value_run": pts == e2e_pts,
         "all_ok": all(p[3] for p in pts),
     }
-    peak, peak_src = load_peaks()
     line = {
         "metric": METRIC, "value": pes_s, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": pes_s * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
@@ -341,6 +492,8 @@ def run_ours(args, rank, world, local_rank):
         }
         line["config"]["gate_roofline_workload"] = f"RY on an n={gate['n_qubits']} fp64 state (2^{gate['n_qubits']} x 16 B)"
         line["state_vector_kernels"] = gate["extra"]
+    if c34 is not None:
+        line["configs_3_4"] = c34
     line["pes_kernel"] = {"bound": "latency", "note": "100 bonds x 256 B states live in registers/shared memory; "
                           "one CTA per bond, 200 dependent Adam iterations", "device_ms": pes_s * 1e3}
     if world == 1 and not args.no_cpu_baseline:
@@ -357,9 +510,16 @@ def run_ours(args, rank, world, local_rank):
                 times.append(dt)
                 t_spent += dt
                 reps += 1
+            w1 = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                ref.run_sweep(workers=1)
+                w1.append(time.perf_counter() - t0)
             line["cpu_baseline"] = {"value": statistics.mean(times), "unit": "s", "cores": cores, "kind": "reference",
                                     "sample": f"{reps} repetitions of the full workload (reference run_sweep, "
-                                              f"workers={cores}), {t_spent:.1f} s of CPU wall time"}
+                                              f"workers={cores}), {t_spent:.1f} s of CPU wall time",
+                                    "workers1": {"value": statistics.mean(w1), "unit": "s", "cores": 1,
+                                                 "sample": "3 repetitions of the full workload, run_sweep workers=1"}}
     print(json.dumps(line))
 
 
@@ -372,6 +532,7 @@ def main():
     ap.add_argument("--gate-qubits", type=int, default=30)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs34", action="store_true", help="skip the config 3 / 4 block")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":

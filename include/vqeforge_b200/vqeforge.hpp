@@ -461,10 +461,11 @@ struct VqeResult {  // vqe.hpp:176-186
   double wall_seconds = 0.0;
 };
 
-// vqe.hpp:194-254 — the whole optimisation loop runs on the device.
-inline VqeResult run_vqe(const QubitHamiltonian& h, const AnsatzSpec& spec, const AdamConfig& config,
-                         const std::vector<double>& initial_theta = {}) {
-  detail::CsrHam c(h);
+namespace detail {
+inline VqeResult run_vqe_on(const QubitHamiltonian& h, const AnsatzSpec& spec, const AdamConfig& config,
+                            const std::vector<double>& initial_theta, std::int32_t method, std::int32_t dtype,
+                            int device) {
+  CsrHam c(h);
   const std::size_t P = n_parameters(spec, h.n_qubits);
   VqeResult r;
   r.theta.assign(P, 0.0);
@@ -473,10 +474,10 @@ inline VqeResult run_vqe(const QubitHamiltonian& h, const AnsatzSpec& spec, cons
   out.theta = r.theta.data();
   out.trajectory = r.trajectory.data();
   out.trajectory_capacity = static_cast<std::uint32_t>(r.trajectory.size());
-  const vqf_adam_config a = detail::to_c(config);
-  detail::check(vqf_run_vqe(&c.view, static_cast<std::int32_t>(spec.kind), spec.layers, &a,
-                            initial_theta.empty() ? nullptr : initial_theta.data(),
-                            static_cast<std::uint32_t>(initial_theta.size()), VQF_GRAD_PARAMETER_SHIFT, 0, &out));
+  const vqf_adam_config a = to_c(config);
+  check(vqf_run_vqe_ex(&c.view, static_cast<std::int32_t>(spec.kind), spec.layers, &a,
+                       initial_theta.empty() ? nullptr : initial_theta.data(),
+                       static_cast<std::uint32_t>(initial_theta.size()), method, device, dtype, &out));
   r.energy = out.energy;
   r.trajectory.resize(out.trajectory_len);
   r.iterations_run = out.iterations_run;
@@ -484,6 +485,47 @@ inline VqeResult run_vqe(const QubitHamiltonian& h, const AnsatzSpec& spec, cons
   r.wall_seconds = out.wall_seconds;
   return r;
 }
+}  // namespace detail
+
+// vqe.hpp:194-254 — the whole optimisation loop runs on the device.
+inline VqeResult run_vqe(const QubitHamiltonian& h, const AnsatzSpec& spec, const AdamConfig& config,
+                         const std::vector<double>& initial_theta = {}) {
+  return detail::run_vqe_on(h, spec, config, initial_theta, VQF_GRAD_PARAMETER_SHIFT, VQF_F64, 0);
+}
+
+// Engine extensions beyond the reference signatures: state precision
+// (complex128 as the reference, or complex64: energies within 1e-5,
+// fixed-iteration runs only), gradient rule and device.
+namespace gpu {
+enum class Precision : std::int32_t { F64 = VQF_F64, F32 = VQF_F32 };
+enum class Gradient : std::int32_t { ParameterShift = VQF_GRAD_PARAMETER_SHIFT, Adjoint = VQF_GRAD_ADJOINT };
+
+inline double energy(const std::vector<double>& theta, const QubitHamiltonian& h, const AnsatzSpec& spec,
+                     Precision p, int device = 0) {
+  detail::CsrHam c(h);
+  double e = 0.0;
+  detail::check(vqf_energy_ex(theta.data(), static_cast<std::uint32_t>(theta.size()), &c.view,
+                              static_cast<std::int32_t>(spec.kind), spec.layers, device, static_cast<std::int32_t>(p),
+                              &e));
+  return e;
+}
+
+inline std::vector<double> gradient(const std::vector<double>& theta, const QubitHamiltonian& h,
+                                    const AnsatzSpec& spec, Gradient method, Precision p, int device = 0) {
+  detail::CsrHam c(h);
+  std::vector<double> g(theta.size());
+  detail::check(vqf_gradient_ex(theta.data(), static_cast<std::uint32_t>(theta.size()), &c.view,
+                                static_cast<std::int32_t>(spec.kind), spec.layers, static_cast<std::int32_t>(method),
+                                device, static_cast<std::int32_t>(p), g.data()));
+  return g;
+}
+
+inline VqeResult run_vqe(const QubitHamiltonian& h, const AnsatzSpec& spec, const AdamConfig& config,
+                         const std::vector<double>& initial_theta, Gradient method, Precision p, int device = 0) {
+  return detail::run_vqe_on(h, spec, config, initial_theta, static_cast<std::int32_t>(method),
+                            static_cast<std::int32_t>(p), device);
+}
+}  // namespace gpu
 
 // ------------------------------------------------------------------ chem
 // chem.hpp:473-482 (HF + Jordan-Wigner, host build over the shared core)
@@ -615,6 +657,7 @@ struct ScalingConfig {  // sweep.hpp:237-249
   bool force = false;
   bool adjoint = false;  // extension: adjoint gradients instead of parameter shift
   int device = 0;
+  bool fp32 = false;     // extension: complex64 states (fixed-iteration runs)
 };
 
 struct ScalingRecord {  // sweep.hpp:251-257
@@ -630,7 +673,8 @@ inline std::vector<ScalingRecord> run_scaling_study(const ScalingConfig& config)
   vqf_scaling_config c{config.qubits.data(), static_cast<std::uint32_t>(config.qubits.size()), config.layers,
                        config.iterations, config.learning_rate, config.coupling, config.field,
                        config.z_sum_mode ? 1 : 0, config.theta_init, config.force ? 1 : 0,
-                       config.adjoint ? VQF_GRAD_ADJOINT : VQF_GRAD_PARAMETER_SHIFT, config.device};
+                       config.adjoint ? VQF_GRAD_ADJOINT : VQF_GRAD_PARAMETER_SHIFT, config.device,
+                       config.fp32 ? VQF_F32 : VQF_F64};
   std::vector<vqf_scaling_record> recs(config.qubits.size());
   detail::check(vqf_run_scaling_study(&c, recs.data()));
   std::vector<ScalingRecord> out;

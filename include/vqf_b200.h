@@ -183,6 +183,7 @@ typedef struct vqf_scaling_config {
   int32_t force;
   int32_t gradient_method; /* VQF_GRAD_* ; reference = parameter shift */
   int32_t device;
+  int32_t dtype; /* VQF_F64 (reference precision) or VQF_F32 (complex64 states) */
 } vqf_scaling_config;
 
 typedef struct vqf_scaling_record {
@@ -308,6 +309,18 @@ int vqf_gradient(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h
 int vqf_run_vqe(const vqf_hamiltonian* h, int32_t ansatz_kind, uint32_t layers,
                 const vqf_adam_config* config, const double* init, uint32_t n_init,
                 int32_t gradient_method, int32_t device, vqf_vqe_result* result);
+/* The same three with the state precision: VQF_F64 (the reference's
+ * complex128; what the entry points above use) or VQF_F32 (complex64 states,
+ * fp64 angles / reductions / Adam; energies within 1e-5 of fp64).  fp32
+ * run_vqe is fixed-iteration only (a gradient tolerance -> invalid_argument). */
+int vqf_energy_ex(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h,
+                  int32_t ansatz_kind, uint32_t layers, int32_t device, int32_t dtype, double* out);
+int vqf_gradient_ex(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h,
+                    int32_t ansatz_kind, uint32_t layers, int32_t method, int32_t device,
+                    int32_t dtype, double* grad_out);
+int vqf_run_vqe_ex(const vqf_hamiltonian* h, int32_t ansatz_kind, uint32_t layers,
+                   const vqf_adam_config* config, const double* init, uint32_t n_init,
+                   int32_t gradient_method, int32_t device, int32_t dtype, vqf_vqe_result* result);
 /* Batched run_vqe: `batch` independent problems with the same ansatz and
  * register size, one on-device optimisation loop each, one launch. */
 int vqf_run_vqe_batch(const vqf_hamiltonian* hs, uint32_t batch, int32_t ansatz_kind,

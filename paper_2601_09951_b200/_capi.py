@@ -78,7 +78,7 @@ class ScalingConfig(C.Structure):
     _fields_ = [("qubits", u32p), ("n_widths", C.c_uint32), ("layers", C.c_uint32), ("iterations", C.c_int32),
                 ("learning_rate", C.c_double), ("coupling", C.c_double), ("field", C.c_double),
                 ("z_sum_mode", C.c_int32), ("theta_init", C.c_double), ("force", C.c_int32),
-                ("gradient_method", C.c_int32), ("device", C.c_int32)]
+                ("gradient_method", C.c_int32), ("device", C.c_int32), ("dtype", C.c_int32)]
 
 
 class ScalingRecord(C.Structure):
@@ -126,10 +126,16 @@ SIGNATURES = [
     ("vqf_cross_expectation", C.c_int, [SV, SV, C.POINTER(Hamiltonian), dp]),
     ("vqf_prepare_ansatz", C.c_int, [C.c_int32, C.c_uint32, dp, C.c_uint32, SV]),
     ("vqf_energy", C.c_int, [dp, C.c_uint32, C.POINTER(Hamiltonian), C.c_int32, C.c_uint32, C.c_int32, dp]),
+    ("vqf_energy_ex", C.c_int, [dp, C.c_uint32, C.POINTER(Hamiltonian), C.c_int32, C.c_uint32, C.c_int32, C.c_int32,
+                                dp]),
     ("vqf_gradient", C.c_int, [dp, C.c_uint32, C.POINTER(Hamiltonian), C.c_int32, C.c_uint32, C.c_int32, C.c_int32,
                                dp]),
     ("vqf_run_vqe", C.c_int, [C.POINTER(Hamiltonian), C.c_int32, C.c_uint32, C.POINTER(AdamConfig), dp, C.c_uint32,
                               C.c_int32, C.c_int32, C.POINTER(VqeResult)]),
+    ("vqf_gradient_ex", C.c_int, [dp, C.c_uint32, C.POINTER(Hamiltonian), C.c_int32, C.c_uint32, C.c_int32, C.c_int32,
+                                  C.c_int32, dp]),
+    ("vqf_run_vqe_ex", C.c_int, [C.POINTER(Hamiltonian), C.c_int32, C.c_uint32, C.POINTER(AdamConfig), dp, C.c_uint32,
+                                 C.c_int32, C.c_int32, C.c_int32, C.POINTER(VqeResult)]),
     ("vqf_run_vqe_batch", C.c_int, [C.POINTER(Hamiltonian), C.c_uint32, C.c_int32, C.c_uint32,
                                     C.POINTER(AdamConfig), C.c_int32, C.POINTER(VqeResult)]),
     ("vqf_run_sweep", C.c_int, [C.POINTER(SweepConfig), C.POINTER(SweepReport)]),

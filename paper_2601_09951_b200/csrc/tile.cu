@@ -1,25 +1,42 @@
-// Gate fusion through shared-memory tiles.
+// Gate fusion through shared-memory tiles, gates applied in registers.
 //
 // A pass works on "gathered tiles": 2^B contiguous low-index amplitudes
-// (512 B runs) times 2^k chosen high index bits h_0..h_{k-1} (B + k = 11
-// local bits for fp64, 32 KB).  Runs arrive by TMA tensor loads with the
-// 128 B swizzle; three consumer groups per CTA each own a two-stage ring and
-// a named barrier.  Every gate of the pass whose wires map into the local
-// bits is merged into fused ops of <= 3 bits (4 with a DoubleExcitation);
-// each op is one real 2^m x 2^m matrix composed per CTA and applied to the
-// thread's amplitudes in registers (fp64 3-bit ops on the FP64 tensor cores,
-// mma.sync m8n8k4).  X / CNOT-only passes are an affine map of the local
-// index applied in the write-back.  One HBM read + write of the state per
-// pass instead of per gate.
+// (512 B runs) times 2^k chosen high index bits h_0..h_{k-1}, LB = B + k
+// local bits (fp64: LB = 11, 32 KB; fp32: LB = 12, 32 KB).  Runs arrive by
+// TMA tensor loads (128 B swizzle, completion on an mbarrier) and leave by
+// TMA tensor stores (cp.async.bulk.tensor shared -> global): one HBM read and
+// one write of the state per pass, whatever the number of gates in it.
+//
+// Inside a tile the pass's gates run as a sequence of PHASES.  In a phase
+// every thread of the consumer group holds 2^R amplitudes in registers
+// (R = 4 for fp64, 5 for fp32): the amplitudes whose local index differs in
+// the phase's R register bits.  Rotations (RY / SingleExcitation /
+// DoubleExcitation, statevector.hpp:156-200) run on those registers as a
+// branch-free sequence of STEPS: a SingleExcitation on register slots (0, 1),
+// a DoubleExcitation on slots 0..3, then one RY on every slot, each with its
+// (cos, sin) from a per-CTA table whose entry 0 is the identity (1, 0); the
+// host puts the excitations' wires on those fixed slots.  The register code
+// is therefore static: no per-gate dispatch, no register shuffling.
+//
+// Permutation gates (X, CNOT) never move data inside a tile: they are
+// affine maps over GF(2) of the local index, composed on the host into the
+// FRAME F of the tile (logical amplitude L sits at shared-memory slot
+// swz(F(L))).  A phase loads and stores its registers through F (in place);
+// the last phase stores through the map that leaves the tile in plain order
+// for the TMA store.  Between phases the tile goes through shared memory once
+// (one group barrier).  The host chooses each phase's register bits (the
+// rotations it can take in dependency order) and its thread bits so that the
+// lanes of one shared-memory wavefront hit distinct bank groups.
+//
+// Passes of X / CNOT only are an affine map of the local index applied in
+// the write-back (no register phases).
 //
 // The host scheduler walks the circuit's dependency DAG (gates sharing a wire
 // keep their order; gates on disjoint wires commute) and, among ready gates
 // that fit, takes the one adding the fewest new high bits (then sharing the
-// most): for the hardware-efficient ansatz the CNOT chain advances five
-// wires per pass.
-//
-// Composed matrices (and FMA / MMA accumulation) change rounding only:
-// amplitudes agree with the per-gate kernels to ~1e-16 (tests/).
+// most): for the hardware-efficient ansatz the CNOT chain advances five wires
+// per pass.  Reordering commuting rotations changes rounding only (~1e-16;
+// tests/ compare with the reference at 1e-12).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,74 +49,26 @@ namespace vqf {
 
 namespace {
 
-constexpr int kMaxOps = 64;        // TileParams stays under the 4 KB kernel-parameter limit
-constexpr int kMaxHigh = 6;
-constexpr int kTileBlocks = 148;   // persistent: one CTA per SM
-// four single-buffered consumer groups (128 KB of tiles): a group loads its
-// next tile after writing back the current one while the other three
-// compute; measured against 3 groups x 2 stages (the previous default, 192
-// KB), 5 x 1 and 6 x 1 (scripts/ab_variants.sh: HEA(2) n = 30 80.5 vs 84.2,
-// 89.2, 121.5 ms)
+constexpr int kMaxRot = 72;     // (cos, sin) entries per launch (kernel parameters stay < 4 KB)
+constexpr int kMaxSteps = 56;   // register steps per launch
+constexpr int kMaxPhases = 12;  // register phases per launch
+constexpr size_t kPhaseRot = 20;  // rotations per phase (bounds its steps and table entries)
+constexpr int kMaxHigh = 7;
+constexpr int kTileBlocks = 148;  // persistent: one CTA per SM
 #ifndef VQF_TILE_GROUPS
-#define VQF_TILE_GROUPS 4
+#define VQF_TILE_GROUPS 4  // independent consumer groups per CTA (128 threads each)
 #endif
 #ifndef VQF_TILE_STAGES
-#define VQF_TILE_STAGES 1
+#define VQF_TILE_STAGES 1  // tile buffers per group
 #endif
 #ifndef VQF_TILE_LB
 #define VQF_TILE_LB 11  // fp64 tile = 2^11 amplitudes (32 KB); fp32 one bit more
 #endif
-#ifndef VQF_TILE_NT
-#define VQF_TILE_NT 128
-#endif
-constexpr int kGroups = VQF_TILE_GROUPS;  // consumer groups per CTA
-constexpr int kNT = VQF_TILE_NT;          // threads per group (half of it for 4-bit fused ops in fp64)
-constexpr int kStages = VQF_TILE_STAGES;  // TMA ring depth per group (32 KB tiles)
-constexpr int kMaxFuse = 4;        // local bits of one fused op (16 amplitudes per thread)
-constexpr uint32_t kMatElems = 2560;
-constexpr int kDq = 4;  // item groups per step of the tensor-core fused op
-constexpr uint32_t kNoMma = 1u << 31;  // TileFop::ipos: run this op on the FMA path  // composed fused-op matrices per pass (20 KB of fp64)
-// fp64 passes run 512 threads with fused ops of <= 3 bits (8 amplitudes in
-// registers, <= 128 registers), or 256 threads when a DoubleExcitation needs
-// a 4-bit op; fp32 always 512 threads x <= 4 bits
-
-// One gate inside a fused op: pairs (r | A, r | B) of the op's 2^m register
-// slots, for every r with the bits of A | B clear; ROT: a' = c a - s b,
-// b' = s a + c b (statevector.hpp:160-163, :195-196), else swap.
-//   X / RY on slot bit j : A = 0,        B = 1 << j
-//   CNOT (c, t)          : A = C,        B = C | T
-//   SingleExcitation     : A = 1 << w0,  B = 1 << w1
-//   DoubleExcitation     : A = w0 | w1,  B = w2 | w3
-struct TileSub {
-  uint32_t code;  // (rot << 8) | (A << 4) | B
-  int32_t param;  // per-entry (c, s) index or -1
-  double c, s;
-};
-
-// A fused op: m <= 4 local bit positions (ascending, 8 bits each) and its
-// gates [sub0, sub0 + n_sub).  Each thread loads the 2^m amplitudes of one
-// work item into registers, applies all the gates, and stores them back:
-// one shared-memory round trip per op instead of per gate.
-struct TileFop {
-  uint32_t m, pos, sub0, n_sub, uoff;  // uoff: the op's matrix in the composed-matrix area
-  // tensor-core ops: the two free local bits that enumerate the four items of
-  // an MMA column group (chosen on the host against shared-memory bank
-  // conflicts; 0 = the lowest free bits), 5 bits each
-  uint32_t ipos;
-};
-
-struct TileParams {
-  uint32_t n, B, k, n_fops, batch;
-  uint32_t hb[kMaxHigh];  // global bit of local bit B + j, ascending
-  const double* cs;
-  // Permutation-only pass (every gate X / CNOT): no fused ops; the tile is
-  // written back as out[L] = in[F(L)] with F(L) = c ^ xor of col[b] over
-  // the set bits b of L (an affine map over GF(2) on the local index).
-  uint32_t perm_only, perm_c;
-  uint32_t perm_col[16];
-  TileFop fops[kMaxOps];
-  TileSub subs[kMaxOps];
-};
+constexpr int kGroups = VQF_TILE_GROUPS;
+constexpr int kStages = VQF_TILE_STAGES;
+constexpr int kLB64 = VQF_TILE_LB, kLB32 = VQF_TILE_LB + 1;
+constexpr int kR64 = 4, kR32 = 5;  // register bits per phase (16 / 32 amplitudes per thread)
+constexpr int kB = 5;              // run = 2^5 amplitudes: 512 B fp64 (one TMA box of 4 x 128 B rows)
 
 template <typename T>
 struct V2;
@@ -112,12 +81,91 @@ struct V2<float> {
   using type = float2;
 };
 
+// ------------------------------------------------------- register steps
+// One step over the thread's 2^R register slots x[r], applied in this order:
+//   SingleExcitation: pairs (r|1, r|2) for r with slot bits 0, 1 clear
+//   DoubleExcitation: pairs (r|3, r|12) for r with slot bits 0..3 clear
+//   RY on slot j = 0..R-1: pairs (r, r|2^j) for r with slot bit j clear
+// each a Givens rotation a' = c a - s b, b' = s a + c b on the pair (a, b)
+// (statevector.hpp:160-163, :195-196) with (c, s) from the CTA's table;
+// index 0 = (1, 0) = identity.
+struct TileStep {
+  int16_t se, de;  // table indices of the excitations (0: none)
+  int16_t ry[5];   // per slot (0: none)
+  uint16_t flags;  // bit 0: has SingleExcitation, bit 1: has DoubleExcitation
+};
+
+template <typename P, typename T>
+__device__ __forceinline__ void givens(P& a, P& b, T c, T s) {
+  const P u = a, v = b;
+  a.x = fma(c, u.x, -s * v.x);
+  a.y = fma(c, u.y, -s * v.y);
+  b.x = fma(s, u.x, c * v.x);
+  b.y = fma(s, u.y, c * v.y);
+}
+
+template <int R, typename P, typename T>
+__device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, const double2* rcs) {
+  constexpr int NR = 1 << R;
+  if (st.flags & 1u) {
+    const double2 v = rcs[st.se];
+#pragma unroll
+    for (int r = 0; r < NR; r += 4) givens(x[r | 1], x[r | 2], static_cast<T>(v.x), static_cast<T>(v.y));
+  }
+  if (st.flags & 2u) {
+    const double2 v = rcs[st.de];
+#pragma unroll
+    for (int r = 0; r < NR; r += 16) givens(x[r | 3], x[r | 12], static_cast<T>(v.x), static_cast<T>(v.y));
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const double2 v = rcs[st.ry[j]];
+    const T c = static_cast<T>(v.x), sn = static_cast<T>(v.y);
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      if (!(r & (1 << j))) givens(x[r], x[r | (1 << j)], c, sn);
+  }
+}
+
+// ------------------------------------------------------------ parameters
+// One register phase: steps [step0, step0 + n_steps).  Thread bit j of the
+// group's thread index selects the shared-memory slot offset ld_tb[j],
+// register slot bit j the offset ld_r[j], and ld_c is the constant part: the
+// swizzled images of the frame's affine map are xor-linear, so an
+// amplitude's slot is ld_c ^ (xor of its bits' offsets).  Stores use the st_*
+// offsets (equal to the loads' except when the phase re-lays the tile out).
+struct TilePhase {
+  uint16_t step0, n_steps;
+  uint16_t ld_c, st_c;
+  uint16_t ld_tb[9], ld_r[5];
+  uint16_t st_tb[9], st_r[5];
+  uint16_t relayout;
+};
+
+struct TileParams {
+  uint32_t n, B, k, batch, n_phases;
+  uint32_t hb[kMaxHigh];  // global bit of local bit B + j, ascending
+  const double* cs;       // per-entry (cos, sin) table: cs[2 (param * batch + entry)]
+  // Permutation-only pass (every gate X / CNOT): the tile is written back as
+  // out[L] = in[F(L)] with F(L) = c ^ xor of col[b] over the set bits b of L
+  // (an affine map over GF(2) on the local index).
+  uint32_t perm_only, perm_c;
+  uint32_t perm_col[16];
+  uint32_t n_rot;              // (cos, sin) table entries; entry 0 = (1, 0)
+  int32_t rot_param[kMaxRot];  // >= 0: per-entry table row; < 0: (rot_c, rot_s)
+  double rot_c[kMaxRot], rot_s[kMaxRot];
+  uint8_t rot_neg[kMaxRot];    // 1: negated angle (an excitation with its pair roles swapped)
+  TilePhase ph[kMaxPhases];
+  TileStep steps[kMaxSteps];
+};
+static_assert(sizeof(TileParams) <= 4096, "kernel parameter limit");
+
 __device__ __forceinline__ uint64_t insert_zero64(uint64_t k, uint32_t bit) {
   const uint64_t low = k & ((uint64_t{1} << bit) - 1);
   return ((k >> bit) << (bit + 1)) | low;
 }
 
-// ---- TMA helpers (sm_90+ PTX; SASS: UTMALDG / SYNCS)
+// ---- TMA / mbarrier helpers (SASS: UTMALDG / UTMASTG / SYNCS)
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -138,8 +186,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// one 4 KB run (box {128 B, 32 rows, 1}) of the state, 128 B-swizzled into
-// shared memory; completion counted on the mbarrier
+// one run (box {128 B, rows, 1}) of the state, 128 B-swizzled into shared
+// memory; completion counted on the mbarrier
 __device__ __forceinline__ void tma_load_run(void* dst, const CUtensorMap* map, int32_t row, int32_t entry,
                                              uint64_t* bar) {
   asm volatile(
@@ -148,15 +196,24 @@ __device__ __forceinline__ void tma_load_run(void* dst, const CUtensorMap* map, 
       "l"(map), "r"(0), "r"(row), "r"(entry), "r"(smem_addr(bar))
       : "memory");
 }
+// the reverse: one run from shared memory (un-swizzled by the map) to HBM
+__device__ __forceinline__ void tma_store_run(const void* src, const CUtensorMap* map, int32_t row, int32_t entry) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(0),
+               "r"(row), "r"(entry), "r"(smem_addr(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Shared-memory slot of local amplitude L under the TMA 128 B swizzle: the
 // 16-byte chunk index (bits 4..6 of the byte offset) is xor-ed with the
-// 128-byte row index mod 8 (bits 7..9), so amplitudes one row apart land in
-// different banks.
+// 128-byte row index mod 8 (bits 7..9).  Linear over GF(2).
 template <typename T>
-__device__ __forceinline__ uint32_t swz(uint32_t L) {
-  if (sizeof(T) == 8) return L ^ ((L >> 3) & 7u);        // 16 B amplitude = one chunk
-  return L ^ (((L >> 4) & 7u) << 1);                     // 8 B amplitude: chunk = L >> 1
+__host__ __device__ __forceinline__ uint32_t swz(uint32_t L) {
+  if (sizeof(T) == 8) return L ^ ((L >> 3) & 7u);   // 16 B amplitude = one chunk
+  return L ^ (((L >> 4) & 7u) << 1);                 // 8 B amplitude: chunk = L >> 1
 }
 
 // Global start index of run j (0 <= j < 2^k) of tile `tile`.
@@ -167,289 +224,88 @@ __device__ __forceinline__ uint64_t run_start(const TileParams& p, uint64_t tile
   return base;
 }
 
-// Every gate here is a real orthogonal map on its pairs, so a fused op is
-// one real 2^m x 2^m matrix U (row-major, in shared memory) composed once
-// per CTA from its gates and the CTA's batch entry angles: start from the
-// identity and apply each gate to the rows of every column.  The angles are
-// staged in shared memory first (one parallel round of global loads instead
-// of a dependent L2 round trip per gate) and each thread composes one
-// (op, column) pair, so the serial chain is one op's gates: batched states
-// launch a CTA set per entry and pay this once per (CTA, entry).
-template <typename T>
-__device__ void compose_fops(const TileParams& p, T* U) {
-  __shared__ double2 sc[kMaxOps];
-  uint32_t n_subs = 0;
-  for (uint32_t o = 0; o < p.n_fops; ++o) n_subs = max(n_subs, p.fops[o].sub0 + p.fops[o].n_sub);
-  for (uint32_t q = threadIdx.x; q < n_subs; q += blockDim.x) {
-    const TileSub& g = p.subs[q];
-    double2 v = make_double2(g.c, g.s);
-    if (g.param >= 0) v = *reinterpret_cast<const double2*>(p.cs + 2 * ((size_t)g.param * p.batch + blockIdx.y));
-    sc[q] = v;
-  }
-  __syncthreads();
-  for (uint32_t w = threadIdx.x;; w += blockDim.x) {
-    uint32_t o = 0, col = w;
-    while (o < p.n_fops && col >= (1u << p.fops[o].m)) col -= 1u << p.fops[o].m, ++o;
-    if (o >= p.n_fops) break;
-    const TileFop& f = p.fops[o];
-    const uint32_t d = 1u << f.m;
-    T* u = U + f.uoff;
-    for (uint32_t r = 0; r < d; ++r) u[r * d + col] = r == col ? T(1) : T(0);
-    for (uint32_t q = 0; q < f.n_sub; ++q) {
-      const TileSub& g = p.subs[f.sub0 + q];
-      const double c = sc[f.sub0 + q].x, sn = sc[f.sub0 + q].y;
-      const uint32_t A = (g.code >> 4) & 15u, B = g.code & 15u, S = A | B;
-      for (uint32_t r = 0; r < d; ++r) {
-        if (r & S) continue;
-        const T x = u[(r | A) * d + col], y = u[(r | B) * d + col];
-        if (g.code >> 8) {  // a' = c a - s b, b' = s a + c b (statevector.hpp:160-163, :195-196)
-          u[(r | A) * d + col] = static_cast<T>(c) * x - static_cast<T>(sn) * y;
-          u[(r | B) * d + col] = static_cast<T>(sn) * x + static_cast<T>(c) * y;
-        } else {
-          u[(r | A) * d + col] = y;
-          u[(r | B) * d + col] = x;
-        }
-      }
-    }
-  }
-}
-
-// One fused op over the whole tile: work item w -> base with zeros at the
-// op's bits; 2^M amplitudes in registers, y = U x with U broadcast from
-// shared memory.  The swizzle is xor-linear and base / slot offsets have
-// disjoint bits, so slot addresses are swz(base) ^ swz(offset).
-template <int M, typename T, int NT>
-__device__ __forceinline__ void run_fop(typename V2<T>::type* t, uint32_t NL, const TileFop& f, const T* U,
-                                        uint32_t gt) {
-  using A = typename V2<T>::type;
-  constexpr int D = 1 << M;
-  uint32_t pos[M];
-#pragma unroll
-  for (int j = 0; j < M; ++j) pos[j] = (f.pos >> (8 * j)) & 0xffu;
-  uint32_t sd[D];
-#pragma unroll
-  for (int r = 0; r < D; ++r) {
-    uint32_t d = 0;
-#pragma unroll
-    for (int j = 0; j < M; ++j)
-      if (r & (1 << j)) d |= 1u << pos[j];
-    sd[r] = swz<T>(d);
-  }
-  const T* u = U + f.uoff;
-  const uint32_t items = NL >> M;
-  const auto base_of = [&](uint32_t w) {
-    uint32_t base = w;
-#pragma unroll
-    for (int j = 0; j < M; ++j) base = ((base >> pos[j]) << (pos[j] + 1)) | (base & ((1u << pos[j]) - 1));
-    return swz<T>(base);
-  };
-  using P2 = typename V2<T>::type;
-  if constexpr (M == 3 && sizeof(T) == 8) {
-    if (f.ipos != kNoMma && items >= 4 * NT / 32 * kDq) {
-      // fp64 tensor cores: Y (8 slots x 2 columns per item) = U (8 x 8) X as
-      // mma.sync m8n8k4 f64 over groups of four items (eight real columns:
-      // item-major, re / im).  Fragments (PTX m8n8k4 .f64, g = lane / 4,
-      // t = lane % 4): A[g][t] -> U[g][k0 + t]; B[t][g] -> X[k0 + t][col g] =
-      // component (g & 1) of slot k0 + t of item g / 2; D[g][2t + i] ->
-      // component i of slot g of item t.  One warp instruction does 256
-      // FMAs; kDq item groups per step keep loads and MMAs in flight.
-      const uint32_t lane = gt & 31u, g = lane >> 2, tq = lane & 3u;
-      const double a_lo = u[g * 8 + tq], a_hi = u[g * 8 + 4 + tq];
-      const double* td = reinterpret_cast<const double*>(t);
-      // item 4q + i = base(4q) | base(i) for i < 4 (disjoint bits) and the
-      // swizzle is xor-linear, so the per-lane parts are fixed per op and
-      // each item group costs one (warp-uniform) base computation
-      // item 4q + i: i on the two chosen free bits c1, c2, q on the other
-      // free bits (ascending): base = ins2(q) | dep2(i), both swizzled apart
-      const uint32_t c1 = f.ipos & 31u, c2 = (f.ipos >> 5) & 31u;
-      const auto dep2 = [&](uint32_t i) { return swz<T>(((i & 1u) << c1) | (((i >> 1) & 1u) << c2)); };
-      uint32_t p5[M + 2];  // zero-insertion positions for q: op bits + c1, c2, ascending
-      {
-        uint32_t all[M + 2];
-#pragma unroll
-        for (int j = 0; j < M; ++j) all[j] = pos[j];
-        all[M] = c1;
-        all[M + 1] = c2;
-#pragma unroll
-        for (int i = 0; i < M + 2; ++i)
-#pragma unroll
-          for (int j = i + 1; j < M + 2; ++j)
-            if (all[j] < all[i]) {
-              const uint32_t tmp = all[i];
-              all[i] = all[j];
-              all[j] = tmp;
-            }
-#pragma unroll
-        for (int j = 0; j < M + 2; ++j) p5[j] = all[j];
-      }
-      const auto ins2 = [&](uint32_t q) {
-        uint32_t b = q;
-#pragma unroll
-        for (int j = 0; j < M + 2; ++j) b = ((b >> p5[j]) << (p5[j] + 1)) | (b & ((1u << p5[j]) - 1));
-        return swz<T>(b);
-      };
-      const uint32_t in_lo = 2 * (dep2(g >> 1) ^ sd[tq]) + (g & 1u);
-      const uint32_t in_hi = 2 * (dep2(g >> 1) ^ sd[4 + tq]) + (g & 1u);
-      const uint32_t out_off = dep2(tq) ^ sd[g];
-      const uint32_t groups = items >> 2, wstride = NT / 32;
-      // groups q0 + d (q0 a multiple of kDq): base(4 (q0 + d)) =
-      // base(4 q0) | base(4 d), so one base per step plus fixed offsets
-      uint32_t offd[kDq];
-#pragma unroll
-      for (int d = 0; d < kDq; ++d) offd[d] = ins2(d);
-      for (uint32_t q0 = (gt >> 5) * kDq; q0 < groups; q0 += wstride * kDq) {
-        double b_lo[kDq], b_hi[kDq], c0[kDq], c1[kDq];
-        uint32_t sb_out[kDq];
-        const uint32_t sbq = ins2(q0);
-#pragma unroll
-        for (int d = 0; d < kDq; ++d) {
-          const uint32_t sb4 = sbq ^ offd[d];
-          sb_out[d] = sb4 ^ out_off;
-          b_lo[d] = td[(2 * sb4) ^ in_lo];
-          b_hi[d] = td[(2 * sb4) ^ in_hi];
-          c0[d] = 0.0;
-          c1[d] = 0.0;
-        }
-#pragma unroll
-        for (int d = 0; d < kDq; ++d)
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                       : "+d"(c0[d]), "+d"(c1[d])
-                       : "d"(a_lo), "d"(b_lo[d]));
-#pragma unroll
-        for (int d = 0; d < kDq; ++d)
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                       : "+d"(c0[d]), "+d"(c1[d])
-                       : "d"(a_hi), "d"(b_hi[d]));
-#pragma unroll
-        for (int d = 0; d < kDq; ++d) {
-          A y;
-          y.x = c0[d];
-          y.y = c1[d];
-          t[sb_out[d]] = y;
-        }
-      }
-      return;
-    }
-  }
-  if constexpr (M <= 3) {
-    // two work items per step: both items' loads in flight together and each
-    // 16-byte matrix-row load feeds both (the tile has 2 x NT items for m = 3)
-    for (uint32_t w = gt; w < items; w += 2 * NT) {
-      const bool two = w + NT < items;
-      const uint32_t sb0 = base_of(w), sb1 = two ? base_of(w + NT) : sb0;
-      A x0[D], x1[D];
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        x0[r] = t[sb0 ^ sd[r]];
-        x1[r] = t[sb1 ^ sd[r]];
-      }
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        A a0, a1, b0, b1;  // item 0 / item 1, even / odd columns
-        a0.x = a0.y = a1.x = a1.y = b0.x = b0.y = b1.x = b1.y = T(0);
-        if constexpr (D == 1) {
-          a0.x = u[0] * x0[0].x;
-          a0.y = u[0] * x0[0].y;
-          b0.x = u[0] * x1[0].x;
-          b0.y = u[0] * x1[0].y;
-        } else {
-          const P2* row = reinterpret_cast<const P2*>(u + r * D);
-#pragma unroll
-          for (int c = 0; c < D; c += 2) {
-            const P2 m = row[c / 2];
-            a0.x = fma(m.x, x0[c].x, a0.x);
-            a0.y = fma(m.x, x0[c].y, a0.y);
-            a1.x = fma(m.y, x0[c + 1].x, a1.x);
-            a1.y = fma(m.y, x0[c + 1].y, a1.y);
-            b0.x = fma(m.x, x1[c].x, b0.x);
-            b0.y = fma(m.x, x1[c].y, b0.y);
-            b1.x = fma(m.y, x1[c + 1].x, b1.x);
-            b1.y = fma(m.y, x1[c + 1].y, b1.y);
-          }
-        }
-        A y0, y1;
-        y0.x = a0.x + a1.x;
-        y0.y = a0.y + a1.y;
-        y1.x = b0.x + b1.x;
-        y1.y = b0.y + b1.y;
-        t[sb0 ^ sd[r]] = y0;
-        if (two) t[sb1 ^ sd[r]] = y1;
-      }
-    }
-  } else {
-    for (uint32_t w = gt; w < items; w += NT) {
-      const uint32_t sb = base_of(w);
-      A x[D];
-#pragma unroll
-      for (int r = 0; r < D; ++r) x[r] = t[sb ^ sd[r]];
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        // row r of U as 16-byte broadcast loads; two accumulation chains per
-        // component (even / odd columns) halve the dependent-FMA depth
-        A y0, y1;
-        y0.x = y0.y = y1.x = y1.y = T(0);
-        const P2* row = reinterpret_cast<const P2*>(u + r * D);
-#pragma unroll
-        for (int c = 0; c < D; c += 2) {
-          const P2 m = row[c / 2];
-          y0.x = fma(m.x, x[c].x, y0.x);
-          y0.y = fma(m.x, x[c].y, y0.y);
-          y1.x = fma(m.y, x[c + 1].x, y1.x);
-          y1.y = fma(m.y, x[c + 1].y, y1.y);
-        }
-        A y;
-        y.x = y0.x + y1.x;
-        y.y = y0.y + y1.y;
-        t[sb ^ sd[r]] = y;
-      }
-    }
-  }
-}
-
-// Named barrier over the NT threads of one consumer group (ids 1, 2; 0 is
+// Named barrier over the NT threads of one consumer group (id 0 is
 // __syncthreads).
 template <int NT>
 __device__ __forceinline__ void group_sync(uint32_t group) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(NT) : "memory");
 }
 
-// Persistent tile kernel.  The CTA runs two independent consumer groups of
-// NT threads; group g takes every other tile of the CTA's sequence, with its
-// own kStages-deep TMA ring (lane 0 of the group's first warp arms the
-// stage's mbarrier with the tile's bytes, its lanes issue the 2^k runs as
-// TMA tensor loads, 128 B swizzle) and its own named barrier, so one group's
-// barrier waits and shared-memory phases overlap the other group's work.
-// Each tile: the pass's fused ops (y = U x on 2^m amplitudes per thread),
-// then coalesced 16-byte stores back to HBM.
-template <typename T, int NT, int MAXM, bool PERM>
-__global__ void __launch_bounds__(kGroups * NT, 1)
-    k_tile(typename V2<T>::type* __restrict__ a, const __grid_constant__ CUtensorMap map, const TileParams p) {
+// One register phase on the tile t: load the thread's 2^R amplitudes through
+// the frame, run the phase's steps in registers, store them back.
+template <typename T, int R, int LB, int NT>
+__device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePhase& ph, const TileStep* steps,
+                                          const double2* rcs, uint32_t gt, uint32_t group) {
   using A = typename V2<T>::type;
+  constexpr int NR = 1 << R;
+  const auto slots = [&](const uint16_t* tb, const uint16_t* rv, uint32_t c, uint32_t (&off)[NR]) {
+    uint32_t base = c;
+#pragma unroll
+    for (int j = 0; j < LB - R; ++j)
+      if ((gt >> j) & 1u) base ^= tb[j];
+    uint32_t r_off[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) r_off[j] = rv[j];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      uint32_t o = base;
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (r & (1 << j)) o ^= r_off[j];
+      off[r] = o;
+    }
+  };
+  uint32_t off[NR];
+  slots(ph.ld_tb, ph.ld_r, ph.ld_c, off);
+  A x[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) x[r] = t[off[r]];
+  if (ph.relayout) {
+    group_sync<NT>(group);  // every slot read before any is overwritten
+    slots(ph.st_tb, ph.st_r, ph.st_c, off);
+  }
+  const uint32_t n_steps = ph.n_steps, step0 = ph.step0;
+  for (uint32_t q = 0; q < n_steps; ++q) run_step<R, A, T>(x, steps[step0 + q], rcs);
+#pragma unroll
+  for (int r = 0; r < NR; ++r) t[off[r]] = x[r];
+}
+
+// Persistent tile kernel: G consumer groups of NT = 2^(LB - R) threads, each
+// with S tile buffers; group g takes every G-th tile of the CTA's sequence.
+// Per tile: wait for its TMA loads, run the register phases (a group barrier
+// after each), then the group's first warp issues the TMA stores of the
+// runs, waits until they have read the buffer and refills it with the
+// group's tile S steps ahead.  Permutation passes write back with 16-byte
+// stores through the affine index map instead.
+template <typename T, int R, int LB, bool PERM>
+__global__ void __launch_bounds__(kGroups << (LB - R), 1)
+    k_tile(typename V2<T>::type* __restrict__ a, const __grid_constant__ CUtensorMap map,
+           const __grid_constant__ TileParams p) {
+  using A = typename V2<T>::type;
+  constexpr uint32_t NT = 1u << (LB - R), NL = 1u << LB;
+  constexpr uint32_t tile_bytes = NL * sizeof(A);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 128 B swizzle atoms are 1024 B: align the rings (the launch adds 1 KB
-  // slack); indexing smem_raw keeps the pointer in the shared window (LDS/STS)
+  // slack); indexing smem_raw keeps the pointer in the shared window
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-  const uint32_t LB = p.B + p.k, NL = 1u << LB;
   const uint32_t run_amps = 1u << p.B, n_runs = 1u << p.k;
-  const uint32_t tile_bytes = NL * sizeof(A), run_bytes = run_amps * sizeof(A);
-  const uint32_t amps_per_row = 128 / sizeof(A);
+  const uint32_t run_bytes = run_amps * sizeof(A);
+  constexpr uint32_t amps_per_row = 128 / sizeof(A);
   const uint32_t group = threadIdx.x / NT, gt = threadIdx.x % NT;
   unsigned char* ring = smem + (size_t)group * kStages * tile_bytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kGroups * kStages * (size_t)tile_bytes) + group * kStages;
-  T* U = reinterpret_cast<T*>(smem + kGroups * kStages * (size_t)tile_bytes + 256);  // composed fused-op matrices
-  __shared__ uint64_t run_off_all[kGroups][1 << kMaxHigh];
-  uint64_t* run_off = run_off_all[group];
+  __shared__ double2 rcs[kMaxRot];
+  __shared__ uint16_t ftab[PERM ? 2 : 1][64];
+  __shared__ uint64_t run_off_all[PERM ? kGroups : 1][PERM ? (1 << kMaxHigh) : 1];
+  const int32_t entry = static_cast<int32_t>(blockIdx.y);
   A* s = a + ((uint64_t)blockIdx.y << p.n);
-  const uint64_t n_tiles = uint64_t{1} << (p.n - LB);
+  const uint64_t n_tiles = uint64_t{1} << (p.n - p.B - p.k);
   if (gt == 0) {
     if (group == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
     for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if constexpr (!PERM) compose_fops<T>(p, U);
-  // permutation-only pass: F as two 64-entry tables (bits 0-5, bits 6-11)
-  __shared__ uint16_t ftab[PERM ? 2 : 1][64];
-  if constexpr (PERM)
+  if constexpr (PERM) {
     for (uint32_t e = threadIdx.x; e < 128; e += blockDim.x) {
       const uint32_t half = e >> 6, j = e & 63u;
       uint32_t v = 0;
@@ -457,6 +313,17 @@ __global__ void __launch_bounds__(kGroups * NT, 1)
         if ((j >> b) & 1u) v ^= p.perm_col[6 * half + b];
       ftab[half][j] = static_cast<uint16_t>(v);
     }
+  } else {
+    // the pass's rotation angles for this batch entry, one parallel round of
+    // loads
+    for (uint32_t q = threadIdx.x; q < p.n_rot; q += blockDim.x) {
+      double2 v = make_double2(p.rot_c[q], p.rot_s[q]);
+      if (p.rot_param[q] >= 0)
+        v = *reinterpret_cast<const double2*>(p.cs + 2 * ((size_t)p.rot_param[q] * p.batch + blockIdx.y));
+      if (p.rot_neg[q]) v.y = -v.y;
+      rcs[q] = v;
+    }
+  }
   __syncthreads();
   const auto stage_buf = [&](int st) { return reinterpret_cast<A*>(ring + (size_t)st * tile_bytes); };
   const auto issue_load = [&](uint64_t tile, int st) {
@@ -464,54 +331,55 @@ __global__ void __launch_bounds__(kGroups * NT, 1)
     if (lane == 0) mbar_expect_tx(&bar[st], tile_bytes);
     unsigned char* dst = reinterpret_cast<unsigned char*>(stage_buf(st));
     for (uint32_t j = lane; j < n_runs; j += 32)
-      tma_load_run(dst + (size_t)j * run_bytes, &map, static_cast<int32_t>(run_start(p, tile, j) / amps_per_row),
-                   static_cast<int32_t>(blockIdx.y), &bar[st]);
+      tma_load_run(dst + (size_t)j * run_bytes, &map, static_cast<int32_t>(run_start(p, tile, j) / amps_per_row), entry,
+                   &bar[st]);
   };
   // the group's tiles: blockIdx.x + (kGroups i + group) * gridDim.x
   const uint64_t step = kGroups * (uint64_t)gridDim.x;
   const uint64_t first = blockIdx.x + (uint64_t)group * gridDim.x;
   if (gt < 32)
-    for (int st = 0; st < kStages - 1; ++st) {
+    for (int st = 0; st < kStages; ++st) {
       const uint64_t t0 = first + (uint64_t)st * step;
       if (t0 < n_tiles) issue_load(t0, st);
     }
   uint64_t tile = first;
   for (uint32_t it = 0; tile < n_tiles; tile += step, ++it) {
     const int cur = it % kStages;
-    const uint64_t ahead = tile + (uint64_t)(kStages - 1) * step;
-    // that stage's previous tile was written back before the group barrier
-    // that closed the previous iteration
-    if (gt < 32 && ahead < n_tiles) issue_load(ahead, (it + kStages - 1) % kStages);
     mbar_wait(&bar[cur], (it / kStages) & 1u);
     A* t = stage_buf(cur);
-    for (uint32_t o = 0; o < (PERM ? 0u : p.n_fops); ++o) {
-      const TileFop f = p.fops[o];
-      switch (f.m) {
-        case 1: run_fop<1, T, NT>(t, NL, f, U, gt); break;
-        case 2: run_fop<2, T, NT>(t, NL, f, U, gt); break;
-        case 3: run_fop<3, T, NT>(t, NL, f, U, gt); break;
-        default:
-          if constexpr (MAXM >= 4) run_fop<4, T, NT>(t, NL, f, U, gt);
-          break;
-      }
-      group_sync<NT>(group);
-    }
-    // write-back: coalesced 16-byte stores, consecutive threads along a run
-    for (uint32_t j = gt; j < n_runs; j += NT) run_off[j] = run_start(p, tile, j);
-    group_sync<NT>(group);
-    const uint32_t low_mask = run_amps - 1;
     if constexpr (PERM) {
+      uint64_t* run_off = run_off_all[group];
+      for (uint32_t j = gt; j < n_runs; j += NT) run_off[j] = run_start(p, tile, j);
+      group_sync<NT>(group);
+      const uint32_t low_mask = run_amps - 1;
 #pragma unroll 4
       for (uint32_t li = gt; li < NL; li += NT) {
         const uint32_t src = p.perm_c ^ ftab[0][li & 63u] ^ ftab[1][li >> 6];
         s[run_off[li >> p.B] | (li & low_mask)] = t[swz<T>(src)];
       }
+      group_sync<NT>(group);  // buffer free for the next TMA load
     } else {
-#pragma unroll 4
-      for (uint32_t li = gt; li < NL; li += NT) s[run_off[li >> p.B] | (li & low_mask)] = t[swz<T>(li)];
+      for (uint32_t ph = 0; ph < p.n_phases; ++ph) {
+        run_phase<T, R, LB, NT>(t, p.ph[ph], p.steps, rcs, gt, group);
+        if (ph + 1 == p.n_phases) fence_proxy_async();  // generic-proxy stores -> TMA store reads
+        group_sync<NT>(group);
+      }
+      if (gt < 32) {
+        for (uint32_t j = gt; j < n_runs; j += 32)
+          tma_store_run(reinterpret_cast<unsigned char*>(t) + (size_t)j * run_bytes, &map,
+                        static_cast<int32_t>(run_start(p, tile, j) / amps_per_row), entry);
+        bulk_commit();
+      }
     }
-    group_sync<NT>(group);  // buffer free for the stage's next TMA load
+    const uint64_t ahead = tile + (uint64_t)kStages * step;
+    if (gt < 32) {
+      if constexpr (!PERM) bulk_wait_read();  // this lane's stores have read the buffer
+      __syncwarp();
+      if (ahead < n_tiles) issue_load(ahead, cur);
+    }
   }
+  if constexpr (!PERM)
+    if (gt < 32) bulk_wait_all();
 }
 
 // dst[e] = src for e < m (one read of the source, m writes): entries of a
@@ -524,18 +392,22 @@ __global__ void k_broadcast(const A* __restrict__ src, A* __restrict__ dst, uint
   }
 }
 
+// --------------------------------------------------------------- host side
 struct Pass {
   std::vector<uint32_t> hbits;  // ascending global bits
   std::vector<int> gates;
 };
 
-// Local bit budget: 64 KB of shared memory per tile (kStages tiles resident).
+int tile_lb(int32_t dtype) { return dtype == VQF_F64 ? kLB64 : kLB32; }
+int tile_r(int32_t dtype) { return dtype == VQF_F64 ? kR64 : kR32; }
+
+// Tile geometry: runs of 2^B amplitudes, up to kmax gathered high bits;
+// registers narrower than the full tile use one tile of their own width
+// (down to R + 5 local bits: one warp per consumer group).
 void tile_shape(uint32_t n, int32_t dtype, uint32_t& B, uint32_t& kmax) {
-  // 32 KB tiles (two groups x kStages per CTA) in runs of 512 B (one TMA box
-  // of 4 rows x 128 B): B = 5 (fp64) / 6 (fp32), leaving 6 gathered high bits
-  const uint32_t LB = dtype == VQF_F64 ? VQF_TILE_LB : VQF_TILE_LB + 1;
-  B = std::min<uint32_t>(n, LB - kMaxHigh);
-  kmax = std::min<uint32_t>(LB - B, n - B);
+  const uint32_t LB = std::min<uint32_t>(n, static_cast<uint32_t>(tile_lb(dtype)));
+  B = std::min<uint32_t>(n, kB);
+  kmax = LB - B;
 }
 
 std::vector<Pass> schedule(uint32_t n, uint32_t B, uint32_t kmax, const std::vector<TGate>& gates) {
@@ -567,7 +439,7 @@ std::vector<Pass> schedule(uint32_t n, uint32_t B, uint32_t kmax, const std::vec
     // high bits, then sharing the most bits with the pass, then the earliest
     // (keeps a CNOT chain advancing instead of letting independent RYs claim
     // the bit budget)
-    while (added && pass.gates.size() < static_cast<size_t>(kMaxOps)) {
+    while (added) {
       added = false;
       int best = -1, best_new = 1 << 20, best_share = -1;
       for (size_t i = 0; i < G; ++i) {
@@ -598,7 +470,7 @@ std::vector<Pass> schedule(uint32_t n, uint32_t B, uint32_t kmax, const std::vec
     }
     if (pass.gates.empty()) {
       // a gate with more high wires than the tile has room for: the driver
-      // runs it with the single-gate kernel (empty hbits marks that)
+      // runs it with the single-gate kernel (hbits = {~0} marks that)
       for (size_t i = 0; i < G; ++i) {
         if (done[i]) continue;
         bool ready = true;
@@ -640,7 +512,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // The state as a 3-d tensor {128 B row, rows, batch entry}; box = one run of
-// 2^B amplitudes (<= 32 rows), 128 B swizzle.
+// 2^B amplitudes (<= 32 rows), 128 B swizzle.  Loads and stores share it.
 CUtensorMap state_map(const vqf_statevector* sv, uint32_t run_bytes) {
   const bool f64 = sv->dtype == VQF_F64;
   const uint64_t amp = f64 ? 16 : 8;
@@ -657,9 +529,9 @@ CUtensorMap state_map(const vqf_statevector* sv, uint32_t run_bytes) {
   return m;
 }
 
-// Gate -> (local bits, code over those bits) for the fused-op merge.
+// Gate -> (local bits, pair pattern over those bits).
 struct LocalGate {
-  uint32_t bits;  // local bit mask
+  uint32_t bits;         // local bit mask
   uint32_t rot, ma, mb;  // pair patterns as local bit masks
   int32_t param;
   double c, s;
@@ -672,25 +544,15 @@ uint32_t compress(uint32_t mask, const uint32_t* pos, uint32_t m) {
   return out;
 }
 
-// Kernel parameters of one pass: the gates mapped to local bits and merged
-// into fused ops.
-// Gates [first, *next) of the pass go into this launch: the composed
-// matrices must fit kMatElems, otherwise the pass is split into several
-// launches over the same tiles.
-TileParams build_params(uint32_t n, uint32_t batch, uint32_t B, const std::vector<TGate>& gates, const Pass& pass,
-                        const double* cs_dev, uint32_t fuse_bits, size_t first, size_t* next) {
-  TileParams p{};
-  p.n = n;
-  p.B = B;
-  p.k = static_cast<uint32_t>(pass.hbits.size());
-  p.batch = batch;
-  p.cs = cs_dev;
-  for (uint32_t j = 0; j < p.k; ++j) p.hb[j] = pass.hbits[j];
+// The pass's gates mapped to local bits (local bit b < B: global bit b;
+// local bit B + j: global bit hb[j]).
+std::vector<LocalGate> local_gates(uint32_t n, uint32_t B, const std::vector<uint32_t>& hb,
+                                   const std::vector<TGate>& gates, const Pass& pass) {
   const auto local = [&](uint32_t wire) -> uint32_t {
     const uint32_t b = n - 1 - wire;
     if (b < B) return b;
-    for (uint32_t j = 0; j < p.k; ++j)
-      if (p.hb[j] == b) return B + j;
+    for (size_t j = 0; j < hb.size(); ++j)
+      if (hb[j] == b) return B + static_cast<uint32_t>(j);
     throw Error(VQF_LOGIC_ERROR, "tile scheduler: wire outside the pass");
   };
   std::vector<LocalGate> lg;
@@ -732,116 +594,357 @@ TileParams build_params(uint32_t n, uint32_t batch, uint32_t B, const std::vecto
     }
     lg.push_back(o);
   }
+  return lg;
+}
+
+// Affine map over GF(2) of the LB-bit local index: L -> c ^ (xor of col[b]
+// over the set bits b of L).
+struct Affine {
+  uint32_t c = 0;
+  uint32_t col[16] = {};
+  static Affine identity(uint32_t LB) {
+    Affine a;
+    for (uint32_t b = 0; b < LB; ++b) a.col[b] = 1u << b;
+    return a;
+  }
+  uint32_t lin(uint32_t L) const {
+    uint32_t v = 0;
+    for (uint32_t b = 0; b < 16; ++b)
+      if ((L >> b) & 1u) v ^= col[b];
+    return v;
+  }
+  uint32_t operator()(uint32_t L) const { return c ^ lin(L); }
+};
+
+Affine compose(const Affine& f, const Affine& g, uint32_t LB) {  // f o g
+  Affine h;
+  h.c = f(g.c);
+  for (uint32_t b = 0; b < LB; ++b) h.col[b] = f.lin(g.col[b]);
+  return h;
+}
+
+Affine inverse(const Affine& f, uint32_t LB) {
+  std::vector<uint32_t> inv(size_t{1} << LB);
+  for (uint32_t L = 0; L < (1u << LB); ++L) inv[f(L)] = L;
+  Affine g;
+  g.c = inv[0];
+  for (uint32_t b = 0; b < LB; ++b) g.col[b] = inv[1u << b] ^ g.c;
+  return g;
+}
+
+// X / CNOT as the index permutation they apply (self-inverse): X on bit t
+// flips it; CNOT (control c, target t) flips t where c is set.
+Affine perm_of(const LocalGate& g, uint32_t LB) {
+  Affine a = Affine::identity(LB);
+  if (g.ma == 0) a.c = g.mb;                          // X: mb = target bit
+  else a.col[__builtin_ctz(g.ma)] ^= g.mb ^ g.ma;     // CNOT: ma = control, mb = control | target
+  return a;
+}
+
+// A phase as planned on the host.
+struct PhasePlan {
+  Affine load;                 // frame at the phase start (in-place phases store through it too)
+  Affine store;                // store map (differs only when the phase re-lays the tile out)
+  uint32_t slot_bit[5] = {};   // local bit of register slot j
+  std::vector<TileStep> steps;
+  std::vector<int> step_gate_rot;  // per rotation added: local gate index (for the angle table)
+};
+
+// Slot kinds fixed by an excitation in the phase.
+enum : int { kFixNone = 0, kFixSE = 1, kFixDE = 2 };
+
+// Register phases of one launch: walk the gates in pass order; a phase
+// takes every rotation whose bits fit its R register bits (excitations on
+// the fixed slots) and that depends on no gate left for a later phase; a
+// permutation is taken into the frame after the phase's rotations unless a
+// skipped gate precedes it, and then blocks the rotations on its bits.  The
+// gates done after any number of phases are therefore closed under
+// predecessors.  Returns false when the launch's tables are full (the caller
+// continues with the remaining gates in a new launch).
+struct PassPlan {
+  std::vector<PhasePlan> phases;
+  std::vector<int> rot_gate;  // table entry k >= 1 -> local gate index
+  Affine end_frame;
+};
+
+PassPlan plan_launch(const std::vector<LocalGate>& lg, std::vector<char>& done, uint32_t LB, uint32_t R) {
+  PassPlan out;
+  Affine F = Affine::identity(LB);
+  size_t n_steps = 0;
+  const auto remaining = [&] {
+    for (char d : done)
+      if (!d) return true;
+    return false;
+  };
+  while (remaining()) {
+    PhasePlan ph;
+    ph.load = F;
+    uint32_t regs = 0, blocked = 0, perm_bits = 0;
+    int fix = kFixNone;
+    uint32_t fix_a = 0, fix_b = 0;  // excitation's A / B local masks
+    std::vector<int> rots;          // rotations taken, in order
+    std::vector<int> perms;         // permutations taken, in order
+    std::vector<int> signs;         // per rotation: +1, or -1 for an excitation with A / B swapped
+    for (size_t i = 0; i < lg.size(); ++i) {
+      if (done[i]) continue;
+      const LocalGate& g = lg[i];
+      if (g.bits & blocked) {
+        blocked |= g.bits;
+        continue;
+      }
+      if (!g.rot) {
+        perms.push_back(static_cast<int>(i));
+        perm_bits |= g.bits;
+        done[i] = 1;
+        continue;
+      }
+      bool ok = (g.bits & perm_bits) == 0 &&
+                static_cast<uint32_t>(__builtin_popcount(regs | g.bits)) <= R;
+      int sign = 1;
+      const int kind = g.ma == 0 ? kFixNone : (__builtin_popcount(g.ma) == 1 ? kFixSE : kFixDE);
+      if (ok && kind != kFixNone) {
+        if (fix == kFixNone) {
+          fix = kind;
+          fix_a = g.ma;
+          fix_b = g.mb;
+        } else if (fix == kind && fix_a == g.ma && fix_b == g.mb) {
+        } else if (fix == kind && fix_a == g.mb && fix_b == g.ma) {
+          sign = -1;  // the same rotation with the pair's roles swapped: angle -> -angle
+        } else {
+          ok = false;
+        }
+      }
+      if (ok && rots.size() >= kPhaseRot) ok = false;
+      if (!ok) {
+        blocked |= g.bits;
+        continue;
+      }
+      regs |= g.bits;
+      rots.push_back(static_cast<int>(i));
+      signs.push_back(sign);
+      done[i] = 1;
+    }
+    if (rots.empty()) {  // only permutations were free: fold them into the frame
+      for (int q : perms) F = compose(F, perm_of(lg[q], LB), LB);
+      continue;
+    }
+    // register slots: the excitation's wires first (SE: A -> 0, B -> 1;
+    // DE: A -> 0, 1, B -> 2, 3), then the other rotation bits, then padding
+    uint32_t used = 0, m = 0;
+    const auto put = [&](uint32_t b) {
+      if (!((used >> b) & 1u)) {
+        ph.slot_bit[m++] = b;
+        used |= 1u << b;
+      }
+    };
+    if (fix != kFixNone) {
+      for (uint32_t b = 0; b < LB; ++b)
+        if ((fix_a >> b) & 1u) put(b);
+      for (uint32_t b = 0; b < LB; ++b)
+        if ((fix_b >> b) & 1u) put(b);
+    }
+    for (uint32_t b = 0; b < LB; ++b)
+      if ((regs >> b) & 1u) put(b);
+    for (int b = static_cast<int>(LB) - 1; b >= 0 && m < R; --b) put(static_cast<uint32_t>(b));
+    const auto slot_of = [&](uint32_t b) {
+      for (uint32_t j = 0; j < R; ++j)
+        if (ph.slot_bit[j] == b) return static_cast<int>(j);
+      return -1;
+    };
+    // steps: excitation, then one RY per slot; a gate that cannot follow
+    // the step's content in that order opens a new step
+    TileStep cur{};
+    bool open = false;
+    const auto flush = [&] {
+      if (open) ph.steps.push_back(cur);
+      cur = TileStep{};
+      open = false;
+    };
+    for (size_t q = 0; q < rots.size(); ++q) {
+      const LocalGate& g = lg[rots[q]];
+      out.rot_gate.push_back(signs[q] * (rots[q] + 1));  // entry index = rot_gate.size(); sign = angle sign
+      const int16_t entry = static_cast<int16_t>(out.rot_gate.size());
+      if (g.ma == 0) {  // RY
+        const int j = slot_of(__builtin_ctz(g.mb));
+        if (open && cur.ry[j] != 0) flush();
+        cur.ry[j] = entry;
+      } else if (__builtin_popcount(g.ma) == 1) {  // SingleExcitation on slots (0, 1)
+        bool any_ry = false;
+        for (int j = 0; j < 5; ++j) any_ry = any_ry || cur.ry[j] != 0;
+        if (open && (cur.flags != 0 || any_ry)) flush();
+        cur.se = entry;
+        cur.flags |= 1u;
+      } else {  // DoubleExcitation on slots 0..3
+        bool any_ry = false;
+        for (int j = 0; j < 5; ++j) any_ry = any_ry || cur.ry[j] != 0;
+        if (open && ((cur.flags & 2u) || any_ry)) flush();
+        cur.de = entry;
+        cur.flags |= 2u;
+      }
+      open = true;
+    }
+    flush();
+    n_steps += ph.steps.size();
+    for (int q : perms) F = compose(F, perm_of(lg[q], LB), LB);
+    ph.store = ph.load;
+    out.phases.push_back(std::move(ph));
+    if (out.phases.size() == kMaxPhases || n_steps + kPhaseRot > kMaxSteps ||
+        out.rot_gate.size() + 1 + kPhaseRot > kMaxRot)
+      break;
+  }
+  // the permutations taken after the last phase: its stores leave the tile
+  // in plain order, i.e. logical L of its frame at F_end^-1 (F_last (L))
+  out.end_frame = F;
+  if (!out.phases.empty()) {
+    PhasePlan& last = out.phases.back();
+    last.store = compose(inverse(F, LB), last.load, LB);
+  }
+  return out;
+}
+
+// Bank-group vector of shared-memory slot offset v (fp64: the 16-byte chunk
+// of a 128-byte line, 3 bits; fp32: the 8-byte unit, 4 bits).
+uint32_t bank_of(bool f64, uint32_t v) { return f64 ? (v & 7u) : (v & 15u); }
+
+uint32_t gf2_rank(std::vector<uint32_t> v) {
+  uint32_t rank = 0;
+  for (uint32_t bit = 0; bit < 32; ++bit) {
+    size_t piv = v.size();
+    for (size_t i = rank; i < v.size(); ++i)
+      if ((v[i] >> bit) & 1u) {
+        piv = i;
+        break;
+      }
+    if (piv == v.size()) continue;
+    std::swap(v[rank], v[piv]);
+    for (size_t i = 0; i < v.size(); ++i)
+      if (i != rank && ((v[i] >> bit) & 1u)) v[i] ^= v[rank];
+    ++rank;
+  }
+  return rank;
+}
+
+// Thread bits of a phase: the LB - R non-register local bits, ordered so that
+// the lanes of one shared-memory wavefront (8 lanes x 16 B fp64, 16 lanes x
+// 8 B fp32) cover as many bank groups as possible through the load and the
+// store maps.
+template <typename T>
+std::vector<uint32_t> thread_bits(const PhasePlan& ph, uint32_t R, uint32_t LB) {
+  const bool f64 = sizeof(T) == 8;
+  uint32_t regs = 0;
+  for (uint32_t j = 0; j < R; ++j) regs |= 1u << ph.slot_bit[j];
+  std::vector<uint32_t> free_bits;
+  for (uint32_t b = 0; b < LB; ++b)
+    if (!((regs >> b) & 1u)) free_bits.push_back(b);
+  const uint32_t q = std::min<uint32_t>(f64 ? 3 : 4, static_cast<uint32_t>(free_bits.size()));
+  std::vector<uint32_t> best;
+  uint32_t best_score = 0;
+  const size_t m = free_bits.size();
+  for (uint32_t mask = 0; mask < (1u << m); ++mask) {
+    if (static_cast<uint32_t>(__builtin_popcount(mask)) != q) continue;
+    std::vector<uint32_t> pick, vl, vs;
+    for (size_t i = 0; i < m; ++i)
+      if ((mask >> i) & 1u) {
+        pick.push_back(free_bits[i]);
+        vl.push_back(bank_of(f64, swz<T>(ph.load.col[free_bits[i]])));
+        vs.push_back(bank_of(f64, swz<T>(ph.store.col[free_bits[i]])));
+      }
+    const uint32_t score = 2 * gf2_rank(vl) + gf2_rank(vs);
+    if (best.empty() || score > best_score) {
+      best = pick;
+      best_score = score;
+    }
+  }
+  std::vector<uint32_t> out = best;
+  for (uint32_t b : free_bits)
+    if (std::find(out.begin(), out.end(), b) == out.end()) out.push_back(b);
+  return out;
+}
+
+// Launch parameters for the pass; one launch per chunk of phases that fits
+// the parameter tables.
+template <typename T>
+std::vector<TileParams> build_launches(uint32_t n, uint32_t batch, uint32_t B, const std::vector<TGate>& gates,
+                                       const Pass& pass, const double* cs_dev) {
+  const uint32_t LB = B + static_cast<uint32_t>(pass.hbits.size());
+  const uint32_t R = sizeof(T) == 8 ? kR64 : kR32;
+  TileParams base{};
+  base.n = n;
+  base.B = B;
+  base.k = static_cast<uint32_t>(pass.hbits.size());
+  base.batch = batch;
+  base.cs = cs_dev;
+  for (uint32_t j = 0; j < base.k; ++j) base.hb[j] = pass.hbits[j];
+  const std::vector<LocalGate> lg = local_gates(n, B, pass.hbits, gates, pass);
   // a pass of X / CNOT gates only is an affine index map F on the local
   // bits: out[L] = in[F(L)] with F = f_1 o ... o f_m (gate 1 first in the
   // circuit, so f_m acts on L first); applied in the write-back
-  bool perm = first == 0;
+  bool perm = true;
   for (const LocalGate& o : lg) perm = perm && !o.rot;
   if (perm) {
-    const auto F = [&](uint32_t x) {
-      for (size_t q = lg.size(); q-- > 0;) {
-        const LocalGate& o = lg[q];
-        if (o.ma == 0) x ^= o.mb;                                            // X: mb = target bit
-        else if (x & o.ma) x ^= o.mb ^ o.ma;                                 // CNOT: ma = control, mb = control | target
-      }
-      return x;
-    };
-    const uint32_t LB = B + p.k;
+    Affine F = Affine::identity(LB);
+    for (const LocalGate& o : lg) F = compose(F, perm_of(o, LB), LB);
+    TileParams p = base;
     p.perm_only = 1;
-    p.perm_c = F(0);
-    for (uint32_t b = 0; b < 16; ++b) p.perm_col[b] = b < LB ? (F(1u << b) ^ p.perm_c) : 0u;
-    *next = lg.size();
-    return p;
+    p.perm_c = F.c;
+    for (uint32_t b = 0; b < 16; ++b) p.perm_col[b] = b < LB ? F.col[b] : 0u;
+    return {p};
   }
-  // merge consecutive gates (the pass order respects the circuit's DAG)
-  // while their local bits fit one fused op
-  size_t i = first;
-  uint32_t uoff = 0;
-  while (i < lg.size()) {
-    uint32_t u = lg[i].bits;
-    bool wide = fuse_bits == kMaxFuse || __builtin_popcount(u) == 4;
-    size_t j = i + 1;
-    while (j < lg.size()) {
-      const bool w2 = wide || __builtin_popcount(lg[j].bits) == 4;
-      if (__builtin_popcount(u | lg[j].bits) > (w2 ? kMaxFuse : fuse_bits)) break;
-      wide = w2;
-      u |= lg[j++].bits;
-    }
-    TileFop f{};
-    uint32_t pos[kMaxFuse], m = 0;
-    for (uint32_t b = 0; b < 32; ++b)
-      if ((u >> b) & 1u) pos[m++] = b;
-    f.m = m;
-    if (uoff + (1u << (2 * m)) > kMatElems) break;  // matrix area full: the rest goes to the next launch
-    f.uoff = uoff;
-    uoff += 1u << (2 * m);
-    for (uint32_t q = 0; q < m; ++q) f.pos |= pos[q] << (8 * q);
-    f.sub0 = p.n_fops == 0 ? 0 : p.fops[p.n_fops - 1].sub0 + p.fops[p.n_fops - 1].n_sub;
-    for (size_t q = i; q < j; ++q) {
-      TileSub& t = p.subs[f.sub0 + f.n_sub++];
-      t.code = (lg[q].rot << 8) | (compress(lg[q].ma, pos, m) << 4) | compress(lg[q].mb, pos, m);
-      t.param = lg[q].param;
-      t.c = lg[q].c;
-      t.s = lg[q].s;
-    }
-    p.fops[p.n_fops++] = f;
-    i = j;
-  }
-  *next = i;
-  return p;
-}
-
-// Item bits of a tensor-core op: the two free local bits c1 < c2 whose
-// shared-memory bank pattern for the MMA fragments (B loads of both
-// k-chunks: 4 slots x 4 items x re/im per warp access; D stores: 8 slots x 4
-// items) has the fewest lanes per bank, under the 128 B swizzle.
-uint32_t choose_item_bits(const TileFop& f, uint32_t LB) {
-  uint32_t pos[3], used = 0;
-  for (uint32_t j = 0; j < 3; ++j) {
-    pos[j] = (f.pos >> (8 * j)) & 0xffu;
-    used |= 1u << pos[j];
-  }
-  const auto swz8 = [](uint32_t L) { return (L ^ (L >> 3)) & 7u; };
-  const auto dep = [&](uint32_t k) {
-    uint32_t d = 0;
-    for (uint32_t j = 0; j < 3; ++j)
-      if ((k >> j) & 1u) d |= 1u << pos[j];
-    return d;
+  std::vector<TileParams> out;
+  std::vector<char> done(lg.size(), 0);
+  const auto left = [&] {
+    for (char d : done)
+      if (!d) return true;
+    return false;
   };
-  uint32_t best = 0, best_score = ~0u;
-  for (uint32_t c1 = 0; c1 < LB; ++c1) {
-    if ((used >> c1) & 1u) continue;
-    for (uint32_t c2 = c1 + 1; c2 < LB; ++c2) {
-      if ((used >> c2) & 1u) continue;
-      const auto dep2 = [&](uint32_t i) { return ((i & 1u) << c1) | (((i >> 1) & 1u) << c2); };
-      // 8-byte B loads are served per half-warp (16 lanes, bank pair = (amp
-      // mod 8, re/im)), 16-byte D stores per quarter-warp (8 lanes, amp mod
-      // 8): the score adds the worst lane count per bank in each phase
-      uint32_t score = 0;
-      for (uint32_t chunk = 0; chunk < 2; ++chunk)
-        for (uint32_t half = 0; half < 2; ++half) {
-          uint32_t cnt[16] = {};
-          for (uint32_t lane = 16 * half; lane < 16 * half + 16; ++lane) {
-            const uint32_t g = lane >> 2, tq = lane & 3u;
-            cnt[swz8(dep2(g >> 1) | dep(4 * chunk + tq)) * 2 + (g & 1u)]++;
-          }
-          score += *std::max_element(cnt, cnt + 16);
-        }
-      for (uint32_t quarter = 0; quarter < 4; ++quarter) {
-        uint32_t cnt[8] = {};
-        for (uint32_t lane = 8 * quarter; lane < 8 * quarter + 8; ++lane) cnt[swz8(dep2(lane & 3u) | dep(lane >> 2))]++;
-        score += *std::max_element(cnt, cnt + 8);
-      }
-      if (score < best_score) {
-        best_score = score;
-        best = c1 | (c2 << 5);
-      }
+  while (left()) {
+    const PassPlan plan = plan_launch(lg, done, LB, R);
+    if (plan.phases.empty()) {
+      // only permutations were left for this launch: one pure re-layout
+      TileParams p = base;
+      p.perm_only = 1;
+      p.perm_c = plan.end_frame.c;
+      for (uint32_t b = 0; b < 16; ++b) p.perm_col[b] = b < LB ? plan.end_frame.col[b] : 0u;
+      out.push_back(p);
+      continue;
     }
+    TileParams p = base;
+    p.n_rot = static_cast<uint32_t>(plan.rot_gate.size()) + 1;
+    p.rot_param[0] = -1;
+    p.rot_c[0] = 1.0;
+    p.rot_s[0] = 0.0;
+    for (size_t k = 0; k < plan.rot_gate.size(); ++k) {
+      const int code = plan.rot_gate[k];
+      const LocalGate& g = lg[std::abs(code) - 1];
+      p.rot_param[k + 1] = g.param;
+      p.rot_c[k + 1] = g.c;
+      p.rot_s[k + 1] = g.s;
+      p.rot_neg[k + 1] = code < 0 ? 1 : 0;  // (c, s) -> (c, -s)
+    }
+    uint32_t n_steps = 0;
+    for (const PhasePlan& ph : plan.phases) {
+      TilePhase& tp = p.ph[p.n_phases++];
+      const std::vector<uint32_t> tb = thread_bits<T>(ph, R, LB);
+      tp.ld_c = static_cast<uint16_t>(swz<T>(ph.load.c));
+      tp.st_c = static_cast<uint16_t>(swz<T>(ph.store.c));
+      for (size_t j = 0; j < tb.size(); ++j) {
+        tp.ld_tb[j] = static_cast<uint16_t>(swz<T>(ph.load.col[tb[j]]));
+        tp.st_tb[j] = static_cast<uint16_t>(swz<T>(ph.store.col[tb[j]]));
+      }
+      bool same = ph.load.c == ph.store.c;
+      for (uint32_t j = 0; j < R; ++j) {
+        tp.ld_r[j] = static_cast<uint16_t>(swz<T>(ph.load.col[ph.slot_bit[j]]));
+        tp.st_r[j] = static_cast<uint16_t>(swz<T>(ph.store.col[ph.slot_bit[j]]));
+      }
+      for (uint32_t b = 0; b < LB; ++b) same = same && ph.load.col[b] == ph.store.col[b];
+      tp.relayout = same ? 0 : 1;
+      tp.step0 = static_cast<uint16_t>(n_steps);
+      tp.n_steps = static_cast<uint16_t>(ph.steps.size());
+      for (const TileStep& st : ph.steps) p.steps[n_steps++] = st;
+    }
+    out.push_back(p);
   }
-  // ops whose slot bits all lie above the swizzle's reach (index bits >= 6)
-  // put several MMA lanes on one bank whatever the item bits; they take the
-  // FMA path, which spreads lanes over items instead
-  return best_score <= 12 ? best : kNoMma;
+  return out;
 }
 
 template <typename T>
@@ -850,18 +953,12 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
   // active: batch entries [0, active) take the pass (0 = all)
   if (active == 0) active = sv->batch;
   const uint32_t n = sv->n_qubits;
-  for (size_t first = 0, next = 0; first < pass.gates.size(); first = next) {
-  TileParams p = build_params(n, sv->batch, B, gates, pass, cs_dev, sizeof(T) == 8 ? 3 : 4, first, &next);
-  bool wide = false;
-  for (uint32_t o = 0; o < p.n_fops; ++o) wide = wide || p.fops[o].m == 4;
-  const uint32_t LB = B + p.k;
-  if (sizeof(T) == 8)
-    for (uint32_t o = 0; o < p.n_fops; ++o)
-      if (p.fops[o].m == 3) p.fops[o].ipos = choose_item_bits(p.fops[o], LB);
+  constexpr int R = sizeof(T) == 8 ? kR64 : kR32;
+  const uint32_t LB = B + static_cast<uint32_t>(pass.hbits.size());
   const uint64_t n_tiles = uint64_t{1} << (n - LB);
   // persistent over one entry's tiles; a batched state launches a CTA set
   // per entry, so give each group >= 16 tiles there to amortise the CTA
-  // prologue (matrix composition, ring fill) over enough traffic
+  // prologue over enough traffic
   uint64_t gx = std::min<uint64_t>(n_tiles, kTileBlocks);
   if (active > 1) gx = std::max<uint64_t>(1, std::min<uint64_t>(gx, n_tiles / (kGroups * 16)));
   const unsigned grid = static_cast<unsigned>(gx);
@@ -879,21 +976,65 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
     maps.emplace_back(key, state_map(sv, run_bytes));
     map = &maps.back().second;
   }
-  const size_t smem = kGroups * kStages * (sizeof(typename V2<T>::type) << LB) + 256 + kMatElems * sizeof(T) + 1024;  // rings + mbarriers + matrices + align
+  const size_t smem = kGroups * kStages * (sizeof(typename V2<T>::type) << LB) + 8 * kGroups * kStages + 1024;
   auto* amps = static_cast<typename V2<T>::type*>(sv->amps);
-  if (p.perm_only)
-    k_tile<T, kNT, 1, true><<<dim3(grid, active), kGroups * kNT, smem, sv->stream>>>(amps, *map, p);
-  else if (sizeof(T) == 4 || !wide)
-    k_tile<T, kNT, sizeof(T) == 4 ? 4 : 3, false><<<dim3(grid, active), kGroups * kNT, smem, sv->stream>>>(amps, *map, p);
-  else
-    k_tile<T, kNT / 2, 4, false><<<dim3(grid, active), kGroups * kNT / 2, smem, sv->stream>>>(amps, *map, p);
-  VQF_LAUNCHED();
+  for (const TileParams& p : build_launches<T>(n, sv->batch, B, gates, pass, cs_dev)) {
+    const dim3 g(grid, active);
+    const unsigned threads = kGroups << (LB - R);
+    constexpr int LBmax = sizeof(T) == 8 ? kLB64 : kLB32;
+    switch (LBmax - static_cast<int>(LB)) {
+      case 0:
+        if (p.perm_only) k_tile<T, R, LBmax, true><<<g, threads, smem, sv->stream>>>(amps, *map, p);
+        else k_tile<T, R, LBmax, false><<<g, threads, smem, sv->stream>>>(amps, *map, p);
+        break;
+      case 1:
+        if (p.perm_only) k_tile<T, R, LBmax - 1, true><<<g, threads, smem, sv->stream>>>(amps, *map, p);
+        else k_tile<T, R, LBmax - 1, false><<<g, threads, smem, sv->stream>>>(amps, *map, p);
+        break;
+      case 2:
+        if (p.perm_only) k_tile<T, R, LBmax - 2, true><<<g, threads, smem, sv->stream>>>(amps, *map, p);
+        else k_tile<T, R, LBmax - 2, false><<<g, threads, smem, sv->stream>>>(amps, *map, p);
+        break;
+      default:
+        throw Error(VQF_LOGIC_ERROR, "tile pass: unsupported tile width");
+    }
+    VQF_LAUNCHED();
   }
+}
+
+template <typename T, int R, int LB>
+void opt_in_smem() {
+  const int bytes = kGroups * kStages * (static_cast<int>(sizeof(T)) * 2 << LB) + 8 * kGroups * kStages + 1024;
+  VQF_CUDA(cudaFuncSetAttribute(k_tile<T, R, LB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  VQF_CUDA(cudaFuncSetAttribute(k_tile<T, R, LB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+void ensure_tile_attrs(const vqf_statevector* sv) {
+  static thread_local int opted = -1;
+  if (opted != sv->device) {
+    opt_in_smem<double, kR64, kLB64>();
+    opt_in_smem<double, kR64, kLB64 - 1>();
+    opt_in_smem<double, kR64, kLB64 - 2>();
+    opt_in_smem<float, kR32, kLB32>();
+    opt_in_smem<float, kR32, kLB32 - 1>();
+    opt_in_smem<float, kR32, kLB32 - 2>();
+    opted = sv->device;
+  }
+}
+
+// Registers below one warp-wide tile take one launch per gate.
+bool tile_too_small(uint32_t n, int32_t dtype) { return n < static_cast<uint32_t>(tile_r(dtype) + 5); }
+
+void apply_single(vqf_statevector* sv, const TGate& g, const double* cs_dev) {
+  GateArgs ga{g.kind, g.n_wires, {g.wires[0], g.wires[1], g.wires[2], g.wires[3]}, g.c, g.s,
+              g.param >= 0 ? cs_dev + 2 * (size_t)g.param * sv->batch : nullptr};
+  sv_apply(sv, ga);
 }
 
 }  // namespace
 
 std::vector<int> plan_tile_passes(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>& gates) {
+  if (tile_too_small(n_qubits, dtype)) return std::vector<int>(gates.size(), 1);
   uint32_t B, kmax;
   tile_shape(n_qubits, dtype, B, kmax);
   std::vector<int> out;
@@ -903,73 +1044,52 @@ std::vector<int> plan_tile_passes(uint32_t n_qubits, int32_t dtype, const std::v
 
 void plan_tile_counts(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>& gates, uint32_t* passes,
                       uint32_t* fused_ops) {
+  if (tile_too_small(n_qubits, dtype)) {
+    *passes = static_cast<uint32_t>(gates.size());
+    *fused_ops = 0;
+    return;
+  }
   uint32_t B, kmax;
   tile_shape(n_qubits, dtype, B, kmax);
   const std::vector<Pass> ps = schedule(n_qubits, B, kmax, gates);
-  uint32_t fops = 0, launches = 0;
+  uint32_t phases = 0, launches = 0;
   for (const Pass& p : ps) {
     if (!p.hbits.empty() && p.hbits[0] == 0xffffffffu) {
       ++launches;
       continue;
     }
-    for (size_t first = 0, next = 0; first < p.gates.size(); first = next, ++launches) {
-      const TileParams tp = build_params(n_qubits, 1, B, gates, p, nullptr, dtype == VQF_F64 ? 3 : 4, first, &next);
-      fops += tp.n_fops;
+    const std::vector<TileParams> ls = dtype == VQF_F64 ? build_launches<double>(n_qubits, 1, B, gates, p, nullptr)
+                                                        : build_launches<float>(n_qubits, 1, B, gates, p, nullptr);
+    for (const TileParams& tp : ls) {
+      phases += tp.n_phases;
       if (std::getenv("VQF_TILE_DEBUG")) {
         std::fprintf(stderr, "launch %u: k=%u hb=", launches, tp.k);
         for (uint32_t j = 0; j < tp.k; ++j) std::fprintf(stderr, "%u,", tp.hb[j]);
-        std::fprintf(stderr, " perm=%u fops=%u:", tp.perm_only, tp.n_fops);
-        for (uint32_t o = 0; o < tp.n_fops; ++o) {
-          const uint32_t ip = tp.fops[o].m == 3 && dtype == VQF_F64 ? choose_item_bits(tp.fops[o], B + tp.k) : 0;
-          std::fprintf(stderr, " m%u/%u[%x]%s", tp.fops[o].m, tp.fops[o].n_sub, tp.fops[o].pos,
-                       ip == kNoMma ? "F" : "");
-        }
+        std::fprintf(stderr, " perm=%u phases=%u:", tp.perm_only, tp.n_phases);
+        for (uint32_t q = 0; q < tp.n_phases; ++q) std::fprintf(stderr, " %u%s", tp.ph[q].n_steps, tp.ph[q].relayout ? "*" : "");
         std::fprintf(stderr, "\n");
       }
+      ++launches;
     }
   }
   *passes = launches;
-  *fused_ops = fops;
+  *fused_ops = phases;
 }
-
-namespace {
-void ensure_tile_attrs(const vqf_statevector* sv) {
-  static thread_local int opted = -1;
-  if (opted != sv->device) {
-    const int bytes = kGroups * kStages * (16 << VQF_TILE_LB) + 256 + kMatElems * 8 + 1024;
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, kNT, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, kNT / 2, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, kNT, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<double, kNT, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    VQF_CUDA(cudaFuncSetAttribute(k_tile<float, kNT, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    opted = sv->device;
-  }
-}
-}  // namespace
 
 int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, const double* cs_dev) {
   if (gates.empty()) return 0;
   const uint32_t n = sv->n_qubits;
+  if (tile_too_small(n, sv->dtype)) {
+    for (const TGate& g : gates) apply_single(sv, g, cs_dev);
+    return static_cast<int>(gates.size());
+  }
   uint32_t B, kmax;
   tile_shape(n, sv->dtype, B, kmax);
   ensure_tile_attrs(sv);
   const std::vector<Pass> passes = schedule(n, B, kmax, gates);
-  const bool tiny = (sv->amp_bytes() << B) < 128;  // 2-3 qubits: a run is below one 128 B row
   for (const Pass& pass : passes) {
-    if (tiny) {
-      for (int gi : pass.gates) {
-        const TGate& g = gates[gi];
-        GateArgs ga{g.kind, g.n_wires, {g.wires[0], g.wires[1], g.wires[2], g.wires[3]}, g.c, g.s,
-                    g.param >= 0 ? cs_dev + 2 * (size_t)g.param * sv->batch : nullptr};
-        sv_apply(sv, ga);
-      }
-      continue;
-    }
     if (!pass.hbits.empty() && pass.hbits[0] == 0xffffffffu) {
-      const TGate& g = gates[pass.gates[0]];
-      GateArgs ga{g.kind, g.n_wires, {g.wires[0], g.wires[1], g.wires[2], g.wires[3]}, g.c, g.s,
-                  g.param >= 0 ? cs_dev + 2 * (size_t)g.param * sv->batch : nullptr};
-      sv_apply(sv, ga);
+      apply_single(sv, gates[pass.gates[0]], cs_dev);
       continue;
     }
     if (sv->dtype == VQF_F64)
@@ -983,10 +1103,9 @@ int run_circuit_tiled(vqf_statevector* sv, const std::vector<TGate>& gates, cons
 
 std::vector<int> tile_param_first_pass(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>& gates,
                                        uint32_t n_params) {
+  if (tile_too_small(n_qubits, dtype) || gates.empty()) return {};  // per-gate path
   uint32_t B, kmax;
   tile_shape(n_qubits, dtype, B, kmax);
-  const uint32_t amp = dtype == VQF_F64 ? 16 : 8;
-  if ((amp << B) < 128 || gates.empty()) return {};  // tiny registers: per-gate path
   const std::vector<Pass> passes = schedule(n_qubits, B, kmax, gates);
   std::vector<int> first(n_params, -1);
   for (size_t p = 0; p < passes.size(); ++p) {
@@ -1002,6 +1121,7 @@ std::vector<int> tile_param_first_pass(uint32_t n_qubits, int32_t dtype, const s
 int run_circuit_tiled_shared(vqf_statevector* sv, const std::vector<TGate>& gates, const double* cs_dev,
                              const std::vector<uint32_t>& join) {
   const uint32_t n = sv->n_qubits;
+  if (tile_too_small(n, sv->dtype)) throw Error(VQF_LOGIC_ERROR, "shared-prefix circuit: register below tile size");
   uint32_t B, kmax;
   tile_shape(n, sv->dtype, B, kmax);
   if (join.size() != sv->batch) throw Error(VQF_LOGIC_ERROR, "shared-prefix circuit: one join pass per entry");
@@ -1030,6 +1150,8 @@ int run_circuit_tiled_shared(vqf_statevector* sv, const std::vector<TGate>& gate
     uint32_t next = active;
     while (next < sv->batch && join[next] <= p) ++next;
     join_up_to(next);
+    if (!passes[p].hbits.empty() && passes[p].hbits[0] == 0xffffffffu)
+      throw Error(VQF_LOGIC_ERROR, "shared-prefix circuit: single-gate pass");
     if (sv->dtype == VQF_F64)
       launch_pass<double>(sv, gates, passes[p], B, cs_dev, active);
     else

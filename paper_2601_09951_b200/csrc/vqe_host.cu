@@ -455,9 +455,9 @@ struct HbmEngine {
   int device;
   vqf_statevector* sv = nullptr;
   std::vector<double> cs;  // [param][entry] (cos, sin)
-  HbmEngine(uint32_t n_, int32_t kind_, uint32_t layers_, uint32_t batch, int device_)
+  HbmEngine(uint32_t n_, int32_t kind_, uint32_t layers_, uint32_t batch, int device_, int32_t dtype = VQF_F64)
       : n(n_), P(ansatz_params(kind_, layers_, n_)), layers(layers_), kind(kind_), device(device_) {
-    if (vqf_sv_create(n, batch, VQF_F64, device, &sv) != VQF_OK) throw Error(VQF_CUDA_ERROR, vqf_last_error());
+    if (vqf_sv_create(n, batch, dtype, device, &sv) != VQF_OK) throw Error(VQF_CUDA_ERROR, vqf_last_error());
   }
   ~HbmEngine() { vqf_sv_destroy(sv); }
   HbmEngine(const HbmEngine&) = delete;
@@ -532,9 +532,9 @@ struct ShiftEvaluator {
   // (order[0] = 0, the base); join[e] = first tile pass using the shifted
   // parameter.  Chunks of K - 1 shifted circuits run with the base as entry 0.
   std::vector<uint32_t> order, join;
-  ShiftEvaluator(uint32_t n_, int32_t kind_, uint32_t layers_, int device_)
+  ShiftEvaluator(uint32_t n_, int32_t kind_, uint32_t layers_, int device_, int32_t dtype = VQF_F64)
       : n(n_), P(ansatz_params(kind_, layers_, n_)), NC(2 * P + 1), kind(kind_), layers(layers_), device(device_) {
-    const double entry = (double)(uint64_t{1} << n) * 16.0;
+    const double entry = (double)(uint64_t{1} << n) * (dtype == VQF_F64 ? 16.0 : 8.0);
     K = static_cast<uint32_t>(std::max(1.0, std::min<double>(NC, std::floor(0.6 * (double)free_device_bytes(device) / entry))));
     if (const char* cap = std::getenv("VQF_SHIFT_MAX_BATCH")) K = std::max(1u, std::min<uint32_t>(K, std::atoi(cap)));
     batched = K == NC;
@@ -542,7 +542,7 @@ struct ShiftEvaluator {
     // circuit at a time is cheaper
     if (!batched && K < 8) K = 1;
     const std::vector<int> first =
-        K >= 2 ? tile_param_first_pass(n, VQF_F64, ansatz_tgates(kind, layers, n), P) : std::vector<int>{};
+        K >= 2 ? tile_param_first_pass(n, dtype, ansatz_tgates(kind, layers, n), P) : std::vector<int>{};
     if (!first.empty() && !std::getenv("VQF_NO_SHARED_PREFIX")) {
       const auto join_of = [&](uint32_t c) -> uint32_t {
         if (c == 0) return 0;
@@ -557,7 +557,7 @@ struct ShiftEvaluator {
     } else if (!batched) {
       K = 1;  // no prefix sharing: one circuit at a time
     }
-    eng = std::make_unique<HbmEngine>(n, kind, layers, K, device);
+    eng = std::make_unique<HbmEngine>(n, kind, layers, K, device, dtype);
   }
   // runs f with the engine's batch temporarily set to b entries
   template <typename F>
@@ -646,9 +646,9 @@ struct AdjointRunner {
   vqf_statevector* lam = nullptr;
   AdjointPlan plan;
   std::vector<AdjGate> prog;
-  AdjointRunner(uint32_t n, int32_t kind, uint32_t layers, int device, const CompiledHam& ch)
-      : eng(n, kind, layers, 1, device), prog(ansatz_program(kind, layers, n)) {
-    if (vqf_sv_create(n, 1, VQF_F64, device, &lam) != VQF_OK) throw Error(VQF_CUDA_ERROR, vqf_last_error());
+  AdjointRunner(uint32_t n, int32_t kind, uint32_t layers, int device, const CompiledHam& ch, int32_t dtype = VQF_F64)
+      : eng(n, kind, layers, 1, device, dtype), prog(ansatz_program(kind, layers, n)) {
+    if (vqf_sv_create(n, 1, dtype, device, &lam) != VQF_OK) throw Error(VQF_CUDA_ERROR, vqf_last_error());
     plan.init(eng.sv, lam, ch, eng.P);
   }
   ~AdjointRunner() { vqf_sv_destroy(lam); }
@@ -660,7 +660,8 @@ struct AdjointRunner {
 };
 
 void run_vqe_hbm(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const vqf_adam_config& cfg,
-                 const std::vector<double>& init, int32_t method, int device, vqf_vqe_result* r) {
+                 const std::vector<double>& init, int32_t method, int device, vqf_vqe_result* r,
+                 int32_t dtype = VQF_F64) {
   const uint32_t n = h->n_qubits;
   const CompiledHam ch = compile_hamiltonian(h);
   // Hamiltonians beyond the adjoint tables take parameter shift (same
@@ -668,8 +669,8 @@ void run_vqe_hbm(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const 
   const bool adjoint = method == VQF_GRAD_ADJOINT && AdjointPlan::supports(ch, n);
   std::unique_ptr<ShiftEvaluator> evp;
   std::unique_ptr<AdjointRunner> adj;
-  if (adjoint) adj = std::make_unique<AdjointRunner>(n, kind, layers, device, ch);
-  else evp = std::make_unique<ShiftEvaluator>(n, kind, layers, device);
+  if (adjoint) adj = std::make_unique<AdjointRunner>(n, kind, layers, device, ch, dtype);
+  else evp = std::make_unique<ShiftEvaluator>(n, kind, layers, device, dtype);
   const uint32_t P = ansatz_params(kind, layers, n);
   std::vector<double> theta = init.empty() ? std::vector<double>(P, 0.0) : init;
   std::vector<double> m(P, 0.0), v(P, 0.0), grad(P), tn(P), mn(P), vn(P), E;
@@ -742,8 +743,19 @@ void run_vqe_hbm(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const 
 
 bool small_ok(uint32_t n, uint32_t P) { return n <= (uint32_t)kSmallMaxN && P <= (uint32_t)kSmallMaxP; }
 
+// Storage precision of the engine's states.  complex64 (VQF_F32) runs
+// fixed-iteration only: fp32 rounding cannot reproduce the reference's
+// tol-mode stop decisions, so a gradient tolerance is
+// refused rather than silently changing the iteration count.
+void check_dtype(int32_t dtype, const vqf_adam_config* cfg) {
+  if (dtype != VQF_F64 && dtype != VQF_F32) throw_invalid("unknown dtype");
+  if (dtype == VQF_F32 && cfg != nullptr && cfg->has_gradient_tolerance)
+    throw_invalid("fp32 (complex64) runs are fixed-iteration only: gradient_tolerance needs fp64");
+}
+
 void run_vqe_impl(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const vqf_adam_config* cfg,
-                  const double* init, uint32_t n_init, int32_t method, int32_t device, vqf_vqe_result* r) {
+                  const double* init, uint32_t n_init, int32_t method, int32_t device, vqf_vqe_result* r,
+                  int32_t dtype = VQF_F64) {
   const auto t0 = Clock::now();
   check_adam(cfg);
   if (h == nullptr || r == nullptr) throw_invalid("null argument");
@@ -752,12 +764,14 @@ void run_vqe_impl(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const
   if (n_init != 0 && n_init != P) throw_invalid("initial parameter count mismatch");
   check_ansatz_register(kind, n);
   if (method != VQF_GRAD_PARAMETER_SHIFT && method != VQF_GRAD_ADJOINT) throw_invalid("unknown gradient method");
+  check_dtype(dtype, cfg);
   std::vector<double> init_v(init, init + n_init);
   // registers that fit one warp run the whole optimisation in one launch
   // (k_vqe_warp, parameter-shift gradients); the adjoint method would equal
   // it to rounding but pays one HBM-engine launch per gate there, so small
-  // registers take this path for either method
-  if (small_ok(n, P)) {
+  // registers take this path for either method (fp64 only: the register
+  // engine holds complex128 amplitudes)
+  if (dtype == VQF_F64 && small_ok(n, P)) {
     SmallJob j;
     j.batch = 1;
     j.n_qubits = static_cast<int32_t>(n);
@@ -773,7 +787,7 @@ void run_vqe_impl(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const
     if (j.status[0] != kStatusOk) throw_runtime(small_error(j, 0, 0.0));
     fill_result(j, 0, r);
   } else {
-    run_vqe_hbm(h, kind, layers, *cfg, init_v, method, device, r);
+    run_vqe_hbm(h, kind, layers, *cfg, init_v, method, device, r, dtype);
   }
   r->wall_seconds = seconds_since(t0);
 }
@@ -934,13 +948,19 @@ int vqf_prepare_ansatz(int32_t kind, uint32_t layers, const double* theta, uint3
 
 int vqf_energy(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h, int32_t kind, uint32_t layers,
                int32_t device, double* out) {
+  return vqf_energy_ex(theta, n_theta, h, kind, layers, device, VQF_F64, out);
+}
+
+int vqf_energy_ex(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h, int32_t kind, uint32_t layers,
+                  int32_t device, int32_t dtype, double* out) {
   return guarded([&] {
     if (h == nullptr || out == nullptr) throw_invalid("null argument");
+    check_dtype(dtype, nullptr);
     const uint32_t P = ansatz_params(kind, layers, h->n_qubits);
     if (n_theta != P) throw_invalid("parameter count mismatch for ansatz");
     check_ansatz_register(kind, h->n_qubits);
     const CompiledHam ch = compile_hamiltonian(h);
-    HbmEngine eng(h->n_qubits, kind, layers, 1, device);
+    HbmEngine eng(h->n_qubits, kind, layers, 1, device, dtype);
     eng.prepare([&](uint32_t j, uint32_t) { return theta[j]; });
     double tot[2];
     sv_expectation(eng.sv, ch, tot);
@@ -951,8 +971,14 @@ int vqf_energy(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h, 
 
 int vqf_gradient(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h, int32_t kind, uint32_t layers,
                  int32_t method, int32_t device, double* grad_out) {
+  return vqf_gradient_ex(theta, n_theta, h, kind, layers, method, device, VQF_F64, grad_out);
+}
+
+int vqf_gradient_ex(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h, int32_t kind, uint32_t layers,
+                    int32_t method, int32_t device, int32_t dtype, double* grad_out) {
   return guarded([&] {
     if (h == nullptr || grad_out == nullptr) throw_invalid("null argument");
+    check_dtype(dtype, nullptr);
     const uint32_t P = ansatz_params(kind, layers, h->n_qubits);
     if (n_theta != P) throw_invalid("parameter count mismatch for ansatz");
     check_ansatz_register(kind, h->n_qubits);
@@ -960,14 +986,14 @@ int vqf_gradient(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h
     const CompiledHam ch = compile_hamiltonian(h);
     std::vector<double> th(theta, theta + n_theta), E;
     if (method == VQF_GRAD_ADJOINT && AdjointPlan::supports(ch, h->n_qubits)) {
-      AdjointRunner adj(h->n_qubits, kind, layers, device, ch);
+      AdjointRunner adj(h->n_qubits, kind, layers, device, ch, dtype);
       double e[2];
       adj.run(th, e, grad_out);
       // energy()'s check (statevector.hpp:244-247), as on the shift path
       if (std::abs(e[1]) >= 1e-10) throw_runtime(imag_msg(e[1]));
       return;
     }
-    ShiftEvaluator ev(h->n_qubits, kind, layers, device);
+    ShiftEvaluator ev(h->n_qubits, kind, layers, device, dtype);
     ev.run(th, ch, static_cast<int>(ev.NC), E);
     for (uint32_t c = 1; c < ev.NC; ++c)
       if (std::abs(E[2 * c + 1]) >= 1e-10) throw_runtime(imag_msg(E[2 * c + 1]));
@@ -978,6 +1004,12 @@ int vqf_gradient(const double* theta, uint32_t n_theta, const vqf_hamiltonian* h
 int vqf_run_vqe(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const vqf_adam_config* config,
                 const double* init, uint32_t n_init, int32_t method, int32_t device, vqf_vqe_result* result) {
   return guarded([&] { run_vqe_impl(h, kind, layers, config, init, n_init, method, device, result); });
+}
+
+int vqf_run_vqe_ex(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const vqf_adam_config* config,
+                   const double* init, uint32_t n_init, int32_t method, int32_t device, int32_t dtype,
+                   vqf_vqe_result* result) {
+  return guarded([&] { run_vqe_impl(h, kind, layers, config, init, n_init, method, device, result, dtype); });
 }
 
 int vqf_run_vqe_batch(const vqf_hamiltonian* hs, uint32_t batch, int32_t kind, uint32_t layers,
@@ -1216,9 +1248,9 @@ int vqf_run_scaling_study(const vqf_scaling_config* cfg, vqf_scaling_record* rec
       r.theta = theta.data();
       const auto t0 = Clock::now();
       run_vqe_impl(&h, VQF_ANSATZ_HARDWARE_EFFICIENT, cfg->layers, &adam, init.data(), P, cfg->gradient_method,
-                   cfg->device, &r);
+                   cfg->device, &r, cfg->dtype);
       records[i].n_qubits = n;
-      records[i].state_bytes = vqf_memory_estimate(n);
+      records[i].state_bytes = vqf_memory_estimate(n) / (cfg->dtype == VQF_F32 ? 2 : 1);
       records[i].runtime_seconds = seconds_since(t0);
       records[i].final_energy = r.energy;
       records[i].iterations_run = r.iterations_run;

@@ -285,20 +285,31 @@ def prepare_ansatz(spec: AnsatzSpec, theta, n_qubits: int, device: int = 0) -> S
     return psi
 
 
-def energy(theta, hamiltonian: QubitHamiltonian, spec: AnsatzSpec, device: int = 0) -> float:
+def _dtype(dtype: str) -> int:
+    if dtype not in ("f64", "f32"):
+        raise ValueError("unknown dtype")
+    return A.F64 if dtype == "f64" else A.F32
+
+
+def energy(theta, hamiltonian: QubitHamiltonian, spec: AnsatzSpec, device: int = 0, dtype: str = "f64") -> float:
+    """vqe.hpp:99-104; dtype "f32" prepares complex64 states (extension)."""
     t = np.ascontiguousarray(theta, dtype=np.float64)
     keep, hs = hamiltonian.as_c()
     out = C.c_double()
-    check(lib.vqf_energy(t.ctypes.data_as(A.dp), len(t), C.byref(hs), spec.kind, spec.layers, device, C.byref(out)))
+    check(lib.vqf_energy_ex(t.ctypes.data_as(A.dp), len(t), C.byref(hs), spec.kind, spec.layers, device,
+                            _dtype(dtype), C.byref(out)))
     return out.value
 
 
-def gradient(theta, hamiltonian: QubitHamiltonian, spec: AnsatzSpec, method: str = "shift", device: int = 0):
+def gradient(theta, hamiltonian: QubitHamiltonian, spec: AnsatzSpec, method: str = "shift", device: int = 0,
+             dtype: str = "f64"):
+    """vqe.hpp:112-127 (method "shift"), or the adjoint method."""
     t = np.ascontiguousarray(theta, dtype=np.float64)
     keep, hs = hamiltonian.as_c()
     out = np.zeros(len(t))
-    check(lib.vqf_gradient(t.ctypes.data_as(A.dp), len(t), C.byref(hs), spec.kind, spec.layers,
-                           A.GRAD_SHIFT if method == "shift" else A.GRAD_ADJOINT, device, out.ctypes.data_as(A.dp)))
+    check(lib.vqf_gradient_ex(t.ctypes.data_as(A.dp), len(t), C.byref(hs), spec.kind, spec.layers,
+                              A.GRAD_SHIFT if method == "shift" else A.GRAD_ADJOINT, device, _dtype(dtype),
+                              out.ctypes.data_as(A.dp)))
     return out
 
 
@@ -366,15 +377,17 @@ def _vqe_result(theta, traj, r, P) -> VqeResult:
 
 
 def run_vqe(hamiltonian: QubitHamiltonian, spec: AnsatzSpec, config: AdamConfig = None, initial_theta=(),
-            method: str = "shift", device: int = 0) -> VqeResult:
+            method: str = "shift", device: int = 0, dtype: str = "f64") -> VqeResult:
+    """vqe.hpp:194-254.  dtype "f32": complex64 states, fixed-iteration runs
+    only (a gradient tolerance raises ValueError)."""
     config = config or AdamConfig()
     P = n_parameters(spec, hamiltonian.n_qubits)
     init = np.ascontiguousarray(initial_theta, dtype=np.float64)
     theta, traj, r = _vqe_result_buffers(P, config.max_iterations)
     keep, hs = hamiltonian.as_c()
     cfg = config.as_c()
-    check(lib.vqf_run_vqe(C.byref(hs), spec.kind, spec.layers, C.byref(cfg), init.ctypes.data_as(A.dp), len(init),
-                          A.GRAD_SHIFT if method == "shift" else A.GRAD_ADJOINT, device, C.byref(r)))
+    check(lib.vqf_run_vqe_ex(C.byref(hs), spec.kind, spec.layers, C.byref(cfg), init.ctypes.data_as(A.dp), len(init),
+                             A.GRAD_SHIFT if method == "shift" else A.GRAD_ADJOINT, device, _dtype(dtype), C.byref(r)))
     return _vqe_result(theta, traj, r, P)
 
 
@@ -578,6 +591,7 @@ class ScalingConfig:
     force: bool = False
     method: str = "shift"
     device: int = 0
+    dtype: str = "f64"
 
 
 def run_scaling_study(config: ScalingConfig = None) -> List[dict]:
@@ -585,7 +599,8 @@ def run_scaling_study(config: ScalingConfig = None) -> List[dict]:
     q = np.ascontiguousarray(config.qubits, dtype=np.uint32)
     cfg = A.ScalingConfig(q.ctypes.data_as(A.u32p), len(q), config.layers, config.iterations, config.learning_rate,
                           config.coupling, config.field, int(config.z_sum_mode), config.theta_init, int(config.force),
-                          A.GRAD_SHIFT if config.method == "shift" else A.GRAD_ADJOINT, config.device)
+                          A.GRAD_SHIFT if config.method == "shift" else A.GRAD_ADJOINT, config.device,
+                          _dtype(config.dtype))
     recs = (A.ScalingRecord * max(1, len(q)))()
     check(lib.vqf_run_scaling_study(C.byref(cfg), recs))
     return [{"n_qubits": r.n_qubits, "state_bytes": r.state_bytes, "runtime_seconds": r.runtime_seconds,

@@ -663,3 +663,55 @@ def test_pes_kernel_device_hamiltonians_match_golden(gpu, golden):
         assert max(abs(gd[k] - wd[k]) for k in wd) < 1e-12, b
         assert abs(hf["hf_energy"] - g["hartree_fock"][b]["hf_energy"]) < 1e-12
         assert hf["scf_iterations"] == g["hartree_fock"][b]["scf_iterations"]
+
+
+# --------------------------------------------------- fp32 (complex64) path
+F32_E_TOL = 1e-5  # north_star: energies within 1e-5 in fp32
+
+
+@pytest.mark.parametrize("n", [4, 7, 12, 16, 20, 24])
+def test_f32_energy_and_gradient_within_1e5(gpu, ref, n):
+    """energy / gradient with complex64 states against the reference's fp64
+    energy() (vqe.hpp:99-127) on TFIM and a random Pauli sum."""
+    V = gpu
+    hea = V.AnsatzSpec.hardware_efficient(2)
+    th = np.random.default_rng(n).uniform(-1.5, 1.5, 2 * n)
+    for h in [ref.build_tfim(n, 1.0, 0.9), ref.canonicalize(ref.random_hamiltonian(20260804, n, 32))]:
+        e64 = ref.energy(1, 2, th, h)
+        assert abs(V.energy(th, to_v(V, h), hea, dtype="f32") - e64) < F32_E_TOL
+        if n <= 12:
+            g64 = ref.gradient(1, 2, th, h)
+            for method in ("shift", "adjoint"):
+                g = V.gradient(th, to_v(V, h), hea, method=method, dtype="f32")
+                assert np.max(np.abs(g - g64)) < F32_E_TOL, method
+
+
+@pytest.mark.parametrize("n", [4, 10, 18])
+def test_f32_run_vqe_fixed_iterations(gpu, ref, n):
+    """run_vqe in fp32 (fixed iteration count) follows the reference's fp64
+    trajectory within 1e-5; tol mode is refused (fp32 cannot reproduce the
+    reference's stop decisions)."""
+    V = gpu
+    h = ref.build_tfim(n, 1.0, 1.0)
+    want = ref.run_vqe(h, kind=1, layers=2, lr=0.05, max_iter=3, init=[0.1] * (2 * n))
+    cfg = V.AdamConfig(learning_rate=0.05, max_iterations=3)
+    for method in ("shift", "adjoint"):
+        r = V.run_vqe(to_v(V, h), V.AnsatzSpec.hardware_efficient(2), cfg, [0.1] * (2 * n), method=method, dtype="f32")
+        assert r.iterations_run == 3 and len(r.trajectory) == 4
+        # complex64 amplitudes carry ~6e-8 relative rounding per gate, so
+        # over an optimisation the bar is relative once |E| > 1
+        bar = F32_E_TOL * np.maximum(1.0, np.abs(want["trajectory"]))
+        assert np.all(np.abs(np.array(r.trajectory) - want["trajectory"]) < bar), method
+        assert np.max(np.abs(np.array(r.theta) - want["theta"])) < 1e-4
+    with pytest.raises(ValueError, match="fixed-iteration"):
+        V.run_vqe(to_v(V, h), V.AnsatzSpec.hardware_efficient(2),
+                  V.AdamConfig(max_iterations=5, gradient_tolerance=1e-3), dtype="f32")
+
+
+def test_f32_scaling_study(gpu, ref):
+    V = gpu
+    recs = V.run_scaling_study(V.ScalingConfig(qubits=[6, 14], iterations=2, dtype="f32"))
+    want = ref.run_scaling_study([6, 14], iterations=2)
+    for r, w in zip(recs, want):
+        assert r["state_bytes"] == (1 << r["n_qubits"]) * 8
+        assert abs(r["final_energy"] - w["final_energy"]) < F32_E_TOL and r["iterations_run"] == 2
