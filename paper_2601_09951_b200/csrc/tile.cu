@@ -140,6 +140,11 @@ struct TilePhase {
   uint16_t ld_tb[9], ld_r[5];
   uint16_t st_tb[9], st_r[5];
   uint16_t relayout;
+  // last phase only: store straight to HBM from the registers.  st_* then
+  // hold the UNswizzled store map (local index of the register in the
+  // plain tile); the lanes are local bits 0..4, so a warp's store covers one
+  // 512-byte run.
+  uint16_t direct;
 };
 
 struct TileParams {
@@ -233,9 +238,14 @@ __device__ __forceinline__ void group_sync(uint32_t group) {
 
 // One register phase on the tile t: load the thread's 2^R amplitudes through
 // the frame, run the phase's steps in registers, store them back.
-template <typename T, int R, int LB, int NT>
+// Direct last phase: after the loads (one group barrier: the buffer is then
+// free) `refill` issues the group's next TMA loads into it, so the next tile
+// streams in while this one computes and stores.
+template <typename T, int R, int LB, int NT, typename Refill>
 __device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePhase& ph, const TileStep* steps,
-                                          const double2* rcs, uint32_t gt, uint32_t group) {
+                                          const double2* rcs, uint32_t gt, uint32_t group,
+                                          typename V2<T>::type* s, const uint64_t* run_off, uint32_t B,
+                                          Refill&& refill) {
   using A = typename V2<T>::type;
   constexpr int NR = 1 << R;
   const auto slots = [&](const uint16_t* tb, const uint16_t* rv, uint32_t c, uint32_t (&off)[NR]) {
@@ -260,14 +270,22 @@ __device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePha
   A x[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) x[r] = t[off[r]];
-  if (ph.relayout) {
-    group_sync<NT>(group);  // every slot read before any is overwritten
+  const bool direct = ph.direct != 0;
+  if (direct || ph.relayout) {
+    group_sync<NT>(group);  // every slot read before any is overwritten / refilled
     slots(ph.st_tb, ph.st_r, ph.st_c, off);
+    if (direct) refill();
   }
   const uint32_t n_steps = ph.n_steps, step0 = ph.step0;
   for (uint32_t q = 0; q < n_steps; ++q) run_step<R, A, T>(x, steps[step0 + q], rcs);
+  if (direct) {
+    const uint32_t low = (1u << B) - 1;
 #pragma unroll
-  for (int r = 0; r < NR; ++r) t[off[r]] = x[r];
+    for (int r = 0; r < NR; ++r) s[run_off[off[r] >> B] | (off[r] & low)] = x[r];
+  } else {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) t[off[r]] = x[r];
+  }
 }
 
 // Persistent tile kernel: G consumer groups of NT = 2^(LB - R) threads, each
@@ -296,7 +314,9 @@ __global__ void __launch_bounds__(kGroups << (LB - R), 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kGroups * kStages * (size_t)tile_bytes) + group * kStages;
   __shared__ double2 rcs[kMaxRot];
   __shared__ uint16_t ftab[PERM ? 2 : 1][64];
-  __shared__ uint64_t run_off_all[PERM ? kGroups : 1][PERM ? (1 << kMaxHigh) : 1];
+  // run starts of the group's current tile (double-buffered: a fast thread
+  // fills the next tile's while slow ones still store the current one)
+  __shared__ uint64_t run_off_all[kGroups][2][1 << kMaxHigh];
   const int32_t entry = static_cast<int32_t>(blockIdx.y);
   A* s = a + ((uint64_t)blockIdx.y << p.n);
   const uint64_t n_tiles = uint64_t{1} << (p.n - p.B - p.k);
@@ -343,39 +363,54 @@ __global__ void __launch_bounds__(kGroups << (LB - R), 1)
       if (t0 < n_tiles) issue_load(t0, st);
     }
   uint64_t tile = first;
+  const bool direct = !PERM && p.ph[p.n_phases - 1].direct != 0;
   for (uint32_t it = 0; tile < n_tiles; tile += step, ++it) {
     const int cur = it % kStages;
+    const uint64_t ahead = tile + (uint64_t)kStages * step;
     mbar_wait(&bar[cur], (it / kStages) & 1u);
     A* t = stage_buf(cur);
-    if constexpr (PERM) {
-      uint64_t* run_off = run_off_all[group];
+    uint64_t* run_off = run_off_all[group][it & 1u];
+    if (PERM || direct)
       for (uint32_t j = gt; j < n_runs; j += NT) run_off[j] = run_start(p, tile, j);
-      group_sync<NT>(group);
-      const uint32_t low_mask = run_amps - 1;
-#pragma unroll 4
-      for (uint32_t li = gt; li < NL; li += NT) {
-        const uint32_t src = p.perm_c ^ ftab[0][li & 63u] ^ ftab[1][li >> 6];
-        s[run_off[li >> p.B] | (li & low_mask)] = t[swz<T>(src)];
+    if constexpr (PERM) {
+      // read the whole tile through the index map into registers, free the
+      // buffer for the next load, then 16-byte stores along the runs
+      constexpr uint32_t U = NL / NT;
+      A v[U];
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) {
+        const uint32_t li = gt + u * NT;
+        v[u] = t[swz<T>(p.perm_c ^ ftab[0][li & 63u] ^ ftab[1][li >> 6])];
       }
-      group_sync<NT>(group);  // buffer free for the next TMA load
+      group_sync<NT>(group);
+      if (gt < 32 && ahead < n_tiles) issue_load(ahead, cur);
+      const uint32_t low_mask = run_amps - 1;
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) {
+        const uint32_t li = gt + u * NT;
+        s[run_off[li >> p.B] | (li & low_mask)] = v[u];
+      }
     } else {
+      const auto refill = [&] {
+        if (gt < 32 && ahead < n_tiles) issue_load(ahead, cur);
+      };
       for (uint32_t ph = 0; ph < p.n_phases; ++ph) {
-        run_phase<T, R, LB, NT>(t, p.ph[ph], p.steps, rcs, gt, group);
-        if (ph + 1 == p.n_phases) fence_proxy_async();  // generic-proxy stores -> TMA store reads
+        run_phase<T, R, LB, NT>(t, p.ph[ph], p.steps, rcs, gt, group, s, run_off, p.B, refill);
+        if (ph + 1 == p.n_phases) {
+          if (direct) break;
+          fence_proxy_async();  // generic-proxy stores -> TMA store reads
+        }
         group_sync<NT>(group);
       }
-      if (gt < 32) {
+      if (!direct && gt < 32) {
         for (uint32_t j = gt; j < n_runs; j += 32)
           tma_store_run(reinterpret_cast<unsigned char*>(t) + (size_t)j * run_bytes, &map,
                         static_cast<int32_t>(run_start(p, tile, j) / amps_per_row), entry);
         bulk_commit();
+        bulk_wait_read();  // this lane's stores have read the buffer
+        __syncwarp();
+        if (ahead < n_tiles) issue_load(ahead, cur);
       }
-    }
-    const uint64_t ahead = tile + (uint64_t)kStages * step;
-    if (gt < 32) {
-      if constexpr (!PERM) bulk_wait_read();  // this lane's stores have read the buffer
-      __syncwarp();
-      if (ahead < n_tiles) issue_load(ahead, cur);
     }
   }
   if constexpr (!PERM)
@@ -922,22 +957,40 @@ std::vector<TileParams> build_launches(uint32_t n, uint32_t batch, uint32_t B, c
       p.rot_neg[k + 1] = code < 0 ? 1 : 0;  // (c, s) -> (c, -s)
     }
     uint32_t n_steps = 0;
-    for (const PhasePlan& ph : plan.phases) {
+    for (size_t pi = 0; pi < plan.phases.size(); ++pi) {
+      const PhasePlan& ph = plan.phases[pi];
       TilePhase& tp = p.ph[p.n_phases++];
-      const std::vector<uint32_t> tb = thread_bits<T>(ph, R, LB);
+      // the launch's last phase stores straight to HBM when its lanes can be
+      // the run bits 0..B-1 (no register slot there) and the store map keeps
+      // those bits among themselves (a warp then writes one run)
+      bool direct = pi + 1 == plan.phases.size() && !std::getenv("VQF_TILE_NO_DIRECT");
+      for (uint32_t j = 0; j < R; ++j) direct = direct && ph.slot_bit[j] >= B;
+      for (uint32_t b = 0; b < B; ++b) direct = direct && (ph.store.col[b] >> B) == 0;
+      std::vector<uint32_t> tb;
+      if (direct) {
+        for (uint32_t b = 0; b < LB; ++b) {
+          bool reg = false;
+          for (uint32_t j = 0; j < R; ++j) reg = reg || ph.slot_bit[j] == b;
+          if (!reg) tb.push_back(b);
+        }
+      } else {
+        tb = thread_bits<T>(ph, R, LB);
+      }
+      const auto st_map = [&](uint32_t v) { return static_cast<uint16_t>(direct ? v : swz<T>(v)); };
+      tp.direct = direct ? 1 : 0;
       tp.ld_c = static_cast<uint16_t>(swz<T>(ph.load.c));
-      tp.st_c = static_cast<uint16_t>(swz<T>(ph.store.c));
+      tp.st_c = st_map(ph.store.c);
       for (size_t j = 0; j < tb.size(); ++j) {
         tp.ld_tb[j] = static_cast<uint16_t>(swz<T>(ph.load.col[tb[j]]));
-        tp.st_tb[j] = static_cast<uint16_t>(swz<T>(ph.store.col[tb[j]]));
+        tp.st_tb[j] = st_map(ph.store.col[tb[j]]);
       }
       bool same = ph.load.c == ph.store.c;
       for (uint32_t j = 0; j < R; ++j) {
         tp.ld_r[j] = static_cast<uint16_t>(swz<T>(ph.load.col[ph.slot_bit[j]]));
-        tp.st_r[j] = static_cast<uint16_t>(swz<T>(ph.store.col[ph.slot_bit[j]]));
+        tp.st_r[j] = st_map(ph.store.col[ph.slot_bit[j]]);
       }
       for (uint32_t b = 0; b < LB; ++b) same = same && ph.load.col[b] == ph.store.col[b];
-      tp.relayout = same ? 0 : 1;
+      tp.relayout = same || direct ? 0 : 1;
       tp.step0 = static_cast<uint16_t>(n_steps);
       tp.n_steps = static_cast<uint16_t>(ph.steps.size());
       for (const TileStep& st : ph.steps) p.steps[n_steps++] = st;
@@ -1066,7 +1119,8 @@ void plan_tile_counts(uint32_t n_qubits, int32_t dtype, const std::vector<TGate>
         std::fprintf(stderr, "launch %u: k=%u hb=", launches, tp.k);
         for (uint32_t j = 0; j < tp.k; ++j) std::fprintf(stderr, "%u,", tp.hb[j]);
         std::fprintf(stderr, " perm=%u phases=%u:", tp.perm_only, tp.n_phases);
-        for (uint32_t q = 0; q < tp.n_phases; ++q) std::fprintf(stderr, " %u%s", tp.ph[q].n_steps, tp.ph[q].relayout ? "*" : "");
+        for (uint32_t q = 0; q < tp.n_phases; ++q)
+          std::fprintf(stderr, " %u%s%s", tp.ph[q].n_steps, tp.ph[q].relayout ? "*" : "", tp.ph[q].direct ? "d" : "");
         std::fprintf(stderr, "\n");
       }
       ++launches;
