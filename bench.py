@@ -253,7 +253,7 @@ def configs_3_4(V, torch, device, n_big, steps, warmup, peak, cpu_ok, cpu_second
     adjoint, at n = 20 / 24 / 26.  CPU: the reference's apply_gate /
     expectation (one call, single-threaded) at n = 20 and 24 and one
     run_vqe iteration at n = 20, timed concurrently in a thread pool (each
-    call single-threaded; ctypes drops the GIL)."""
+    call single-threaded; ctypes drops the GIL) after the GPU timings."""
     from concurrent.futures import ThreadPoolExecutor
 
     out = {"config4": {}, "config3": {}}
@@ -268,8 +268,8 @@ def configs_3_4(V, torch, device, n_big, steps, warmup, peak, cpu_ok, cpu_second
     pool = ThreadPoolExecutor(6) if ref is not None else None
     cpu_jobs = {}
     if pool is not None:
-        # reference CPU baselines run while the GPU measures (single-threaded
-        # calls; the sample sizes below keep the whole leg within ~30 s)
+        # reference CPU baselines (single-threaded calls; the sample sizes
+        # below keep the whole leg within ~30 s)
         def cpu_kernels(nq):
             psi0 = ref.random_state(20260802, nq)
             r = {"n": nq, "ry_s": ref.time_apply_gate(nq, psi0, 1, 0.3, [nq // 2]),
@@ -287,10 +287,6 @@ def configs_3_4(V, torch, device, n_big, steps, warmup, peak, cpu_ok, cpu_second
             ref.run_vqe(h, kind=1, layers=2, lr=0.05, max_iter=1, init=[0.1] * (2 * nq))
             return time.perf_counter() - t0
 
-        cpu_jobs["kernels20"] = pool.submit(cpu_kernels, 20)
-        cpu_jobs["kernels24"] = pool.submit(cpu_kernels, 24)
-        cpu_jobs["iter20_tfim"] = pool.submit(cpu_iteration, 20, "tfim")
-        cpu_jobs["iter20_random32"] = pool.submit(cpu_iteration, 20, "random32")
 
     def timed(fn, reps):
         with torch.cuda.stream(stream):
@@ -363,6 +359,12 @@ def configs_3_4(V, torch, device, n_big, steps, warmup, peak, cpu_ok, cpu_second
                 row[f"{hname}_{method}_energy"] = r.energy
         out["config3"][f"n{nq}"] = row
     if pool is not None:
+        # after the GPU timings, so host-side launch overheads are not slowed
+        # by the CPU baselines' threads
+        cpu_jobs["kernels20"] = pool.submit(cpu_kernels, 20)
+        cpu_jobs["kernels24"] = pool.submit(cpu_kernels, 24)
+        cpu_jobs["iter20_tfim"] = pool.submit(cpu_iteration, 20, "tfim")
+        cpu_jobs["iter20_random32"] = pool.submit(cpu_iteration, 20, "random32")
         cpu = {k: f.result() for k, f in cpu_jobs.items()}
         pool.shutdown()
         out["cpu_baseline"] = {

@@ -44,10 +44,58 @@
 #include <mutex>
 
 #include "tile.cuh"
+#include "tma.cuh"
 
 namespace vqf {
 
+namespace tma {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  if (fn == nullptr) throw Error(VQF_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap state_map(const vqf_statevector* sv, uint32_t run_bytes) {
+  const bool f64 = sv->dtype == VQF_F64;
+  const uint64_t amp = f64 ? 16 : 8;
+  const cuuint64_t dims[3] = {f64 ? 16u : 32u, (sv->dim() * amp) / 128, sv->batch};
+  const cuuint64_t strides[2] = {128, sv->dim() * amp};
+  const cuuint32_t box[3] = {f64 ? 16u : 32u, run_bytes / 128, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = encode_fn()(&m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                 sv->amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(VQF_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+const CUtensorMap* cached_state_map(const vqf_statevector* sv, uint32_t run_bytes) {
+  static thread_local std::vector<std::pair<std::pair<const void*, uint64_t>, CUtensorMap>> maps;
+  const auto key = std::make_pair(static_cast<const void*>(sv->amps),
+                                  (uint64_t)run_bytes | ((uint64_t)sv->n_qubits << 32) | ((uint64_t)sv->batch << 40) |
+                                      ((uint64_t)sv->dtype << 62));
+  for (auto& e : maps)
+    if (e.first == key) return &e.second;
+  if (maps.size() > 16) maps.erase(maps.begin());
+  maps.emplace_back(key, state_map(sv, run_bytes));
+  return &maps.back().second;
+}
+}  // namespace tma
+
 namespace {
+
+using namespace tma;
 
 constexpr int kMaxRot = 72;     // (cos, sin) entries per launch (kernel parameters stay < 4 KB)
 constexpr int kMaxSteps = 56;   // register steps per launch
@@ -64,10 +112,19 @@ constexpr int kTileBlocks = 148;  // persistent: one CTA per SM
 #ifndef VQF_TILE_LB
 #define VQF_TILE_LB 11  // fp64 tile = 2^11 amplitudes (32 KB); fp32 one bit more
 #endif
-constexpr int kGroups = VQF_TILE_GROUPS;
+#ifndef VQF_TILE_GROUPS32
+#define VQF_TILE_GROUPS32 4  // fp32: 128-thread groups (32 amplitudes per thread over 2^12-amplitude tiles)
+#endif
+#ifndef VQF_TILE_R32
+#define VQF_TILE_R32 5
+#endif
 constexpr int kStages = VQF_TILE_STAGES;
 constexpr int kLB64 = VQF_TILE_LB, kLB32 = VQF_TILE_LB + 1;
-constexpr int kR64 = 4, kR32 = 5;  // register bits per phase (16 / 32 amplitudes per thread)
+constexpr int kR64 = 4, kR32 = VQF_TILE_R32;  // register bits per phase (16 / 32 amplitudes per thread)
+// consumer groups per CTA: 4 x 128 threads (<= 128 registers each); measured for fp32 against
+// 2 x 256 threads with 16 registers of amplitudes (scripts/build_variant.sh): 24.5 vs 33.6 ms per n = 30 layer
+template <typename T>
+constexpr int kGroupsOf = sizeof(T) == 8 ? VQF_TILE_GROUPS : VQF_TILE_GROUPS32;
 constexpr int kB = 5;              // run = 2^5 amplitudes: 512 B fp64 (one TMA box of 4 x 128 B rows)
 
 template <typename T>
@@ -165,75 +222,12 @@ struct TileParams {
 };
 static_assert(sizeof(TileParams) <= 4096, "kernel parameter limit");
 
-__device__ __forceinline__ uint64_t insert_zero64(uint64_t k, uint32_t bit) {
-  const uint64_t low = k & ((uint64_t{1} << bit) - 1);
-  return ((k >> bit) << (bit + 1)) | low;
-}
-
-// ---- TMA / mbarrier helpers (SASS: UTMALDG / UTMASTG / SYNCS)
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-// one run (box {128 B, rows, 1}) of the state, 128 B-swizzled into shared
-// memory; completion counted on the mbarrier
-__device__ __forceinline__ void tma_load_run(void* dst, const CUtensorMap* map, int32_t row, int32_t entry,
-                                             uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(smem_addr(dst)),
-      "l"(map), "r"(0), "r"(row), "r"(entry), "r"(smem_addr(bar))
-      : "memory");
-}
-// the reverse: one run from shared memory (un-swizzled by the map) to HBM
-__device__ __forceinline__ void tma_store_run(const void* src, const CUtensorMap* map, int32_t row, int32_t entry) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(0),
-               "r"(row), "r"(entry), "r"(smem_addr(src))
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// Shared-memory slot of local amplitude L under the TMA 128 B swizzle: the
-// 16-byte chunk index (bits 4..6 of the byte offset) is xor-ed with the
-// 128-byte row index mod 8 (bits 7..9).  Linear over GF(2).
-template <typename T>
-__host__ __device__ __forceinline__ uint32_t swz(uint32_t L) {
-  if (sizeof(T) == 8) return L ^ ((L >> 3) & 7u);   // 16 B amplitude = one chunk
-  return L ^ (((L >> 4) & 7u) << 1);                 // 8 B amplitude: chunk = L >> 1
-}
-
 // Global start index of run j (0 <= j < 2^k) of tile `tile`.
 __device__ __forceinline__ uint64_t run_start(const TileParams& p, uint64_t tile, uint32_t j) {
   uint64_t base = tile << p.B;
   for (uint32_t m = 0; m < p.k; ++m) base = insert_zero64(base, p.hb[m]);
   for (uint32_t m = 0; m < p.k; ++m) base |= (uint64_t)((j >> m) & 1u) << p.hb[m];
   return base;
-}
-
-// Named barrier over the NT threads of one consumer group (id 0 is
-// __syncthreads).
-template <int NT>
-__device__ __forceinline__ void group_sync(uint32_t group) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(NT) : "memory");
 }
 
 // One register phase on the tile t: load the thread's 2^R amplitudes through
@@ -296,10 +290,11 @@ __device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePha
 // group's tile S steps ahead.  Permutation passes write back with 16-byte
 // stores through the affine index map instead.
 template <typename T, int R, int LB, bool PERM>
-__global__ void __launch_bounds__(kGroups << (LB - R), 1)
+__global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
     k_tile(typename V2<T>::type* __restrict__ a, const __grid_constant__ CUtensorMap map,
            const __grid_constant__ TileParams p) {
   using A = typename V2<T>::type;
+  constexpr int kGroups = kGroupsOf<T>;
   constexpr uint32_t NT = 1u << (LB - R), NL = 1u << LB;
   constexpr uint32_t tile_bytes = NL * sizeof(A);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -529,39 +524,6 @@ std::vector<Pass> schedule(uint32_t n, uint32_t B, uint32_t kmax, const std::vec
     passes.push_back(std::move(pass));
   }
   return passes;
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  });
-  if (fn == nullptr) throw Error(VQF_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled unavailable");
-  return fn;
-}
-
-// The state as a 3-d tensor {128 B row, rows, batch entry}; box = one run of
-// 2^B amplitudes (<= 32 rows), 128 B swizzle.  Loads and stores share it.
-CUtensorMap state_map(const vqf_statevector* sv, uint32_t run_bytes) {
-  const bool f64 = sv->dtype == VQF_F64;
-  const uint64_t amp = f64 ? 16 : 8;
-  const cuuint64_t dims[3] = {f64 ? 16u : 32u, (sv->dim() * amp) / 128, sv->batch};
-  const cuuint64_t strides[2] = {128, sv->dim() * amp};
-  const cuuint32_t box[3] = {f64 ? 16u : 32u, run_bytes / 128, 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUtensorMap m;
-  const CUresult r = encode_fn()(&m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-                                 sv->amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Error(VQF_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
-  return m;
 }
 
 // Gate -> (local bits, pair pattern over those bits).
@@ -1013,22 +975,11 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
   // per entry, so give each group >= 16 tiles there to amortise the CTA
   // prologue over enough traffic
   uint64_t gx = std::min<uint64_t>(n_tiles, kTileBlocks);
+  constexpr int kGroups = kGroupsOf<T>;
   if (active > 1) gx = std::max<uint64_t>(1, std::min<uint64_t>(gx, n_tiles / (kGroups * 16)));
   const unsigned grid = static_cast<unsigned>(gx);
   const uint32_t run_bytes = static_cast<uint32_t>(sizeof(typename V2<T>::type) << B);
-  // the encoded map is cached per (state allocation, run size)
-  static thread_local std::vector<std::pair<std::pair<const void*, uint64_t>, CUtensorMap>> maps;
-  const auto key = std::make_pair(static_cast<const void*>(sv->amps),
-                                  (uint64_t)run_bytes | ((uint64_t)n << 32) | ((uint64_t)sv->batch << 40) |
-                                      ((uint64_t)sv->dtype << 62));
-  const CUtensorMap* map = nullptr;
-  for (auto& e : maps)
-    if (e.first == key) map = &e.second;
-  if (map == nullptr) {
-    if (maps.size() > 16) maps.erase(maps.begin());
-    maps.emplace_back(key, state_map(sv, run_bytes));
-    map = &maps.back().second;
-  }
+  const CUtensorMap* map = tma::cached_state_map(sv, run_bytes);
   const size_t smem = kGroups * kStages * (sizeof(typename V2<T>::type) << LB) + 8 * kGroups * kStages + 1024;
   auto* amps = static_cast<typename V2<T>::type*>(sv->amps);
   for (const TileParams& p : build_launches<T>(n, sv->batch, B, gates, pass, cs_dev)) {
@@ -1057,6 +1008,7 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
 
 template <typename T, int R, int LB>
 void opt_in_smem() {
+  constexpr int kGroups = kGroupsOf<T>;
   const int bytes = kGroups * kStages * (static_cast<int>(sizeof(T)) * 2 << LB) + 8 * kGroups * kStages + 1024;
   VQF_CUDA(cudaFuncSetAttribute(k_tile<T, R, LB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   VQF_CUDA(cudaFuncSetAttribute(k_tile<T, R, LB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -1075,8 +1027,11 @@ void ensure_tile_attrs(const vqf_statevector* sv) {
   }
 }
 
-// Registers below one warp-wide tile take one launch per gate.
-bool tile_too_small(uint32_t n, int32_t dtype) { return n < static_cast<uint32_t>(tile_r(dtype) + 5); }
+// Registers below the narrowest instantiated tile (full width - 2 bits, at
+// least one warp per group) take one launch per gate.
+bool tile_too_small(uint32_t n, int32_t dtype) {
+  return n < static_cast<uint32_t>(std::max(tile_lb(dtype) - 2, tile_r(dtype) + 5));
+}
 
 void apply_single(vqf_statevector* sv, const TGate& g, const double* cs_dev) {
   GateArgs ga{g.kind, g.n_wires, {g.wires[0], g.wires[1], g.wires[2], g.wires[3]}, g.c, g.s,
