@@ -1,0 +1,386 @@
+// Multi-group expectation passes over gathered TMA tiles.
+//
+// expectation (statevector.hpp:217-249) = sum over flip groups of
+//   sum_t cb_t sum_i (-1)^popc(i & yz_t) conj(psi_i) psi_{i ^ flip}.
+// A flip group whose flip is ONE index bit q (TFIM's X_q, and any X_q / Y_q
+// string dressed with Z's) pairs amplitudes that differ in bit q only.  A
+// tile pass reads the state once as gathered tiles -- 2^B contiguous
+// amplitudes (one 128-byte row) times the 2^k values of a window of
+// contiguous bits [h, h + k), ONE 4-d TMA box per tile (tma::window_map) --
+// and
+// evaluates every group whose bit is local to the tile: up to kExpPhases
+// register phases, each holding 2^4 amplitudes per thread whose local index
+// differs in 4 register bits, one flip group per register bit.  TFIM at
+// n = 30 needs 4 such passes (plus the diagonal pass) instead of one pass per
+// group.
+//
+// Per pair (i with bit q clear, j = i ^ 2^q) and term t, v = conj(psi_i)
+// psi_j; both directions together give cb_t s_t(i) (v + sigma_t conj(v)) with
+// sigma_t = (-1)^[q in yz_t]: 2 Re(v) or 2i Im(v) (the same split as
+// k_expect_flip in sv.cu).  s_t(i) factorises into the parity of the thread's
+// base index (register bits zero; tile and thread bits) and a 16-bit sign
+// mask over the register slots, precomputed on the host.  Each thread keeps
+// one fp64 accumulator per (phase, slot, term) across all its tiles; at the
+// end the CTA reduces them in a fixed order and writes one complex partial
+// per group -- deterministic, no floating-point atomics.
+//
+// Algorithmic bytes: S per pass (read only).
+#include <algorithm>
+
+#include "expect_tile.cuh"
+#include "tma.cuh"
+
+namespace vqf {
+
+namespace {
+
+using namespace tma;
+
+template <typename T>
+struct V2;
+template <>
+struct V2<double> {
+  using type = double2;
+};
+template <>
+struct V2<float> {
+  using type = float2;
+};
+
+// consumer groups per CTA: fp64 3 x 128 threads, fp32 2 x 256 threads
+template <typename T>
+constexpr int kEGroupsOf = sizeof(T) == 8 ? 3 : 2;
+constexpr int kAcc = kExpPhases * kExpSlots * kExpTerms;
+constexpr int kEBlocks = 148;
+template <typename T>
+constexpr int kELB = sizeof(T) == 8 ? 11 : 12;  // 32 KB tiles
+template <typename T>
+constexpr int kEB = sizeof(T) == 8 ? 3 : 4;  // runs of 128 B
+constexpr int kER = kExpSlots;               // register bits per phase
+
+
+template <typename T, int LB>
+__global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
+    k_expect_tile(const __grid_constant__ CUtensorMap map, const __grid_constant__ ExpTileParams p,
+                  double* __restrict__ partials) {
+  using A = typename V2<T>::type;
+  constexpr int kEGroups = kEGroupsOf<T>;
+  constexpr uint32_t NT = 1u << (LB - kER), NL = 1u << LB, NR = 1u << kER;
+  constexpr uint32_t tile_bytes = NL * sizeof(A);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  const uint32_t group = threadIdx.x / NT, gt = threadIdx.x % NT;
+  A* t = reinterpret_cast<A*>(smem + (size_t)group * tile_bytes);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kEGroups * (size_t)tile_bytes) + group;  // 1 KB gap
+  const uint64_t n_tiles = uint64_t{1} << (p.n - p.B - p.k);
+  const uint32_t mid_bits = p.h - p.B;
+  const uint64_t top_per_entry = uint64_t{1} << (p.n - p.h - p.k);
+  if (gt == 0) {
+    if (group == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // tile T of the entry: mid = low (h - B) bits of T, top = the rest
+  const auto issue_load = [&](uint64_t tile) {
+    if (gt == 0) {
+      mbar_expect_tx(bar, tile_bytes);
+      tma_load_window(t, &map, static_cast<int32_t>(tile & ((uint64_t{1} << mid_bits) - 1)),
+                      static_cast<int32_t>((tile >> mid_bits) + blockIdx.y * top_per_entry), bar);
+    }
+  };
+  const uint64_t step = kEGroups * (uint64_t)gridDim.x;
+  const uint64_t first = blockIdx.x + (uint64_t)group * gridDim.x;
+  if (first < n_tiles) issue_load(first);
+  // one fp64 accumulator per (phase, slot, term) and thread, slot-major in
+  // shared memory behind the tiles (consecutive threads, consecutive words)
+  const uint32_t nthr = blockDim.x;
+  double* acc = reinterpret_cast<double*>(smem + kEGroups * (size_t)tile_bytes + 1024);
+  for (uint32_t q = 0; q < (uint32_t)kAcc; ++q) acc[q * nthr + threadIdx.x] = 0.0;
+  uint64_t tile = first;
+  for (uint32_t it = 0; tile < n_tiles; tile += step, ++it) {
+    mbar_wait(bar, it & 1u);
+    // global index of the tile's local index 0: (top << (h + k)) | (mid << B)
+    const uint64_t g0 = ((tile >> mid_bits) << (p.h + p.k)) | ((tile & ((uint64_t{1} << mid_bits) - 1)) << p.B);
+#pragma unroll
+    for (int ph = 0; ph < kExpPhases; ++ph) {
+      if (ph >= (int)p.n_phases) break;
+      const ExpPhase& P = p.ph[ph];
+      uint32_t base_s = 0, base_l = 0;
+#pragma unroll
+      for (int j = 0; j < LB - kER; ++j)
+        if ((gt >> j) & 1u) {
+          base_s ^= P.tb_s[j];
+          base_l ^= P.tb_l[j];
+        }
+      uint32_t rv[kER];
+#pragma unroll
+      for (int j = 0; j < kER; ++j) rv[j] = P.rv_s[j];
+      A x[NR];
+#pragma unroll
+      for (uint32_t r = 0; r < NR; ++r) {
+        uint32_t o = base_s;
+#pragma unroll
+        for (int j = 0; j < kER; ++j)
+          if (r & (1u << j)) o ^= rv[j];
+        x[r] = t[o];
+      }
+      if (ph + 1 == (int)p.n_phases) {
+        // every thread has read the tile: refill the buffer with the next one
+        group_sync<NT>(group);
+        if (tile + step < n_tiles) issue_load(tile + step);
+      }
+      const uint64_t ib = g0 | ((uint64_t)(base_l >> p.B) << p.h) | (base_l & ((1u << p.B) - 1));
+#pragma unroll
+      for (int j = 0; j < kExpSlots; ++j) {
+        const ExpSlot& S = P.slot[j];
+        if (S.n_terms == 0) continue;
+        double re[NR / 2], im[NR / 2];
+#pragma unroll
+        for (uint32_t r = 0, q = 0; r < NR; ++r) {
+          if (r & (1u << j)) continue;
+          const A a = x[r], b = x[r | (1u << j)];
+          re[q] = static_cast<double>(fma(a.x, b.x, a.y * b.y));
+          im[q] = static_cast<double>(fma(a.x, b.y, -(a.y * b.x)));
+          ++q;
+        }
+#pragma unroll
+        for (int k = 0; k < kExpTerms; ++k) {
+          if (k >= (int)S.n_terms) break;
+          const uint32_t sm = S.smask[k];
+          const bool use_im = S.sigma[k] != 0;
+          double part = 0.0;
+#pragma unroll
+          for (uint32_t r = 0, q = 0; r < NR; ++r) {
+            if (r & (1u << j)) continue;
+            const double v = use_im ? im[q] : re[q];
+            part += ((sm >> r) & 1u) ? -v : v;
+            ++q;
+          }
+          acc[((ph * kExpSlots + j) * kExpTerms + k) * nthr + threadIdx.x] += (__popcll(ib & S.yz[k]) & 1) ? -part : part;
+        }
+      }
+    }
+  }
+  // fixed-order CTA reduction of the accumulators
+  __syncthreads();
+  const double* red = acc;
+  __shared__ double term_sum[kAcc];
+  if (threadIdx.x < (uint32_t)kAcc) {
+    double s = 0.0;
+    for (uint32_t q = 0; q < nthr; ++q) s += red[threadIdx.x * nthr + q];
+    term_sum[threadIdx.x] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < (uint32_t)(kExpPhases * kExpSlots)) {
+    const uint32_t ph = threadIdx.x / kExpSlots, j = threadIdx.x % kExpSlots;
+    if (ph < p.n_phases) {
+      const ExpSlot& S = p.ph[ph].slot[j];
+      if (S.n_terms) {
+        double er = 0.0, ei = 0.0;
+        for (uint32_t k = 0; k < S.n_terms; ++k) {
+          const double v = 2.0 * term_sum[(ph * kExpSlots + j) * kExpTerms + k];
+          if (S.sigma[k]) {  // cb * (i v)
+            er -= S.cb_im[k] * v;
+            ei += S.cb_re[k] * v;
+          } else {  // cb * v
+            er += S.cb_re[k] * v;
+            ei += S.cb_im[k] * v;
+          }
+        }
+        const size_t idx = ((size_t)blockIdx.y * p.G + S.group) * p.nb + blockIdx.x;
+        partials[2 * idx] = er;
+        partials[2 * idx + 1] = ei;
+      }
+    }
+  }
+}
+
+template <typename T>
+size_t exp_smem_bytes() {
+  constexpr int LB = kELB<T>;
+  constexpr int kEGroups = kEGroupsOf<T>;
+  const size_t tiles = kEGroups * (sizeof(typename V2<T>::type) << LB);
+  const size_t accs = sizeof(double) * kAcc * (kEGroups << (LB - kER));
+  return 1024 + tiles + 1024 + accs;  // align slack, tiles, mbarriers (in the 1 KB gap), accumulators
+}
+
+uint32_t bank_of_local(bool f64, uint32_t L) {
+  return f64 ? (tma::swz<double>(L) & 7u) : (tma::swz<float>(L) & 15u);
+}
+
+uint32_t rank_gf2(std::vector<uint32_t> v) {
+  uint32_t rank = 0;
+  for (uint32_t bit = 0; bit < 32; ++bit) {
+    size_t piv = v.size();
+    for (size_t i = rank; i < v.size(); ++i)
+      if ((v[i] >> bit) & 1u) {
+        piv = i;
+        break;
+      }
+    if (piv == v.size()) continue;
+    std::swap(v[rank], v[piv]);
+    for (size_t i = 0; i < v.size(); ++i)
+      if (i != rank && ((v[i] >> bit) & 1u)) v[i] ^= v[rank];
+    ++rank;
+  }
+  return rank;
+}
+
+}  // namespace
+
+std::vector<ExpTileParams> plan_expect_tiles(const CompiledHam& h, uint32_t n, int32_t dtype,
+                                             std::vector<char>& taken) {
+  const bool f64 = dtype == VQF_F64;
+  const uint32_t LB = f64 ? kELB<double> : kELB<float>;
+  const uint32_t B = f64 ? kEB<double> : kEB<float>;
+  const uint32_t K = LB - B;
+  const uint32_t G = static_cast<uint32_t>(h.group_flip.size());
+  taken.assign(G, 0);
+  std::vector<ExpTileParams> out;
+  if (n < LB || std::getenv("VQF_NO_EXPECT_TILES")) return out;
+  // candidate groups by flip bit
+  std::vector<std::pair<uint32_t, uint32_t>> cand;  // (bit, group)
+  for (uint32_t g = 1; g < G; ++g) {
+    const uint64_t f = h.group_flip[g];
+    const uint32_t cnt = h.group_offset[g + 1] - h.group_offset[g];
+    if (cnt == 0 || cnt > (uint32_t)kExpTerms || __builtin_popcountll(f) != 1) continue;
+    cand.emplace_back(static_cast<uint32_t>(__builtin_ctzll(f)), g);
+  }
+  // a pass needs at least two groups to beat the per-group kernels
+  if (cand.size() < 2) return out;
+  std::sort(cand.begin(), cand.end());
+  const uint32_t cap = kExpPhases * kExpSlots;
+  size_t next = 0;
+  while (next < cand.size()) {
+    // window [hw, hw + K): from the lowest uncovered group bit (>= B), kept
+    // inside the register; groups below B ride along in every pass
+    const uint32_t lo = std::max<uint32_t>(B, cand[next].first);
+    const uint32_t hw = std::min<uint32_t>(lo, n - K);
+    std::vector<std::pair<uint32_t, uint32_t>> mine;
+    while (next < cand.size() && mine.size() < cap) {
+      const uint32_t bit = cand[next].first;
+      if (bit >= B && (bit < hw || bit >= hw + K)) break;
+      mine.push_back(cand[next++]);
+    }
+    if (mine.size() < 2 && !out.empty()) break;  // a lone leftover: the per-group kernels
+    const auto local = [&](uint32_t bit) -> uint32_t {
+      if (bit < B) return bit;
+      if (bit >= hw && bit < hw + K) return B + bit - hw;
+      throw Error(VQF_LOGIC_ERROR, "expectation tile: bit outside the pass");
+    };
+    const auto global_of = [&](uint32_t lb) { return lb < B ? lb : hw + lb - B; };
+    ExpTileParams p{};
+    p.n = n;
+    p.B = B;
+    p.k = K;
+    p.h = hw;
+    for (size_t c0 = 0; c0 < mine.size(); c0 += kExpSlots) {
+      ExpPhase& P = p.ph[p.n_phases++];
+      uint32_t regs[kExpSlots], used = 0;
+      size_t m = std::min<size_t>(kExpSlots, mine.size() - c0);
+      for (size_t q = 0; q < m; ++q) {
+        regs[q] = local(mine[c0 + q].first);
+        used |= 1u << regs[q];
+      }
+      for (int b = static_cast<int>(LB) - 1; b >= 0 && m < (size_t)kExpSlots; --b)
+        if (!((used >> b) & 1u)) {
+          regs[m++] = static_cast<uint32_t>(b);
+          used |= 1u << b;
+        }
+      // thread bits: lanes of one shared-memory wavefront on distinct banks
+      std::vector<uint32_t> fr;
+      for (uint32_t b = 0; b < LB; ++b)
+        if (!((used >> b) & 1u)) fr.push_back(b);
+      const uint32_t q = f64 ? 3 : 4;
+      std::vector<uint32_t> best;
+      uint32_t best_rank = 0;
+      for (uint32_t mask = 0; mask < (1u << fr.size()); ++mask) {
+        if (static_cast<uint32_t>(__builtin_popcount(mask)) != q) continue;
+        std::vector<uint32_t> pick, vecs;
+        for (size_t i = 0; i < fr.size(); ++i)
+          if ((mask >> i) & 1u) {
+            pick.push_back(fr[i]);
+            vecs.push_back(bank_of_local(f64, 1u << fr[i]));
+          }
+        const uint32_t r = rank_gf2(vecs);
+        if (best.empty() || r > best_rank) {
+          best = pick;
+          best_rank = r;
+        }
+      }
+      std::vector<uint32_t> tb = best;
+      for (uint32_t b : fr)
+        if (std::find(tb.begin(), tb.end(), b) == tb.end()) tb.push_back(b);
+      for (size_t j = 0; j < tb.size(); ++j) {
+        P.tb_s[j] = static_cast<uint16_t>(f64 ? tma::swz<double>(1u << tb[j]) : tma::swz<float>(1u << tb[j]));
+        P.tb_l[j] = static_cast<uint16_t>(1u << tb[j]);
+      }
+      for (uint32_t j = 0; j < (uint32_t)kExpSlots; ++j)
+        P.rv_s[j] = static_cast<uint16_t>(f64 ? tma::swz<double>(1u << regs[j]) : tma::swz<float>(1u << regs[j]));
+      for (size_t s = 0; s < std::min<size_t>(kExpSlots, mine.size() - c0); ++s) {
+        const uint32_t g = mine[c0 + s].second;
+        ExpSlot& S = P.slot[s];
+        S.group = g;
+        S.n_terms = h.group_offset[g + 1] - h.group_offset[g];
+        const uint64_t f = h.group_flip[g];
+        for (uint32_t k = 0; k < S.n_terms; ++k) {
+          const MaskTerm& mt = h.terms[h.group_offset[g] + k];
+          S.cb_re[k] = mt.cb_re;
+          S.cb_im[k] = mt.cb_im;
+          S.sigma[k] = __builtin_popcountll(f & mt.yz) & 1;
+          // register-slot part of yz: slot j's local bit regs[j] -> global bit
+          uint32_t ysl = 0;
+          for (uint32_t j = 0; j < (uint32_t)kExpSlots; ++j) {
+            const uint32_t gb = global_of(regs[j]);
+            if ((mt.yz >> gb) & 1u) ysl |= 1u << j;
+          }
+          uint32_t sm = 0;
+          for (uint32_t r = 0; r < 16; ++r)
+            if (__builtin_popcount(r & ysl) & 1) sm |= 1u << r;
+          S.smask[k] = sm;
+          // the thread's base index has zeros on the register bits, so the
+          // full mask gives the tile / thread parity
+          S.yz[k] = mt.yz;
+        }
+        taken[g] = 1;
+      }
+    }
+    out.push_back(p);
+  }
+  return out;
+}
+
+namespace {
+template <typename T>
+void launch_t(vqf_statevector* sv, std::vector<ExpTileParams>& passes, double* partials, uint32_t G, uint32_t nb) {
+  constexpr int LB = kELB<T>;
+  static thread_local int opted = -1;
+  if (opted != sv->device) {
+    VQF_CUDA(cudaFuncSetAttribute(k_expect_tile<T, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(exp_smem_bytes<T>())));
+    opted = sv->device;
+  }
+  const uint64_t n_tiles = uint64_t{1} << (sv->n_qubits - LB);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>({n_tiles, (uint64_t)kEBlocks, (uint64_t)nb}));
+  for (ExpTileParams& p : passes) {
+    p.G = G;
+    p.nb = nb;
+    const CUtensorMap* map = tma::cached_window_map(sv, p.h, p.k);
+    k_expect_tile<T, LB><<<dim3(grid, sv->batch), kEGroupsOf<T> << (LB - kER), exp_smem_bytes<T>(), sv->stream>>>(
+        *map, p, partials);
+    VQF_LAUNCHED();
+  }
+}
+}  // namespace
+
+void launch_expect_tiles(vqf_statevector* sv, std::vector<ExpTileParams> passes, double* partials, uint32_t G,
+                         uint32_t nb) {
+  if (passes.empty()) return;
+  if (sv->dtype == VQF_F64)
+    launch_t<double>(sv, passes, partials, G, nb);
+  else
+    launch_t<float>(sv, passes, partials, G, nb);
+}
+
+}  // namespace vqf

@@ -15,6 +15,7 @@
 #include <mutex>
 #include <utility>
 
+#include "expect_tile.cuh"
 #include "sv.cuh"
 #include "tile.cuh"
 
@@ -968,14 +969,18 @@ struct ExpPlan {
     bool need_im;
   };
   std::vector<FactFlip> fact;  // single groups on k_expect_flip_fact (top flip bit >= 11)
+  std::vector<ExpTileParams> tiles;  // single-bit flip groups on k_expect_tile passes (expect_tile.cu)
   uint32_t state_passes() const {
-    return (diag != DIAG_NONE ? 1u : 0u) + static_cast<uint32_t>(multi.size() + single.size() + fact.size());
+    return (diag != DIAG_NONE ? 1u : 0u) +
+           static_cast<uint32_t>(multi.size() + single.size() + fact.size() + tiles.size());
   }
 };
 
-ExpPlan plan_expectation(const CompiledHam& h, uint32_t n) {
+ExpPlan plan_expectation(const CompiledHam& h, uint32_t n, int32_t dtype = VQF_F64) {
   ExpPlan pl;
   const uint32_t G = static_cast<uint32_t>(h.group_flip.size());
+  std::vector<char> on_tiles;
+  pl.tiles = plan_expect_tiles(h, n, dtype, on_tiles);
   pl.all = h.terms;
   if (G > 0 && h.group_offset[1] > h.group_offset[0]) {
     // tiled split: support all below / all above the 2048-amplitude tile, mixed
@@ -1030,7 +1035,7 @@ ExpPlan plan_expectation(const CompiledHam& h, uint32_t n) {
   }
   for (uint32_t g = 1; g < G; ++g) {
     const uint32_t cnt = h.group_offset[g + 1] - h.group_offset[g];
-    if (cnt == 0) continue;
+    if (cnt == 0 || on_tiles[g]) continue;
     const uint64_t out = h.group_flip[g] & ~uint64_t{31};
     if (n < 5 + kRegBits || cnt > (uint32_t)kMultiMaxTerms || __builtin_popcountll(out) > kRegBits) {
       pl.single.push_back(g);
@@ -1144,7 +1149,7 @@ void expectation_t(vqf_statevector* sv, const CompiledHam& h, double* dev_out) {
   const uint32_t nb = std::max(nb_diag, nb_flip);
   ensure_partials(sv, 2 * (size_t)sv->batch * G * nb);
   VQF_CUDA(cudaMemsetAsync(sv->partials, 0, 2 * sizeof(double) * sv->batch * G * nb, sv->stream));
-  const ExpPlan pl = plan_expectation(h, n);
+  const ExpPlan pl = plan_expectation(h, n, sv->dtype);
   ensure_terms(sv, std::max<size_t>(1, pl.all.size()) * sizeof(MaskTerm));
   if (!pl.all.empty())
     VQF_CUDA(cudaMemcpyAsync(sv->terms_dev, pl.all.data(), pl.all.size() * sizeof(MaskTerm), cudaMemcpyHostToDevice,
@@ -1175,6 +1180,7 @@ void expectation_t(vqf_statevector* sv, const CompiledHam& h, double* dev_out) {
       break;
     case ExpPlan::DIAG_NONE: break;
   }
+  launch_expect_tiles(sv, pl.tiles, sv->partials, G, nb);
   for (const uint32_t g : pl.single) {
     const uint32_t t0 = h.group_offset[g], cnt = h.group_offset[g + 1] - t0;
     const uint64_t f = h.group_flip[g];
@@ -1509,7 +1515,7 @@ int vqf_expectation_plan(const vqf_hamiltonian* h, uint32_t* state_passes, uint3
     for (size_t g = 1; g < c.group_flip.size(); ++g) groups += c.group_offset[g + 1] > c.group_offset[g] ? 1 : 0;
     if (state_passes) *state_passes = pl.state_passes();
     if (flip_groups) *flip_groups = groups;
-    if (multi_passes) *multi_passes = static_cast<uint32_t>(pl.multi.size());
+    if (multi_passes) *multi_passes = static_cast<uint32_t>(pl.multi.size() + pl.tiles.size());
   });
 }
 

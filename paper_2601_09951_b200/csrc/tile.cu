@@ -91,6 +91,42 @@ const CUtensorMap* cached_state_map(const vqf_statevector* sv, uint32_t run_byte
   maps.emplace_back(key, state_map(sv, run_bytes));
   return &maps.back().second;
 }
+// Window map: the state as {128 B row, mid, window, top x batch} for a tile
+// made of the B low bits (one 128 B row) and the k contiguous bits [h, h + k):
+// dims {elements per row, 2^(h - B), 2^k, 2^(n - h - k) * batch}, box
+// {elements per row, 1, 2^k, 1}, so one TMA instruction moves a whole tile.
+CUtensorMap window_map(const vqf_statevector* sv, uint32_t h, uint32_t k) {
+  const bool f64 = sv->dtype == VQF_F64;
+  const uint64_t amp = f64 ? 16 : 8, per_row = 128 / amp;
+  const uint32_t B = f64 ? 3 : 4;
+  const uint32_t n = sv->n_qubits;
+  if (h < B || h + k > n || k > 8) throw Error(VQF_LOGIC_ERROR, "window map: bad window");
+  const cuuint64_t dims[4] = {f64 ? 16u : 32u, uint64_t{1} << (h - B), uint64_t{1} << k,
+                              (uint64_t{1} << (n - h - k)) * sv->batch};
+  const cuuint64_t strides[3] = {128, (uint64_t{1} << h) * amp, (uint64_t{1} << (h + k)) * amp};
+  const cuuint32_t box[4] = {f64 ? 16u : 32u, 1, 1u << k, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  (void)per_row;
+  CUtensorMap m;
+  const CUresult r = encode_fn()(&m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                                 sv->amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(VQF_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+const CUtensorMap* cached_window_map(const vqf_statevector* sv, uint32_t h, uint32_t k) {
+  static thread_local std::vector<std::pair<std::pair<const void*, uint64_t>, CUtensorMap>> maps;
+  const auto key = std::make_pair(static_cast<const void*>(sv->amps),
+                                  (uint64_t)h | ((uint64_t)k << 8) | ((uint64_t)sv->n_qubits << 16) |
+                                      ((uint64_t)sv->batch << 24) | ((uint64_t)sv->dtype << 62));
+  for (auto& e : maps)
+    if (e.first == key) return &e.second;
+  if (maps.size() > 64) maps.erase(maps.begin());
+  maps.emplace_back(key, window_map(sv, h, k));
+  return &maps.back().second;
+}
 }  // namespace tma
 
 namespace {

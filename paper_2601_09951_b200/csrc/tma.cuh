@@ -87,5 +87,20 @@ CUtensorMap state_map(const vqf_statevector* sv, uint32_t run_bytes);
 // Cached per (allocation, run size, shape) on the calling thread.
 const CUtensorMap* cached_state_map(const vqf_statevector* sv, uint32_t run_bytes);
 
+// Window map of a tile = B low bits (one 128 B row; B = 3 fp64, 4 fp32) x the
+// contiguous bits [h, h + k): one TMA box per tile (cached per thread).
+CUtensorMap window_map(const vqf_statevector* sv, uint32_t h, uint32_t k);
+const CUtensorMap* cached_window_map(const vqf_statevector* sv, uint32_t h, uint32_t k);
+
+// One tile of a window map: coordinates {0, mid, 0, top}.
+__device__ __forceinline__ void tma_load_window(void* dst, const CUtensorMap* map, int32_t mid, int32_t top,
+                                                uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(0), "r"(mid), "r"(0), "r"(top), "r"(smem_addr(bar))
+      : "memory");
+}
+
 }  // namespace tma
 }  // namespace vqf

@@ -715,3 +715,30 @@ def test_f32_scaling_study(gpu, ref):
     for r, w in zip(recs, want):
         assert r["state_bytes"] == (1 << r["n_qubits"]) * 8
         assert abs(r["final_energy"] - w["final_energy"]) < F32_E_TOL and r["iterations_run"] == 2
+
+
+@pytest.mark.parametrize("n,dtype", [(11, "f64"), (14, "f64"), (20, "f64"), (12, "f32"), (17, "f32")])
+def test_expectation_tile_passes_single_bit_flips(gpu, orc, n, dtype):
+    """Single-bit flip groups (X_q / Y_q dressed with Z's, one or two terms
+    per group) go through the gathered-tile multi-group passes
+    (expect_tile.cu); every bit position, Y signs, complex phases and the
+    tile-constant parity against the oracle."""
+    V = gpu
+    pr = random.Random(500 + n)
+    terms = []
+    for q in range(n):
+        dress = sorted(pr.sample([w for w in range(n) if w != q], min(3, n - 1)))
+        terms.append((pr.uniform(-2, 2), [(q, 1)]))                                     # X_q
+        if q % 2 == 0:
+            axes = sorted([(q, 2)] + [(w, 3) for w in dress])                          # Y_q Z...
+            terms.append((pr.uniform(-2, 2), axes))
+    terms += [(0.7, [(0, 3), (n - 1, 3)]), (-0.3, [])]
+    h = orc.canonicalize(Ham(n, terms))
+    psi0 = random_state(np.random.default_rng(n), n)
+    psi = V.StateVector(n, dtype=dtype)
+    psi.amplitudes = psi0
+    got = V.expectation(psi, to_v(V, h))
+    want = orc.expectation(n, psi0, h)
+    assert abs(got - want) < (E_TOL if dtype == "f64" else 1e-5 * max(1.0, abs(want)))
+    plan = V.expectation_plan(to_v(V, h))
+    assert plan["state_passes"] < n  # groups share tile passes
