@@ -21,6 +21,7 @@
 #include "pauli_host.h"
 #include "sv.cuh"
 #include "tile.cuh"
+#include "vqe_block.cuh"
 #include "vqe_small.cuh"
 
 namespace vqf {
@@ -741,7 +742,199 @@ void run_vqe_hbm(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const 
   if (r->theta) std::memcpy(r->theta, theta.data(), P * sizeof(double));
 }
 
-bool small_ok(uint32_t n, uint32_t P) { return n <= (uint32_t)kSmallMaxN && P <= (uint32_t)kSmallMaxP; }
+// One warp holds the problem with <= 16 amplitudes per lane (32 would spill:
+// 5-qubit registers with >= 8 parameters take the shared-memory engine).
+bool small_ok(uint32_t n, uint32_t P) {
+  return n <= (uint32_t)kSmallMaxN && P <= (uint32_t)kSmallMaxP &&
+         small_amps_per_lane(static_cast<int>(n), static_cast<int>(P)) <= 16;
+}
+
+// Engine override for diagnostics and cross-engine tests: VQF_ENGINE =
+// warp | block | hbm (default: the fastest engine that holds the problem).
+const char* engine_override() {
+  const char* e = std::getenv("VQF_ENGINE");
+  return (e && *e) ? e : nullptr;
+}
+
+bool block_ok(int32_t kind, uint32_t n, uint32_t P, int32_t dtype) {
+  return kind == VQF_ANSATZ_HARDWARE_EFFICIENT && n >= (uint32_t)kBlockMinN && n <= (uint32_t)block_max_n(dtype) &&
+         P <= (uint32_t)kBlockMaxP;
+}
+
+// 1 - beta^t for t = 1..T, interleaved (bc1, bc2), by the host libm pow as
+// adam_step computes them (vqe.hpp:161-162); cached per (beta1, beta2, T).
+std::vector<double> raw_bias_tables(const vqf_adam_config& c, int32_t T) {
+  struct Entry {
+    double b1, b2;
+    int32_t T;
+    std::vector<double> bc;
+  };
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<Entry>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& e : cache)
+    if (e->b1 == c.beta1 && e->b2 == c.beta2 && e->T == T) return e->bc;
+  auto e = std::make_unique<Entry>();
+  e->b1 = c.beta1;
+  e->b2 = c.beta2;
+  e->T = T;
+  e->bc.assign(2 * static_cast<size_t>(std::max(T, 1)), 0.0);
+  for (int32_t t = 1; t <= T; ++t) {
+    e->bc[2 * (t - 1)] = 1.0 - std::pow(c.beta1, static_cast<double>(t));
+    e->bc[2 * (t - 1) + 1] = 1.0 - std::pow(c.beta2, static_cast<double>(t));
+  }
+  if (cache.size() >= 16) cache.erase(cache.begin());
+  cache.push_back(std::move(e));
+  return cache.back()->bc;
+}
+
+// Barrier words of the shared-memory engine, one per (thread, device):
+// zeroed once, reset by the kernel's last CTA (or here after an abort).
+unsigned* block_barrier(int device) {
+  thread_local std::vector<std::pair<int, unsigned*>> words;
+  for (const auto& w : words)
+    if (w.first == device) return w.second;
+  unsigned* d = nullptr;
+  VQF_CUDA(cudaMalloc(&d, 4 * sizeof(unsigned)));
+  VQF_CUDA(cudaMemset(d, 0, 4 * sizeof(unsigned)));
+  words.emplace_back(device, d);
+  return d;
+}
+
+// Shared-memory engine (vqe_block.cu): the whole run_vqe in one cooperative
+// launch.  Inputs ride in the kernel parameter block when they fit
+// (kBlockInline bytes), else go up in one H2D copy; results are written by
+// the kernel straight into mapped pinned memory.
+void run_vqe_block(const CompiledHam& ch, int32_t kind, uint32_t layers, const vqf_adam_config& cfg,
+                   const std::vector<double>& init, int device, vqf_vqe_result* r, int32_t dtype) {
+  const uint32_t n = ch.n_qubits;
+  const uint32_t P = ansatz_params(kind, layers, n);
+  const int NC = 2 * static_cast<int>(P) + 1;
+  HMARK("block:enter");
+  const BlockProgram prog = compile_block_program(kind, layers, n, ch, dtype);
+  HMARK("compile");
+  const int32_t T = cfg.max_iterations;
+  const std::vector<double> bc = raw_bias_tables(cfg, T);
+  Workspace& ws = workspace(device);
+  VQF_CUDA(cudaSetDevice(device));
+  HMARK("bias+ws");
+  Carver c;  // inputs
+  const size_t o_bc = c.take<double>(bc.size());
+  const size_t o_pass = c.take<BlockPass>(prog.passes.size());
+  const size_t o_gf = c.take<uint32_t>(prog.group_flip.size());
+  const size_t o_go = c.take<uint32_t>(prog.group_off.size());
+  const size_t o_terms = c.take<BlockTerm>(prog.herm ? 0 : prog.terms.size());  // complex form: non-Hermitian only
+  const size_t o_rterms = c.take<BlockRTerm>(prog.rterms.size());
+  const size_t o_init = c.take<double>(init.size());
+  const size_t in_end = c.off;
+  const bool inl = in_end <= static_cast<size_t>(kBlockInline);
+  Carver oc;  // outputs (mapped pinned), after the staged inputs
+  oc.off = inl ? 0 : in_end;
+  const size_t o_energy = oc.take<double>(1);
+  const size_t o_theta = oc.take<double>(P);
+  const size_t o_traj = oc.take<double>(static_cast<size_t>(std::max(T, 0)) + 1);
+  const size_t o_iters = oc.take<int32_t>(1);
+  const size_t o_conv = oc.take<int32_t>(1);
+  const size_t o_status = oc.take<int32_t>(1);
+  const size_t o_errv = oc.take<double>(1);
+  const size_t o_erri = oc.take<int32_t>(1);
+  const size_t o_errt = oc.take<double>(P);
+  const size_t o_clk = oc.take<uint64_t>(2);
+  const size_t pin_total = oc.off;
+  Carver dc;  // device scratch: staged inputs, then the energy exchange
+  dc.off = inl ? 0 : in_end;
+  const size_t o_E = dc.take<double2>(2 * static_cast<size_t>(NC));
+  ws.reserve(dc.off, pin_total);
+  auto* pin = static_cast<unsigned char*>(ws.pin);
+  auto* dev = static_cast<unsigned char*>(ws.dev);
+  static thread_local BlockArgs args;  // 8 KB: not on the stack
+  unsigned char* in = inl ? args.blob : pin;
+  auto put = [&](size_t off, const void* src, size_t bytes) {
+    if (bytes) std::memcpy(in + off, src, bytes);
+  };
+  put(o_bc, bc.data(), bc.size() * sizeof(double));
+  put(o_pass, prog.passes.data(), prog.passes.size() * sizeof(BlockPass));
+  put(o_gf, prog.group_flip.data(), prog.group_flip.size() * sizeof(uint32_t));
+  put(o_go, prog.group_off.data(), prog.group_off.size() * sizeof(uint32_t));
+  if (!prog.herm) put(o_terms, prog.terms.data(), prog.terms.size() * sizeof(BlockTerm));
+  put(o_rterms, prog.rterms.data(), prog.rterms.size() * sizeof(BlockRTerm));
+  put(o_init, init.data(), init.size() * sizeof(double));
+  std::memset(pin + (inl ? 0 : in_end), 0, pin_total - (inl ? 0 : in_end));
+  // input addresses: device pointers (staged) or offsets into args.blob
+  const auto src = [&](size_t off) -> const unsigned char* {
+    return inl ? reinterpret_cast<const unsigned char*>(off) : dev + off;
+  };
+  BlockParams& p = args.p;
+  p = BlockParams{};
+  args.inl = inl ? 1 : 0;
+  p.n = static_cast<int32_t>(n);
+  p.P = static_cast<int32_t>(P);
+  p.NC = NC;
+  p.max_iterations = T;
+  p.has_tol = cfg.has_gradient_tolerance;
+  p.dtype = dtype;
+  p.tol = cfg.gradient_tolerance;
+  p.lr = cfg.learning_rate;
+  p.beta1 = cfg.beta1;
+  p.beta2 = cfg.beta2;
+  p.eps = cfg.epsilon;
+  p.bc = reinterpret_cast<const double*>(src(o_bc));
+  p.passes = reinterpret_cast<const BlockPass*>(src(o_pass));
+  p.n_passes = static_cast<int32_t>(prog.passes.size());
+  p.init_index = prog.init_index;
+  p.group_flip = reinterpret_cast<const uint32_t*>(src(o_gf));
+  p.group_off = reinterpret_cast<const uint32_t*>(src(o_go));
+  p.n_groups = static_cast<int32_t>(prog.group_flip.size());
+  p.terms = reinterpret_cast<const BlockTerm*>(src(o_terms));
+  p.herm = prog.herm ? 1 : 0;
+  p.n_terms = static_cast<int32_t>(prog.terms.size());
+  p.obytes = prog.obytes;
+  p.team_lanes = static_cast<int32_t>(prog.lanes);
+  p.rterms = reinterpret_cast<const BlockRTerm*>(src(o_rterms));
+  p.init_theta = init.empty() ? nullptr : reinterpret_cast<const double*>(src(o_init));
+  p.energies = reinterpret_cast<double2*>(dev + o_E);
+  p.barrier = block_barrier(device);
+  p.energy = reinterpret_cast<double*>(pin + o_energy);
+  p.theta_out = reinterpret_cast<double*>(pin + o_theta);
+  p.traj = reinterpret_cast<double*>(pin + o_traj);
+  p.iters = reinterpret_cast<int32_t*>(pin + o_iters);
+  p.converged = reinterpret_cast<int32_t*>(pin + o_conv);
+  p.status = reinterpret_cast<int32_t*>(pin + o_status);
+  p.err_val = reinterpret_cast<double*>(pin + o_errv);
+  p.err_iter = reinterpret_cast<int32_t*>(pin + o_erri);
+  p.err_theta = reinterpret_cast<double*>(pin + o_errt);
+  p.clk = reinterpret_cast<unsigned long long*>(pin + o_clk);
+  const int grid = block_grid(prog, dtype, NC, device);
+  HMARK("stage");
+  if (!inl) VQF_CUDA(cudaMemcpyAsync(dev, pin, in_end, cudaMemcpyHostToDevice, ws.stream));
+  launch_vqe_block(args, in_end, prog, grid, ws.stream);
+  HMARK("launch");
+  VQF_CUDA(cudaStreamSynchronize(ws.stream));
+  HMARK("sync");
+  const int32_t st = *p.status;
+  if (st == kStatusAbort) {
+    VQF_CUDA(cudaMemset(p.barrier, 0, 4 * sizeof(unsigned)));
+    throw Error(VQF_CUDA_ERROR, "block engine: grid barrier timed out");
+  }
+  if (st == kStatusImag) throw_runtime(imag_msg(*p.err_val));
+  if (st == kStatusNonFinite) throw_runtime(nonfinite_msg(*p.err_iter, p.err_theta, P));
+  if (st != kStatusOk) throw Error(VQF_LOGIC_ERROR, "block engine: status " + std::to_string(st));
+  const int32_t it = *p.iters;
+  const bool conv = *p.converged != 0;
+  const uint32_t len = conv ? static_cast<uint32_t>(it) + 1 : static_cast<uint32_t>(T) + 1;
+  r->energy = *p.energy;
+  if (r->theta) std::memcpy(r->theta, p.theta_out, P * sizeof(double));
+  if (r->trajectory) {
+    if (r->trajectory_capacity < len) throw_invalid("vqe_result: trajectory capacity too small");
+    std::memcpy(r->trajectory, p.traj, len * sizeof(double));
+  }
+  r->trajectory_len = len;
+  r->iterations_run = it;
+  const uint64_t grads = conv ? static_cast<uint64_t>(it) + 1 : static_cast<uint64_t>(T);
+  r->circuit_evaluations = grads * (1 + 2 * (uint64_t)P) + (conv ? 0 : 1);
+  HMARK("results");
+  HDUMP();
+}
 
 // Storage precision of the engine's states.  complex64 (VQF_F32) runs
 // fixed-iteration only: fp32 rounding cannot reproduce the reference's
@@ -771,7 +964,13 @@ void run_vqe_impl(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const
   // it to rounding but pays one HBM-engine launch per gate there, so small
   // registers take this path for either method (fp64 only: the register
   // engine holds complex128 amplitudes)
-  if (dtype == VQF_F64 && small_ok(n, P)) {
+  const char* eng = engine_override();
+  const bool want_warp = eng ? std::strcmp(eng, "warp") == 0 : true;
+  const bool want_block = eng ? std::strcmp(eng, "block") == 0 : true;
+  // hardware-efficient registers of >= 4 qubits: the shared-memory engine
+  // (teams of lanes per circuit) beats the one-warp register engine
+  const bool block_first = block_ok(kind, n, P, dtype) && !eng;
+  if (dtype == VQF_F64 && small_ok(n, P) && want_warp && !block_first) {
     SmallJob j;
     j.batch = 1;
     j.n_qubits = static_cast<int32_t>(n);
@@ -786,6 +985,12 @@ void run_vqe_impl(const vqf_hamiltonian* h, int32_t kind, uint32_t layers, const
     run_small(j, device);
     if (j.status[0] != kStatusOk) throw_runtime(small_error(j, 0, 0.0));
     fill_result(j, 0, r);
+  } else if (block_ok(kind, n, P, dtype) && want_block) {
+    // one cooperative launch per run (parameter-shift gradients, also for
+    // method = adjoint: equal to rounding, and the shifted circuits run in
+    // parallel CTAs)
+    HMARK("impl:enter");
+    run_vqe_block(compile_hamiltonian(h), kind, layers, *cfg, init_v, device, r, dtype);
   } else {
     run_vqe_hbm(h, kind, layers, *cfg, init_v, method, device, r, dtype);
   }

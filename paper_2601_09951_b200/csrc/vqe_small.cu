@@ -1055,8 +1055,10 @@ void launch_a(const SmallParams& p, uint32_t batch, bool pes, cudaStream_t strea
       return;
     }
   }
-  if (pes) launch_k<A, true, false>(p, batch, stream);
-  else launch_k<A, false, false>(p, batch, stream);
+  // PES mode builds H2 Hamiltonians: only the H2 ansatz reaches it (above),
+  // so the generic kernel is instantiated without the chemistry prologue
+  if (pes) throw Error(VQF_LOGIC_ERROR, "small engine: PES mode needs the H2 ansatz");
+  launch_k<A, false, false>(p, batch, stream);
 }
 
 }  // namespace
@@ -1080,7 +1082,6 @@ void launch_vqe_small(const SmallParams& p, uint32_t batch, bool pes, cudaStream
     case 4: launch_a<4>(p, batch, pes, stream); break;
     case 8: launch_a<8>(p, batch, pes, stream); break;
     case 16: launch_a<16>(p, batch, pes, stream); break;
-    case 32: launch_a<32>(p, batch, pes, stream); break;
     default: throw Error(VQF_LOGIC_ERROR, "small engine: unsupported register size");
   }
   VQF_LAUNCHED();

@@ -20,7 +20,8 @@ enum : int32_t {
   kStatusNonFinite = 3,  // non-finite energy at iteration (vqe.hpp:217)
   kStatusScf = 4,        // NonConvergence (chem.hpp:46-52)
   kStatusHermitian = 5,  // non-Hermitian Pauli coefficient (pauli.hpp:205-214)
-  kStatusBond = 6        // BondLengthOutOfRange (host-side check, chem.hpp:38-44)
+  kStatusBond = 6,       // BondLengthOutOfRange (host-side check, chem.hpp:38-44)
+  kStatusAbort = 7       // block engine: grid barrier watchdog fired
 };
 
 struct SmallParams {

@@ -34,3 +34,23 @@ def test_dropin_header_on_gpu(dropin_binary):
     r = subprocess.run([dropin_binary], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr + r.stdout
     assert r.stdout.startswith("ok ")
+
+
+def test_block_engine_frame_compilation():
+    """compile_block_program (csrc/vqe_block.cu) replayed on the host: the
+    frame-tracked rotation passes and rewritten Pauli masks give the same
+    energies as the direct HEA circuit + reference expectation formula
+    (tests/cpp/block_frame_check.cpp), n = 4..13, 1-3 layers, fp64/fp32 plans."""
+    exe = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"block_frame_check_{os.getpid()}")
+    cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+           "-I", os.path.join(ROOT, "paper_2601_09951_b200", "csrc"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "tests", "cpp", "block_frame_check.cpp"), "-L", LIBDIR, "-lvqf_b200",
+           f"-Wl,-rpath,{LIBDIR}", "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    try:
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert r.stdout.startswith("ok ")
+    finally:
+        os.unlink(exe)
