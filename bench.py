@@ -358,7 +358,28 @@ def configs_3_4(V, torch, device, n_big, steps, warmup, peak, cpu_ok, cpu_second
                 row[f"{hname}_{method}_s"] = time.perf_counter() - t0
                 row[f"{hname}_{method}_energy"] = r.energy
         out["config3"][f"n{nq}"] = row
+    # config 3 at the study's own granularity: run_scaling_study (sweep.hpp:
+    # 265-307: HEA(2), TFIM, 5 Adam iterations, theta0 = 0.1) per width,
+    # median / min / max of 7 runs of the library call's runtime_seconds
+    study = {}
+    for nq in (4, 6, 8, 10, 12, 14, 16):
+        for method in ("shift", "adjoint"):
+            cfg = V.ScalingConfig(qubits=[nq], method=method)
+            V.run_scaling_study(cfg)
+            rts = [V.run_scaling_study(cfg)[0]["runtime_seconds"] for _ in range(7)]
+            study[f"n{nq}_{method}"] = {"median_s": statistics.median(rts), "min_s": min(rts), "max_s": max(rts)}
+    out["config3"]["scaling_study"] = study
     if pool is not None:
+        def cpu_study(widths):
+            rec = {}
+            for nq in widths:
+                reps = 5 if nq <= 10 else 1
+                ts = [ref.run_scaling_study([nq])[0]["runtime_seconds"] for _ in range(reps)]
+                rec[f"n{nq}"] = statistics.median(ts)
+            return rec
+
+        cpu_jobs["study_small"] = pool.submit(cpu_study, (4, 6, 8, 10, 12))
+        cpu_jobs["study_14"] = pool.submit(cpu_study, (14,))
         # after the GPU timings, so host-side launch overheads are not slowed
         # by the CPU baselines' threads
         cpu_jobs["kernels20"] = pool.submit(cpu_kernels, 20)
@@ -371,6 +392,7 @@ def configs_3_4(V, torch, device, n_big, steps, warmup, peak, cpu_ok, cpu_second
             "kind": "reference", "cores": 1,
             "sample": "reference statevector.hpp apply_gate / expectation: one call each on a resident "
                       "random_state (n = 20 and 24); run_vqe (HEA(2), 1 Adam iteration = 82 circuits) at n = 20; "
+                      "run_scaling_study (5 iterations) at n = 4..14 (median of 5 runs to n = 10, 1 run above); "
                       "single-threaded calls run concurrently in a 6-thread pool",
             "n20": cpu["kernels20"], "n24": cpu["kernels24"],
             "iteration_n20_tfim_s": cpu["iter20_tfim"], "iteration_n20_random32_s": cpu["iter20_random32"],
@@ -380,6 +402,10 @@ def configs_3_4(V, torch, device, n_big, steps, warmup, peak, cpu_ok, cpu_second
             "tfim_shift": cpu["iter20_tfim"] / c3["tfim_shift_s"],
             "tfim_adjoint": cpu["iter20_tfim"] / c3["tfim_adjoint_s"],
         }
+        ref_study = dict(cpu["study_small"], **cpu["study_14"])
+        out["cpu_baseline"]["scaling_study_s"] = ref_study
+        out["config3"]["scaling_study_speedup_vs_reference"] = {
+            k: ref_study[k] / study[f"{k}_shift"]["median_s"] for k in ref_study}
         if "random32_shift_s" in c3:
             out["config3"]["speedup_vs_reference_n20"]["random32_shift"] = cpu["iter20_random32"] / c3["random32_shift_s"]
             out["config3"]["speedup_vs_reference_n20"]["random32_adjoint"] = cpu["iter20_random32"] / c3["random32_adjoint_s"]

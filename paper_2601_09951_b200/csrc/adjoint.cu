@@ -610,9 +610,23 @@ void AdjointPlan::init(vqf_statevector* psi_, vqf_statevector* lam_, const Compi
   blob.resize(o_gp);
   const size_t bytes = o_gp + sizeof(double) * ((size_t)P * nb + 2 * (size_t)nb_ham + P + 2);
   VQF_CUDA(cudaSetDevice(psi->device));
-  VQF_CUDA(cudaMalloc(&dev, bytes));
-  VQF_CUDA(cudaMemcpy(dev, blob.data(), blob.size(), cudaMemcpyHostToDevice));
-  VQF_CUDA(cudaMallocHost(&hout, sizeof(double) * (P + 2)));
+  // stream-ordered pool allocation (no device-wide synchronisation on the
+  // free); the small pinned result block is cached per thread
+  free_stream = psi->own_stream;
+  VQF_CUDA(cudaMallocAsync(&dev, bytes, free_stream));
+  VQF_CUDA(cudaMemcpyAsync(dev, blob.data(), blob.size(), cudaMemcpyHostToDevice, free_stream));
+  VQF_CUDA(cudaStreamSynchronize(free_stream));
+  {
+    thread_local double* pin = nullptr;
+    thread_local size_t pin_cap = 0;
+    if (pin_cap < P + 2) {
+      if (pin) VQF_CUDA(cudaFreeHost(pin));
+      pin = nullptr;
+      pin_cap = std::max<size_t>(P + 2, 256);
+      VQF_CUDA(cudaMallocHost(&pin, sizeof(double) * pin_cap));
+    }
+    hout = pin;
+  }
   auto* d = static_cast<unsigned char*>(dev);
   hd = HamDevC{reinterpret_cast<const MaskTerm*>(d + o_lo), reinterpret_cast<const MaskTerm*>(d + o_hi),
                reinterpret_cast<const MaskTerm*>(d + o_mx), static_cast<uint32_t>(lo.size()),
@@ -630,8 +644,7 @@ void AdjointPlan::init(vqf_statevector* psi_, vqf_statevector* lam_, const Compi
 }
 
 AdjointPlan::~AdjointPlan() {
-  if (dev) cudaFree(dev);
-  if (hout) cudaFreeHost(hout);
+  if (dev) cudaFreeAsync(dev, free_stream);
 }
 
 void AdjointPlan::run(const std::vector<AdjGate>& prog, const std::vector<double>& theta, double* e_out,

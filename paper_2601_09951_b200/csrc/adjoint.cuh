@@ -35,7 +35,8 @@ struct AdjointPlan {
   vqf_statevector* lam = nullptr;  // H psi, swept backwards
   uint32_t P = 0, tile_bits = 0, nb = 0, nb_ham = 0;
   void* dev = nullptr;
-  double* hout = nullptr;
+  double* hout = nullptr;           // thread-local pinned block (not owned)
+  cudaStream_t free_stream = nullptr;  // the state's own stream: dev is freed there
   HamDevC hd{};
   double* gpart = nullptr;
   double* epart = nullptr;

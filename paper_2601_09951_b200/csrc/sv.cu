@@ -1298,6 +1298,106 @@ void retain_pool(int device) {
   done.push_back(device);
 }
 
+// Handle resources (stream, pinned / device result words, reduction and
+// term scratch) are recycled per device: creating a state handle then costs
+// one pool allocation instead of cudaStreamCreate + cudaMallocHost +
+// cudaMalloc (and their synchronising frees), whose latency spikes made
+// repeated VQE runs jittery.
+struct SvAux {
+  cudaStream_t stream = nullptr;
+  double* host_out = nullptr;
+  double* dev_out = nullptr;
+  size_t out_cap = 0;  // doubles
+  double* partials = nullptr;
+  size_t partial_cap = 0;
+  void* terms_dev = nullptr;
+  size_t terms_cap = 0;
+  double* cs_dev = nullptr;
+  size_t cs_cap = 0;
+};
+constexpr size_t kAuxKeep = 16;
+
+std::mutex& aux_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+std::vector<std::pair<int, SvAux>>& aux_pool() {
+  static std::vector<std::pair<int, SvAux>> pool;
+  return pool;
+}
+
+void aux_release(const SvAux& a) {
+  if (a.partials) cudaFree(a.partials);
+  if (a.terms_dev) cudaFree(a.terms_dev);
+  if (a.cs_dev) cudaFree(a.cs_dev);
+  if (a.host_out) cudaFreeHost(a.host_out);
+  if (a.dev_out) cudaFree(a.dev_out);
+  if (a.stream) cudaStreamDestroy(a.stream);
+}
+
+void sv_take_aux(vqf_statevector* sv) {
+  SvAux a;
+  bool found = false;
+  {
+    std::lock_guard<std::mutex> lock(aux_mutex());
+    auto& pool = aux_pool();
+    for (size_t i = pool.size(); i-- > 0;)
+      if (pool[i].first == sv->device) {
+        a = pool[i].second;
+        pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(i));
+        found = true;
+        break;
+      }
+  }
+  if (!found) VQF_CUDA(cudaStreamCreateWithFlags(&a.stream, cudaStreamNonBlocking));
+  const size_t need = 2 * static_cast<size_t>(sv->batch);
+  if (a.out_cap < need) {
+    if (a.host_out) VQF_CUDA(cudaFreeHost(a.host_out));
+    if (a.dev_out) VQF_CUDA(cudaFree(a.dev_out));
+    a.host_out = nullptr;
+    a.dev_out = nullptr;
+    const size_t cap = std::max<size_t>(need, 256);
+    VQF_CUDA(cudaMallocHost(&a.host_out, cap * sizeof(double)));
+    VQF_CUDA(cudaMalloc(&a.dev_out, cap * sizeof(double)));
+    a.out_cap = cap;
+  }
+  sv->own_stream = a.stream;
+  sv->host_out = a.host_out;
+  sv->dev_out = a.dev_out;
+  sv->out_cap = a.out_cap;
+  sv->partials = a.partials;
+  sv->partial_cap = a.partial_cap;
+  sv->terms_dev = a.terms_dev;
+  sv->terms_cap = a.terms_cap;
+  sv->cs_dev = a.cs_dev;
+  sv->cs_cap = a.cs_cap;
+}
+
+void sv_return_aux(vqf_statevector* sv) {
+  SvAux a;
+  a.stream = sv->own_stream;
+  a.host_out = sv->host_out;
+  a.dev_out = sv->dev_out;
+  a.out_cap = sv->out_cap;
+  a.partials = sv->partials;
+  a.partial_cap = sv->partial_cap;
+  a.terms_dev = sv->terms_dev;
+  a.terms_cap = sv->terms_cap;
+  a.cs_dev = sv->cs_dev;
+  a.cs_cap = sv->cs_cap;
+  {
+    std::lock_guard<std::mutex> lock(aux_mutex());
+    auto& pool = aux_pool();
+    size_t mine = 0;
+    for (const auto& e : pool) mine += e.first == sv->device;
+    if (mine < kAuxKeep) {
+      pool.emplace_back(sv->device, a);
+      return;
+    }
+  }
+  aux_release(a);
+}
+
 void sv_ensure_cs(vqf_statevector* sv, size_t n_doubles) {
   if (sv->cs_cap >= n_doubles) return;
   if (sv->cs_dev) VQF_CUDA(cudaFree(sv->cs_dev));
@@ -1324,7 +1424,7 @@ int vqf_sv_create(uint32_t n_qubits, uint32_t batch, int32_t dtype, int32_t devi
     sv->device = device;
     try {
       VQF_CUDA(cudaSetDevice(device));
-      VQF_CUDA(cudaStreamCreateWithFlags(&sv->own_stream, cudaStreamNonBlocking));
+      sv_take_aux(sv);
       sv->stream = sv->own_stream;
       // stream-ordered allocation from the device pool, whose release
       // threshold is raised once per device so freed states stay mapped and
@@ -1332,8 +1432,6 @@ int vqf_sv_create(uint32_t n_qubits, uint32_t batch, int32_t dtype, int32_t devi
       // paying cudaMalloc page-mapping costs
       retain_pool(device);
       VQF_CUDA(cudaMallocAsync(&sv->amps, sv->amp_bytes() * sv->dim() * batch, sv->stream));
-      VQF_CUDA(cudaMallocHost(&sv->host_out, 2 * sizeof(double) * batch));
-      VQF_CUDA(cudaMalloc(&sv->dev_out, 2 * sizeof(double) * batch));
       sv_reset(sv, 0);
       VQF_CUDA(cudaStreamSynchronize(sv->stream));
     } catch (...) {
@@ -1354,12 +1452,7 @@ int vqf_sv_destroy(vqf_sv sv) {
       cudaFreeAsync(sv->amps, sv->own_stream);
       cudaStreamSynchronize(sv->own_stream);
     }
-    if (sv->partials) cudaFree(sv->partials);
-    if (sv->terms_dev) cudaFree(sv->terms_dev);
-    if (sv->cs_dev) cudaFree(sv->cs_dev);
-    if (sv->host_out) cudaFreeHost(sv->host_out);
-    if (sv->dev_out) cudaFree(sv->dev_out);
-    if (sv->own_stream) cudaStreamDestroy(sv->own_stream);
+    if (sv->own_stream) sv_return_aux(sv);  // scratch, result words and stream are recycled
     delete sv;
   });
 }

@@ -18,8 +18,9 @@ struct vqf_statevector {
   // reduction scratch: per (entry, group, block) complex partials
   double* partials = nullptr;
   size_t partial_cap = 0;  // in doubles
-  double* host_out = nullptr;  // pinned, 2 * batch doubles
-  double* dev_out = nullptr;   // device, 2 * batch doubles
+  double* host_out = nullptr;  // pinned, >= 2 * batch doubles
+  double* dev_out = nullptr;   // device, >= 2 * batch doubles
+  size_t out_cap = 0;          // doubles in host_out / dev_out
   void* terms_dev = nullptr;   // compiled Hamiltonian terms (MaskTerm)
   size_t terms_cap = 0;        // bytes
   double* cs_dev = nullptr;    // per-entry (cos, sin) scratch for batched gates
