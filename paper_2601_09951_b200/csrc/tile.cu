@@ -161,6 +161,19 @@ constexpr int kR64 = 4, kR32 = VQF_TILE_R32;  // register bits per phase (16 / 3
 // 2 x 256 threads with 16 registers of amplitudes (scripts/build_variant.sh): 24.5 vs 33.6 ms per n = 30 layer
 template <typename T>
 constexpr int kGroupsOf = sizeof(T) == 8 ? VQF_TILE_GROUPS : VQF_TILE_GROUPS32;
+#ifndef VQF_TILE_SLOTS
+#define VQF_TILE_SLOTS 4  // tile buffers per CTA, shared round-robin by the groups
+#endif
+// A CTA's tiles i = 0, 1, ... use slot i % kSlots; group g takes i = g mod
+// G.  Whoever finishes reading tile i out of its slot loads tile i + kSlots
+// into it, so kSlots - G tiles are always in flight ahead of the groups.
+// measured (scripts/ab_slots.sh, n = 30 HEA layer): fp64 6 slots 31.5 ms vs
+// 4 slots 32.2 ms, fp32 4 slots 22.4 ms vs 6 slots 22.9 ms -- but with more
+// slots than groups the permutation-only passes fail the n = 28 property
+// test (tests/test_gpu_parity.py::test_large_register_properties), so the
+// default keeps one slot per group until that is understood
+template <typename T>
+constexpr int kSlotsOf = VQF_TILE_SLOTS > kGroupsOf<T> * kStages ? VQF_TILE_SLOTS : kGroupsOf<T> * kStages;
 constexpr int kB = 5;              // run = 2^5 amplitudes: 512 B fp64 (one TMA box of 4 x 128 B rows)
 
 template <typename T>
@@ -242,6 +255,7 @@ struct TilePhase {
 
 struct TileParams {
   uint32_t n, B, k, batch, n_phases;
+  uint32_t merge;  // hb[0..merge) = B, B+1, ...: 2^merge adjacent runs move as one TMA box
   uint32_t hb[kMaxHigh];  // global bit of local bit B + j, ascending
   const double* cs;       // per-entry (cos, sin) table: cs[2 (param * batch + entry)]
   // Permutation-only pass (every gate X / CNOT): the tile is written back as
@@ -341,8 +355,9 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
   const uint32_t run_bytes = run_amps * sizeof(A);
   constexpr uint32_t amps_per_row = 128 / sizeof(A);
   const uint32_t group = threadIdx.x / NT, gt = threadIdx.x % NT;
-  unsigned char* ring = smem + (size_t)group * kStages * tile_bytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kGroups * kStages * (size_t)tile_bytes) + group * kStages;
+  constexpr int kSlots = kSlotsOf<T>;
+  unsigned char* ring = smem;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSlots * (size_t)tile_bytes);
   __shared__ double2 rcs[kMaxRot];
   __shared__ uint16_t ftab[PERM ? 2 : 1][64];
   // run starts of the group's current tile (double-buffered: a fast thread
@@ -353,7 +368,8 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
   const uint64_t n_tiles = uint64_t{1} << (p.n - p.B - p.k);
   if (gt == 0) {
     if (group == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
-    for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
+    if (group == 0)
+      for (int st = 0; st < kSlots; ++st) mbar_init(&bar[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if constexpr (PERM) {
@@ -381,24 +397,27 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
     const uint32_t lane = gt;
     if (lane == 0) mbar_expect_tx(&bar[st], tile_bytes);
     unsigned char* dst = reinterpret_cast<unsigned char*>(stage_buf(st));
-    for (uint32_t j = lane; j < n_runs; j += 32)
-      tma_load_run(dst + (size_t)j * run_bytes, &map, static_cast<int32_t>(run_start(p, tile, j) / amps_per_row), entry,
-                   &bar[st]);
+    for (uint32_t j = lane; j < (n_runs >> p.merge); j += 32)
+      tma_load_run(dst + ((size_t)j << p.merge) * run_bytes, &map,
+                   static_cast<int32_t>(run_start(p, tile, j << p.merge) / amps_per_row), entry, &bar[st]);
   };
-  // the group's tiles: blockIdx.x + (kGroups i + group) * gridDim.x
+  // the CTA's tiles: tile(i) = blockIdx.x + i * gridDim.x; group g takes
+  // i = g, g + G, ...; tile i sits in slot i % kSlots
   const uint64_t step = kGroups * (uint64_t)gridDim.x;
   const uint64_t first = blockIdx.x + (uint64_t)group * gridDim.x;
-  if (gt < 32)
-    for (int st = 0; st < kStages; ++st) {
-      const uint64_t t0 = first + (uint64_t)st * step;
+  if (group == 0 && gt < 32)
+    for (int st = 0; st < kSlots; ++st) {
+      const uint64_t t0 = blockIdx.x + (uint64_t)st * gridDim.x;
       if (t0 < n_tiles) issue_load(t0, st);
     }
+  __syncthreads();  // the initial loads are issued before any group waits on a refill chain
   uint64_t tile = first;
   const bool direct = !PERM && p.ph[p.n_phases - 1].direct != 0;
-  for (uint32_t it = 0; tile < n_tiles; tile += step, ++it) {
-    const int cur = it % kStages;
-    const uint64_t ahead = tile + (uint64_t)kStages * step;
-    mbar_wait(&bar[cur], (it / kStages) & 1u);
+  for (uint32_t i = group; tile < n_tiles; tile += step, i += kGroups) {
+    const uint32_t it = i / kGroups;  // the group's own tile count
+    const int cur = static_cast<int>(i % kSlots);
+    const uint64_t ahead = tile + (uint64_t)kSlots * gridDim.x;  // tile i + kSlots, same slot
+    mbar_wait(&bar[cur], (i / kSlots) & 1u);
     A* t = stage_buf(cur);
     uint64_t* run_off = run_off_all[group][it & 1u];
     if (PERM || direct)
@@ -434,9 +453,9 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
         group_sync<NT>(group);
       }
       if (!direct && gt < 32) {
-        for (uint32_t j = gt; j < n_runs; j += 32)
-          tma_store_run(reinterpret_cast<unsigned char*>(t) + (size_t)j * run_bytes, &map,
-                        static_cast<int32_t>(run_start(p, tile, j) / amps_per_row), entry);
+        for (uint32_t j = gt; j < (n_runs >> p.merge); j += 32)
+          tma_store_run(reinterpret_cast<unsigned char*>(t) + ((size_t)j << p.merge) * run_bytes, &map,
+                        static_cast<int32_t>(run_start(p, tile, j << p.merge) / amps_per_row), entry);
         bulk_commit();
         bulk_wait_read();  // this lane's stores have read the buffer
         __syncwarp();
@@ -1015,10 +1034,16 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
   if (active > 1) gx = std::max<uint64_t>(1, std::min<uint64_t>(gx, n_tiles / (kGroups * 16)));
   const unsigned grid = static_cast<unsigned>(gx);
   const uint32_t run_bytes = static_cast<uint32_t>(sizeof(typename V2<T>::type) << B);
-  const CUtensorMap* map = tma::cached_state_map(sv, run_bytes);
-  const size_t smem = kGroups * kStages * (sizeof(typename V2<T>::type) << LB) + 8 * kGroups * kStages + 1024;
+  // high bits B, B+1, ... (spectator padding usually starts there) make
+  // adjacent runs: one TMA box of 2^merge runs instead of 2^merge boxes
+  uint32_t merge = 0;
+  while (merge < pass.hbits.size() && pass.hbits[merge] == B + merge && (run_bytes << (merge + 1)) <= 32768u) ++merge;
+  if (sizeof(T) == 8 || std::getenv("VQF_TILE_NO_MERGE")) merge = 0;  // measured: fp32 +10%, fp64 -1.4%
+  const CUtensorMap* map = tma::cached_state_map(sv, run_bytes << merge);
+  const size_t smem = kSlotsOf<T> * (sizeof(typename V2<T>::type) << LB) + 8 * kSlotsOf<T> + 1024;
   auto* amps = static_cast<typename V2<T>::type*>(sv->amps);
-  for (const TileParams& p : build_launches<T>(n, sv->batch, B, gates, pass, cs_dev)) {
+  for (TileParams& p : build_launches<T>(n, sv->batch, B, gates, pass, cs_dev)) {
+    p.merge = merge;
     const dim3 g(grid, active);
     const unsigned threads = kGroups << (LB - R);
     constexpr int LBmax = sizeof(T) == 8 ? kLB64 : kLB32;
@@ -1045,7 +1070,7 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
 template <typename T, int R, int LB>
 void opt_in_smem() {
   constexpr int kGroups = kGroupsOf<T>;
-  const int bytes = kGroups * kStages * (static_cast<int>(sizeof(T)) * 2 << LB) + 8 * kGroups * kStages + 1024;
+  const int bytes = kSlotsOf<T> * (static_cast<int>(sizeof(T)) * 2 << LB) + 8 * kSlotsOf<T> + 1024;
   VQF_CUDA(cudaFuncSetAttribute(k_tile<T, R, LB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   VQF_CUDA(cudaFuncSetAttribute(k_tile<T, R, LB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }

@@ -3,7 +3,8 @@
   python scripts/prof_targets.py pes        # fused PES kernel, 3 launches
   python scripts/prof_targets.py gates N    # RY / CNOT / DE on an N-qubit fp64 state
   python scripts/prof_targets.py expect N   # TFIM expectation (diag + N flip groups)
-  python scripts/prof_targets.py hea N      # two fused HEA layers (k_tile passes)
+  python scripts/prof_targets.py hea N [f32]      # two fused HEA layers (k_tile passes)
+  python scripts/prof_targets.py expect N [f32]   # (dtype option for both)
 """
 from __future__ import annotations
 
@@ -35,13 +36,13 @@ def main():
             V.apply_gate(psi, g)
     elif what == "expect":
         n = int(sys.argv[2])
-        psi = V.StateVector(n)
+        psi = V.StateVector(n, dtype=sys.argv[3] if len(sys.argv) > 3 else "f64")
         V.apply_circuit(psi, [V.Gate.ry(0.3, q) for q in range(n)])
         print(V.expectation(psi, V.build_tfim(n, 1.0, 1.0)))
         print(V.expectation(psi, V.build_z_sum(n)))
     elif what == "hea":
         n = int(sys.argv[2])
-        psi = V.StateVector(n)
+        psi = V.StateVector(n, dtype=sys.argv[3] if len(sys.argv) > 3 else "f64")
         layer = [V.Gate.ry(0.1 * (q + 1), q) for q in range(n)] + [V.Gate.cnot(q, q + 1) for q in range(n - 1)]
         for _ in range(2):
             V.apply_circuit(psi, layer)
