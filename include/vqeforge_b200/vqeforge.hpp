@@ -351,6 +351,51 @@ inline double expectation(const DeviceState& psi, const QubitHamiltonian& h) {
   return e;
 }
 
+// An n-qubit state split over `world` = 2^g shards (BASELINE config 5, beyond
+// one GPU's memory; the reference stops at 26 qubits, sweep.hpp:36-38).
+// comm == nullptr: every shard on `device` (virtual ranks); otherwise one
+// shard per process, exchanges through the caller's communicator (e.g.
+// ncclSend / ncclRecv in sendrecv, ncclAllReduce in allreduce_sum; see
+// INTEGRATION.md).  The qubit layout is updated lazily (layout()).
+class DistributedState {
+ public:
+  DistributedState(std::uint32_t n_qubits, std::uint32_t world, int device = 0, bool fp32 = false,
+                   const vqf_dsv_comm* comm = nullptr, std::uint64_t chunk_bytes = 0) {
+    detail::check(vqf_dsv_create(n_qubits, world, fp32 ? VQF_F32 : VQF_F64, device, comm, chunk_bytes, &h_));
+    n_ = n_qubits;
+  }
+  ~DistributedState() {
+    if (h_) vqf_dsv_destroy(h_);
+  }
+  DistributedState(const DistributedState&) = delete;
+  DistributedState& operator=(const DistributedState&) = delete;
+  std::vector<std::uint32_t> layout() const {
+    std::vector<std::uint32_t> pos(n_);
+    detail::check(vqf_dsv_layout(h_, pos.data()));
+    return pos;
+  }
+  vqf_dsv handle() const { return h_; }
+  std::uint32_t n_qubits() const { return n_; }
+
+ private:
+  vqf_dsv h_ = nullptr;
+  std::uint32_t n_ = 0;
+};
+
+inline void apply_circuit(DistributedState& psi, const std::vector<Gate>& gates) {
+  std::vector<vqf_gate> cs;
+  for (const auto& g : gates) cs.push_back(to_c(g));
+  detail::check(vqf_dsv_apply_circuit(psi.handle(), cs.data(), static_cast<std::uint32_t>(cs.size())));
+}
+
+inline double expectation(const DistributedState& psi, const QubitHamiltonian& h) {
+  if (h.n_qubits != psi.n_qubits()) throw std::invalid_argument("expectation: qubit count mismatch");
+  detail::CsrHam c(h);
+  double e = 0.0;
+  detail::check(vqf_dsv_expectation(psi.handle(), &c.view, &e));
+  return e;
+}
+
 }  // namespace gpu
 
 // statevector.hpp:148-207: the host value is staged through the device.

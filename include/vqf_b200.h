@@ -349,6 +349,98 @@ int vqf_pes_device_hamiltonians(const double* bonds, uint32_t n_bonds, int32_t d
 /* run_scaling_study (sweep.hpp:265-307). records holds n_widths entries. */
 int vqf_run_scaling_study(const vqf_scaling_config* config, vqf_scaling_record* records);
 
+/* ---------------------------------------------- distributed state vector
+ * BASELINE config 5 (34-35 qubits over 8 B200).  An n-qubit state is split
+ * over world = 2^g shards of 2^(n-g) amplitudes.  Every qubit sits at a
+ * POSITION: positions 0..g-1 are global (position p = rank bit g-1-p),
+ * positions g..n-1 are local (position p = local index bit n-1-p of every
+ * shard, i.e. engine wire p-g).  The layout qubit -> position starts as the
+ * identity and changes lazily: a gate or Pauli string that needs a global
+ * qubit local swaps it with a local position (each rank exchanges the half
+ * of its shard whose local bit differs from its own rank bit with
+ * rank ^ (1 << (g-1-p))) and KEEPS the new layout (no swap back).  Circuit
+ * plans evict the local qubit whose next use lies furthest ahead.
+ * Shards live either all in this process on one device (comm == NULL:
+ * virtual ranks, exchanges are in-place device swaps) or one per process
+ * (comm set): exchanges go through comm->sendrecv in chunk_bytes pieces
+ * staged through two preallocated device buffers (peak memory = shard +
+ * 2 chunks), the expectation's totals through comm->allreduce_sum.
+ * Reference: none (the reference caps run_scaling_study at 26 qubits,
+ * sweep.hpp:36-38, 267-283); per shard the engine runs the reference's
+ * apply_gate / expectation semantics (statevector.hpp:148-249). */
+typedef struct vqf_dsv_comm {
+  int32_t rank; /* the shard this process holds */
+  /* send `bytes` device bytes at send_buf to `peer` and receive as many
+   * from it into recv_buf, ordered on cuda_stream (or synchronous);
+   * returns 0 on success */
+  int (*sendrecv)(void* user, const void* send_buf, void* recv_buf, uint64_t bytes, int32_t peer,
+                  void* cuda_stream);
+  /* in-place sum of `count` host doubles over all ranks; 0 on success */
+  int (*allreduce_sum)(void* user, double* values, uint32_t count);
+  void* user;
+} vqf_dsv_comm;
+
+typedef struct vqf_dsv_state* vqf_dsv;
+
+/* One step of a distributed plan.
+ *  VQF_DSV_SWAP : a = global position, b = local position.
+ *  VQF_DSV_LOCAL: gates [first, first + count) of the mapped gate list, on
+ *                 every shard (wires are engine wires of the shard).
+ *  VQF_DSV_EVAL : planned terms [first, first + count): per-shard
+ *                 expectation (no global flips).
+ *  VQF_DSV_CROSS: planned terms [first, first + count): rank r pairs with
+ *                 rank r ^ a (terms flipping global positions that cannot be
+ *                 swapped local).  */
+enum { VQF_DSV_SWAP = 0, VQF_DSV_LOCAL = 1, VQF_DSV_EVAL = 2, VQF_DSV_CROSS = 3 };
+typedef struct vqf_dsv_op {
+  int32_t kind;
+  uint32_t a, b;
+  uint32_t first, count;
+} vqf_dsv_op;
+
+/* A Pauli term of the Hamiltonian under the layout at its evaluation:
+ * on rank r it contributes
+ *   coeff * (-i)^(l_ny + g_ny) * (-1)^popc(r & g_yz)
+ *   * sum_l conj(psi_r[l]) (-1)^popc(l & l_yz) psi_{r ^ g_flip}[l ^ l_flip]. */
+typedef struct vqf_dsv_term {
+  uint32_t term;   /* index into the Hamiltonian */
+  uint32_t g_flip; /* rank-bit mask of global X/Y */
+  uint32_t g_yz;   /* rank-bit mask of global Y/Z */
+  uint32_t g_ny;
+  uint64_t l_flip; /* local index bits of local X/Y */
+  uint64_t l_yz;   /* local index bits of local Y/Z */
+  uint32_t l_ny;
+  uint32_t pad;
+} vqf_dsv_term;
+
+/* Host-only planners (no GPU): position_of_qubit (n entries) is read and
+ * updated; gates / terms are planned against it.  mapped_gates holds
+ * n_gates entries, terms_out one entry per Hamiltonian term. */
+int vqf_dsv_plan_circuit(uint32_t n_qubits, uint32_t world, uint32_t* position_of_qubit, const vqf_gate* gates,
+                         uint32_t n_gates, vqf_dsv_op* ops, uint32_t cap_ops, uint32_t* n_ops,
+                         vqf_gate* mapped_gates);
+int vqf_dsv_plan_expectation(uint32_t n_qubits, uint32_t world, uint32_t* position_of_qubit,
+                             const vqf_hamiltonian* h, vqf_dsv_op* ops, uint32_t cap_ops, uint32_t* n_ops,
+                             vqf_dsv_term* terms_out);
+/* Per-GPU bytes: one shard + the two exchange buffers (comm mode). */
+uint64_t vqf_dsv_memory_per_gpu(uint32_t n_qubits, uint32_t world, int32_t dtype, uint64_t chunk_bytes,
+                                int32_t one_shard_per_process);
+
+/* chunk_bytes: exchange piece (0 = 256 MiB); comm NULL = virtual ranks. */
+int vqf_dsv_create(uint32_t n_qubits, uint32_t world, int32_t dtype, int32_t device, const vqf_dsv_comm* comm,
+                   uint64_t chunk_bytes, vqf_dsv* out);
+int vqf_dsv_destroy(vqf_dsv d);
+/* apply_circuit (statevector.hpp:205-207) on the distributed state. */
+int vqf_dsv_apply_circuit(vqf_dsv d, const vqf_gate* gates, uint32_t n_gates);
+/* expectation (statevector.hpp:217-249): the summed total; imaginary
+ * residue >= 1e-10 -> VQF_RUNTIME_ERROR with the reference's message. */
+int vqf_dsv_expectation(vqf_dsv d, const vqf_hamiltonian* h, double* out);
+int vqf_dsv_layout(vqf_dsv d, uint32_t* position_of_qubit);
+/* A shard held by this process in physical (local index) order. */
+int vqf_dsv_shard_download(vqf_dsv d, uint32_t rank, double* amps);
+int vqf_dsv_shard_upload(vqf_dsv d, uint32_t rank, const double* amps);
+int vqf_dsv_stats(vqf_dsv d, uint64_t* swaps, uint64_t* bytes_sent, uint64_t* scratch_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,6 +88,25 @@ class ScalingRecord(C.Structure):
 
 SV = C.c_void_p
 PES = C.c_void_p
+DSV = C.c_void_p
+
+DSV_SWAP, DSV_LOCAL, DSV_EVAL, DSV_CROSS = range(4)
+SENDRECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, dp, C.c_uint32)
+
+
+class DsvComm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("sendrecv", SENDRECV_FN), ("allreduce_sum", ALLREDUCE_FN), ("user", C.c_void_p)]
+
+
+class DsvOp(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("a", C.c_uint32), ("b", C.c_uint32), ("first", C.c_uint32),
+                ("count", C.c_uint32)]
+
+
+class DsvTerm(C.Structure):
+    _fields_ = [("term", C.c_uint32), ("g_flip", C.c_uint32), ("g_yz", C.c_uint32), ("g_ny", C.c_uint32),
+                ("l_flip", C.c_uint64), ("l_yz", C.c_uint64), ("l_ny", C.c_uint32), ("pad", C.c_uint32)]
 
 # (name, restype, argtypes) for every symbol in include/vqf_b200.h
 SIGNATURES = [
@@ -145,6 +164,20 @@ SIGNATURES = [
     ("vqf_pes_destroy", C.c_int, [PES]),
     ("vqf_pes_device_hamiltonians", C.c_int, [dp, C.c_uint32, C.c_int32, u32p, i32p, dp, dp]),
     ("vqf_run_scaling_study", C.c_int, [C.POINTER(ScalingConfig), C.POINTER(ScalingRecord)]),
+    ("vqf_dsv_plan_circuit", C.c_int, [C.c_uint32, C.c_uint32, u32p, C.POINTER(Gate), C.c_uint32, C.POINTER(DsvOp),
+                                       C.c_uint32, u32p, C.POINTER(Gate)]),
+    ("vqf_dsv_plan_expectation", C.c_int, [C.c_uint32, C.c_uint32, u32p, C.POINTER(Hamiltonian), C.POINTER(DsvOp),
+                                           C.c_uint32, u32p, C.POINTER(DsvTerm)]),
+    ("vqf_dsv_memory_per_gpu", C.c_uint64, [C.c_uint32, C.c_uint32, C.c_int32, C.c_uint64, C.c_int32]),
+    ("vqf_dsv_create", C.c_int, [C.c_uint32, C.c_uint32, C.c_int32, C.c_int32, C.POINTER(DsvComm), C.c_uint64,
+                                 C.POINTER(DSV)]),
+    ("vqf_dsv_destroy", C.c_int, [DSV]),
+    ("vqf_dsv_apply_circuit", C.c_int, [DSV, C.POINTER(Gate), C.c_uint32]),
+    ("vqf_dsv_expectation", C.c_int, [DSV, C.POINTER(Hamiltonian), dp]),
+    ("vqf_dsv_layout", C.c_int, [DSV, u32p]),
+    ("vqf_dsv_shard_download", C.c_int, [DSV, C.c_uint32, dp]),
+    ("vqf_dsv_shard_upload", C.c_int, [DSV, C.c_uint32, dp]),
+    ("vqf_dsv_stats", C.c_int, [DSV, u64p, u64p, u64p]),
 ]
 
 for _name, _res, _args in SIGNATURES:

@@ -1,9 +1,10 @@
 """BASELINE config 5 machinery on one B200: an n-qubit state split over
-`world` virtual shards (paper_2601_09951_b200/dsv.py, LocalComm: shards in
-this process, global-qubit swaps as device copies) vs the single-state
-engine, for one hardware-efficient layer (apply_circuit: fused local runs +
-swaps for the global wires) and a TFIM expectation.  The exchange here is an
-HBM copy, not NVLink; the point is the sharded path's structure and overhead.
+`world` virtual shards (vqf_dsv_* through paper_2601_09951_b200/dsv.py:
+shards in this process, global-qubit swaps as in-place device swaps) vs the
+single-state engine, for one hardware-efficient layer (apply_circuit: fused
+local runs + lazy swaps) and a TFIM expectation.  The exchange here is an
+HBM swap, not NVLink; the point is the sharded path's structure and
+overhead (swaps per layer, bytes exchanged).
 
   python scripts/dsv_bench.py [n] [world]
 """
@@ -20,7 +21,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 from paper_2601_09951_b200 import vqeforge as V  # noqa: E402
-from paper_2601_09951_b200.dsv import DistributedStateVector, GpuBackend, LocalComm  # noqa: E402
+from paper_2601_09951_b200.dsv import DistributedStateVector  # noqa: E402
 
 
 def wall(fn, reps=3):
@@ -42,13 +43,13 @@ def main():
     layer = [(1, 0.1 * (q + 1), [q]) for q in range(n)] + [(2, 0.0, [q, q + 1]) for q in range(n - 1)]
     tfim = V.build_tfim(n, 1.0, 1.0)
     terms = [(t.coefficient, t.axes) for t in tfim.terms]
-    d = DistributedStateVector(n, world, GpuBackend(0), LocalComm(world))
-    s0 = d.swaps_done
+    d = DistributedStateVector(n, world)
+    s0 = d.stats()["swaps"]
     t_layer_d = wall(lambda: d.apply_circuit(layer))
-    swaps_layer = (d.swaps_done - s0) // 4
-    s0 = d.swaps_done
+    swaps_layer = (d.stats()["swaps"] - s0) / 4
+    s0 = d.stats()["swaps"]
     t_exp_d = wall(lambda: d.expectation(terms))
-    swaps_exp = (d.swaps_done - s0) // 4
+    swaps_exp = (d.stats()["swaps"] - s0) / 4
     e_d = d.expectation(terms)
     del d
     torch.cuda.empty_cache()

@@ -3,6 +3,7 @@
 // test_vqe.cpp, test_sweep.cpp), with expected values taken from those
 // tests and from tests/golden.  `--host-only` runs the subset that needs no
 // GPU.  Prints "ok N" and exits 0, or reports the first failure and exits 1.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -148,6 +149,21 @@ static void gpu_part() {
   for (std::uint32_t q = 0; q < 20; ++q) gs.push_back(Gate::ry(0.3, q));
   gpu::apply_circuit(d, gs);
   CHECK(std::abs(gpu::expectation(d, build_z_sum(20)) - 20 * std::cos(0.3)) < 1e-10);
+  // distributed state (virtual ranks): an HEA layer + TFIM vs the single state
+  std::vector<Gate> layer;
+  for (std::uint32_t q = 0; q < 16; ++q) layer.push_back(Gate::ry(0.1 * (q + 1), q));
+  for (std::uint32_t q = 0; q + 1 < 16; ++q) layer.push_back(Gate::cnot(q, q + 1));
+  gpu::DistributedState ds(16, 8);
+  gpu::apply_circuit(ds, layer);
+  gpu::DeviceState one(16);
+  gpu::apply_circuit(one, layer);
+  const auto tfim = build_tfim(16, 1.0, 0.7);
+  CHECK(std::abs(gpu::expectation(ds, tfim) - gpu::expectation(one, tfim)) < 1e-10);
+  const auto lay = ds.layout();
+  std::vector<std::uint32_t> sorted_lay(lay);
+  std::sort(sorted_lay.begin(), sorted_lay.end());
+  for (std::uint32_t q = 0; q < 16; ++q) CHECK(sorted_lay[q] == q);
+  CHECK(throws<std::invalid_argument>([&] { gpu::DistributedState bad_world(16, 3); }));
 }
 
 int main(int argc, char** argv) {
