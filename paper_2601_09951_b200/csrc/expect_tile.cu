@@ -135,13 +135,16 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
       for (int j = 0; j < kExpSlots; ++j) {
         const ExpSlot& S = P.slot[j];
         if (S.n_terms == 0) continue;
-        double re[NR / 2], im[NR / 2];
+        // pair products and the per-term sums over the thread's 8 pairs in
+        // the storage precision (complex64 states: fp32, one conversion per
+        // term instead of two per pair), accumulated across tiles in fp64
+        T re[NR / 2], im[NR / 2];
 #pragma unroll
         for (uint32_t r = 0, q = 0; r < NR; ++r) {
           if (r & (1u << j)) continue;
           const A a = x[r], b = x[r | (1u << j)];
-          re[q] = static_cast<double>(fma(a.x, b.x, a.y * b.y));
-          im[q] = static_cast<double>(fma(a.x, b.y, -(a.y * b.x)));
+          re[q] = fma(a.x, b.x, a.y * b.y);
+          im[q] = fma(a.x, b.y, -(a.y * b.x));
           ++q;
         }
 #pragma unroll
@@ -149,15 +152,16 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
           if (k >= (int)S.n_terms) break;
           const uint32_t sm = S.smask[k];
           const bool use_im = S.sigma[k] != 0;
-          double part = 0.0;
+          T part = T(0);
 #pragma unroll
           for (uint32_t r = 0, q = 0; r < NR; ++r) {
             if (r & (1u << j)) continue;
-            const double v = use_im ? im[q] : re[q];
+            const T v = use_im ? im[q] : re[q];
             part += ((sm >> r) & 1u) ? -v : v;
             ++q;
           }
-          acc[((ph * kExpSlots + j) * kExpTerms + k) * nthr + threadIdx.x] += (__popcll(ib & S.yz[k]) & 1) ? -part : part;
+          const double pd = static_cast<double>(part);
+          acc[((ph * kExpSlots + j) * kExpTerms + k) * nthr + threadIdx.x] += (__popcll(ib & S.yz[k]) & 1) ? -pd : pd;
         }
       }
     }
