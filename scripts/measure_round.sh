@@ -1,16 +1,19 @@
 #!/bin/bash
 # Full GPU evidence run (gpurun, one B200): tests, smoke, bench (both arms),
-# bandwidth sweeps (config 4), fused-circuit timing, scaling study (config 3),
+# bandwidth sweeps (config 4), fused-circuit timing, scaling study (config 3,
+# incl. the shared-memory engine's widths), distributed-state virtual ranks,
 # then the ncu captures of scripts/profile_round.sh.
 OUT=gpurun_out; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/gpu.txt 2>&1
-timeout 1200 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
-timeout 600 python bench.py > $OUT/bench.log 2>&1
+timeout 900 python bench.py > $OUT/bench.log 2>&1
 timeout 600 python bench.py --impl reference > $OUT/bench_ref.log 2>&1
 timeout 900 python scripts/bw_sweep.py 26 28 30 32 33 > $OUT/bw_f64.jsonl 2>&1
 timeout 900 python scripts/bw_sweep.py 30 32 34 --f32 > $OUT/bw_f32.jsonl 2>&1
 timeout 600 python scripts/fusion_check.py > $OUT/fusion_check.log 2>&1
+timeout 900 python scripts/mid_width_probe.py 4 5 6 8 10 12 13 14 16 > $OUT/mid_width.jsonl 2>&1
 timeout 1500 python scripts/bench_scaling.py --ref-max 16 --gpu-max 26 > $OUT/scaling.jsonl 2>&1
-if [ "${PROFILE:-1}" = 1 ]; then timeout 1800 bash scripts/profile_round.sh > $OUT/profile.log 2>&1; fi
+timeout 300 python scripts/dsv_bench.py 30 8 > $OUT/dsv_bench.json 2>&1
+if [ "${PROFILE:-1}" = 1 ]; then timeout 2400 bash scripts/profile_round.sh > $OUT/profile.log 2>&1; fi
 echo done
