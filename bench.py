@@ -504,7 +504,12 @@ def run_ours(args, rank, world, local_rank):
         "ms_per_step": pes_s * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic: H2 Hamiltonians built on device from the bond grid (no external data)",
         "config": base_config(world),
-        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world},
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+                "note": "vqf_run_sweep through the C ABI with host buffers, host wall clock per call: the input is a "
+                        "SweepConfig (as the reference's run_sweep takes), so the bond grid is generated on the device "
+                        "and no input bytes cross; the per-point results (energy, theta*, iterations, status) come "
+                        "back zero-copy into mapped pinned memory and the trajectories by one D2H copy "
+                        "(d2h_bytes_per_step)"},
         "gpu_launches": int(gpu_launches),
         "parity": parity,
         "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
