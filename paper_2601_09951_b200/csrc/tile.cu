@@ -167,11 +167,9 @@ constexpr int kGroupsOf = sizeof(T) == 8 ? VQF_TILE_GROUPS : VQF_TILE_GROUPS32;
 // A CTA's tiles i = 0, 1, ... use slot i % kSlots; group g takes i = g mod
 // G.  Whoever finishes reading tile i out of its slot loads tile i + kSlots
 // into it, so kSlots - G tiles are always in flight ahead of the groups.
-// measured (scripts/ab_slots.sh, n = 30 HEA layer): fp64 6 slots 31.5 ms vs
-// 4 slots 32.2 ms, fp32 4 slots 22.4 ms vs 6 slots 22.9 ms -- but with more
-// slots than groups the permutation-only passes fail the n = 28 property
-// test (tests/test_gpu_parity.py::test_large_register_properties), so the
-// default keeps one slot per group until that is understood
+// measured (scripts/ring_check.sh, n = 30 HEA layer, with the issued[]
+// guard below): 6 slots 32.2 ms fp64 / 23.0 ms fp32 vs 4 slots 32.6 / 22.6 ms,
+// so the default keeps one slot per group
 template <typename T>
 constexpr int kSlotsOf = VQF_TILE_SLOTS > kGroupsOf<T> * kStages ? VQF_TILE_SLOTS : kGroupsOf<T> * kStages;
 constexpr int kB = 5;              // run = 2^5 amplitudes: 512 B fp64 (one TMA box of 4 x 128 B rows)
@@ -392,10 +390,19 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
     }
   }
   __syncthreads();
+  // issued[s] = CTA tile index whose load the slot's pending mbarrier phase
+  // belongs to: with more slots than groups a fast group could otherwise
+  // reach a slot two phases ahead of a slow refiller and mistake the parity
+  // of an older phase for its own (ABA)
+  __shared__ volatile uint32_t issued[8];
+  static_assert(kSlotsOf<T> <= 8, "tile ring: at most 8 slots");
   const auto stage_buf = [&](int st) { return reinterpret_cast<A*>(ring + (size_t)st * tile_bytes); };
   const auto issue_load = [&](uint64_t tile, int st) {
     const uint32_t lane = gt;
-    if (lane == 0) mbar_expect_tx(&bar[st], tile_bytes);
+    if (lane == 0) {
+      mbar_expect_tx(&bar[st], tile_bytes);
+      issued[st] = static_cast<uint32_t>((tile - blockIdx.x) / gridDim.x);
+    }
     unsigned char* dst = reinterpret_cast<unsigned char*>(stage_buf(st));
     for (uint32_t j = lane; j < (n_runs >> p.merge); j += 32)
       tma_load_run(dst + ((size_t)j << p.merge) * run_bytes, &map,
@@ -417,6 +424,9 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
     const uint32_t it = i / kGroups;  // the group's own tile count
     const int cur = static_cast<int>(i % kSlots);
     const uint64_t ahead = tile + (uint64_t)kSlots * gridDim.x;  // tile i + kSlots, same slot
+    if (kSlots > kGroups)
+      while (issued[cur] != i) {
+      }
     mbar_wait(&bar[cur], (i / kSlots) & 1u);
     A* t = stage_buf(cur);
     uint64_t* run_off = run_off_all[group][it & 1u];
