@@ -200,8 +200,10 @@ __device__ void vqe_block_body(const BlockParams& p) {
   const uint32_t D = 1u << p.n;
   const Team<TEAMS> tm(p.team_lanes);
   const int n_slots = TEAMS ? tm.count : 1;  // per-team state / angle slots
-  const BlockSmem L(p.n, sizeof(A2), P, p.obytes, p.herm ? p.n_terms : 0, p.herm ? p.n_groups : 0, n_slots);
-  A2* psi = reinterpret_cast<A2*>(smem_raw + L.psi) + (TEAMS ? (size_t)tm.id << p.n : 0);
+  const BlockSmem L(p.n, p.gstate ? 0 : sizeof(A2), P, p.obytes, p.herm ? p.n_terms : 0, p.herm ? p.n_groups : 0,
+                    n_slots);
+  A2* psi = p.gstate ? static_cast<A2*>(p.gstate) + ((size_t)blockIdx.x << p.n)
+                     : reinterpret_cast<A2*>(smem_raw + L.psi) + (TEAMS ? (size_t)tm.id << p.n : 0);
   double* theta = reinterpret_cast<double*>(smem_raw + L.theta);
   double* mom = reinterpret_cast<double*>(smem_raw + L.mom);
   double* vel = reinterpret_cast<double*>(smem_raw + L.vel);
@@ -665,7 +667,8 @@ BlockProgram compile_block_program(int32_t kind, uint32_t layers, uint32_t n, co
   if (n < (uint32_t)kBlockMinN || n > (uint32_t)block_max_n(dtype)) throw_invalid("block engine: register width");
   BlockProgram prog;
   prog.n = n;
-  prog.teams = use_teams(n, layers * n);
+  prog.gmem = n > static_cast<uint32_t>(block_smem_max_n(dtype));
+  prog.teams = !prog.gmem && use_teams(n, layers * n);
   prog.R = static_cast<uint32_t>(pass_bits(n, prog.teams));
   Frame fr(n);
   const auto bit = [&](uint32_t q) { return n - 1 - q; };  // MSB-first (pauli.hpp:225-227)
@@ -742,12 +745,13 @@ BlockProgram compile_block_program(int32_t kind, uint32_t layers, uint32_t n, co
     prog.slots = 1;
   }
   const uint32_t Th = prog.herm ? T : 0u, Gh = prog.herm ? Gp : 0u;
-  if (BlockSmem(n, amp, P, 0, Th, Gh, prog.slots).total > kBlockSmemCap)
+  const uint32_t samp = prog.gmem ? 0u : amp;  // state bytes in shared memory
+  if (BlockSmem(n, samp, P, 0, Th, Gh, prog.slots).total > kBlockSmemCap)
     throw_invalid("block engine: problem does not fit shared memory");
   prog.obytes = 0;
   if (prog.herm && prog.group_off[1] > prog.group_off[0])
     for (uint32_t ob : {8u, 4u})
-      if (BlockSmem(n, amp, P, ob, Th, Gh, prog.slots).total <= kBlockSmemCap) {
+      if (BlockSmem(n, samp, P, ob, Th, Gh, prog.slots).total <= kBlockSmemCap) {
         prog.obytes = ob;
         break;
       }
@@ -757,7 +761,8 @@ BlockProgram compile_block_program(int32_t kind, uint32_t layers, uint32_t n, co
 size_t block_smem_bytes(const BlockProgram& prog, int32_t dtype, int32_t P) {
   const uint32_t T = prog.herm ? static_cast<uint32_t>(prog.terms.size()) : 0u;
   const uint32_t G = prog.herm ? static_cast<uint32_t>(prog.group_flip.size()) : 0u;
-  return BlockSmem(prog.n, dtype == VQF_F32 ? 8u : 16u, static_cast<uint32_t>(P), prog.obytes, T, G, prog.slots).total;
+  const uint32_t amp = prog.gmem ? 0u : dtype == VQF_F32 ? 8u : 16u;
+  return BlockSmem(prog.n, amp, static_cast<uint32_t>(P), prog.obytes, T, G, prog.slots).total;
 }
 
 namespace {

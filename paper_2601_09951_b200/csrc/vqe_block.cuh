@@ -13,8 +13,14 @@ constexpr int kBlockMinN = 4;
 constexpr int kBlockMaxP = 256;
 constexpr int kBlockMaxR = 4;  // register bits per rotation pass
 
-// Largest register the engine holds in one CTA's shared memory.
-inline int block_max_n(int32_t dtype) { return dtype == VQF_F32 ? 14 : 13; }
+// Largest register whose state fits one CTA's shared memory; one qubit
+// more runs with the state in an L2-resident global buffer per CTA
+// (everything else on chip).  Measured (run_scaling_study, 5 iterations):
+// n = 14 1.42 ms vs 2.38 / 2.91 ms on the HBM engine (adjoint / shift); at
+// n = 15-16 one CTA per circuit is bound by its SM's L2 bandwidth
+// (2.8 / 5.7 ms, no better than the HBM engine), so the engine stops at 14.
+inline int block_smem_max_n(int32_t dtype) { return dtype == VQF_F32 ? 14 : 13; }
+inline int block_max_n(int32_t dtype) { return dtype == VQF_F32 ? 15 : 14; }
 
 // One shared-memory pass: up to R commuting RY rotations applied in
 // registers.  Amplitude member m of a thread's coset sits at physical index
@@ -101,6 +107,7 @@ struct BlockProgram {
   // launch shape: teams of `lanes` threads in one CTA (teams = true), or a
   // cooperative grid of CTAs of `threads`, one circuit per CTA
   bool teams = false;
+  bool gmem = false;  // state in a global (L2-resident) buffer per CTA
   uint32_t lanes = 0, threads = 0, slots = 1;
 };
 
@@ -123,6 +130,7 @@ struct BlockParams {
   int32_t herm, n_terms;
   uint32_t obytes;
   int32_t team_lanes;
+  void* gstate;  // gmem programs: gridDim.x states of 2^n amplitudes (CTA b uses state b)
   const BlockRTerm* rterms;
   const double* init_theta;  // P or null
   // grid exchange

@@ -841,9 +841,11 @@ void run_vqe_block(const CompiledHam& ch, int32_t kind, uint32_t layers, const v
   const size_t o_errt = oc.take<double>(P);
   const size_t o_clk = oc.take<uint64_t>(2);
   const size_t pin_total = oc.off;
-  Carver dc;  // device scratch: staged inputs, then the energy exchange
+  Carver dc;  // device scratch: staged inputs, the energy exchange, global states
   dc.off = inl ? 0 : in_end;
   const size_t o_E = dc.take<double2>(2 * static_cast<size_t>(NC));
+  const int grid = block_grid(prog, dtype, NC, device);
+  const size_t o_state = dc.take<double2>(prog.gmem ? static_cast<size_t>(grid) << n : 0);
   ws.reserve(dc.off, pin_total);
   auto* pin = static_cast<unsigned char*>(ws.pin);
   auto* dev = static_cast<unsigned char*>(ws.dev);
@@ -890,6 +892,7 @@ void run_vqe_block(const CompiledHam& ch, int32_t kind, uint32_t layers, const v
   p.n_terms = static_cast<int32_t>(prog.terms.size());
   p.obytes = prog.obytes;
   p.team_lanes = static_cast<int32_t>(prog.lanes);
+  p.gstate = prog.gmem ? static_cast<void*>(dev + o_state) : nullptr;
   p.rterms = reinterpret_cast<const BlockRTerm*>(src(o_rterms));
   p.init_theta = init.empty() ? nullptr : reinterpret_cast<const double*>(src(o_init));
   p.energies = reinterpret_cast<double2*>(dev + o_E);
@@ -904,7 +907,6 @@ void run_vqe_block(const CompiledHam& ch, int32_t kind, uint32_t layers, const v
   p.err_iter = reinterpret_cast<int32_t*>(pin + o_erri);
   p.err_theta = reinterpret_cast<double*>(pin + o_errt);
   p.clk = reinterpret_cast<unsigned long long*>(pin + o_clk);
-  const int grid = block_grid(prog, dtype, NC, device);
   HMARK("stage");
   if (!inl) VQF_CUDA(cudaMemcpyAsync(dev, pin, in_end, cudaMemcpyHostToDevice, ws.stream));
   launch_vqe_block(args, in_end, prog, grid, ws.stream);

@@ -158,7 +158,7 @@ double direct_energy(uint32_t n, uint32_t layers, const std::vector<double>& the
 int main() {
   std::mt19937 rng(20260804);
   int cases = 0, herm_cases = 0;
-  for (uint32_t n : {4u, 5u, 6u, 7u, 9u, 12u, 13u}) {
+  for (uint32_t n : {4u, 5u, 6u, 7u, 9u, 12u, 13u, 14u, 15u}) {
     for (uint32_t layers : {1u, 2u, 3u}) {
       // random Pauli sum: 12 strings, X/Y/Z/I per wire, real coefficients
       std::vector<double> coeffs;

@@ -30,8 +30,10 @@ def hams(ref, n):
     return {"tfim": tf, "random16": ref.canonicalize(rh)}
 
 
-@pytest.mark.parametrize("n", [4, 6, 8, 10, 12, 13])
+@pytest.mark.parametrize("n", [4, 6, 8, 10, 12, 13, 14])
 def test_block_engine_run_vqe_matches_reference(gpu, ref, n, monkeypatch):
+    """4..13 qubits: state in shared memory; 14: in an L2-resident global
+    buffer per CTA."""
     V = gpu
     monkeypatch.setenv("VQF_ENGINE", "block")  # n = 4, 5 default to the warp engine
     hea = V.AnsatzSpec.hardware_efficient(2)
@@ -118,7 +120,7 @@ def test_block_engine_equals_hbm_engine(gpu, ref, n, monkeypatch):
     assert np.max(np.abs(np.array(rb.theta) - rh.theta)) < 1e-11
 
 
-@pytest.mark.parametrize("n", [6, 10, 14])
+@pytest.mark.parametrize("n", [6, 10, 14, 15])
 def test_block_engine_fp32(gpu, ref, n):
     V = gpu
     h = ref.build_tfim(n, 1.0, 0.7)
@@ -135,9 +137,9 @@ def test_block_engine_fp32(gpu, ref, n):
 
 def test_scaling_study_mid_widths_match_reference(gpu, ref):
     """run_scaling_study (sweep.hpp:265-307) at the config-3 widths the
-    engine holds: 4 (warp engine), 6..13 (this engine)."""
+    engine holds (4..14)."""
     V = gpu
-    widths = [4, 6, 8, 10, 12, 13]
+    widths = [4, 6, 8, 10, 12, 13, 14]
     recs = V.run_scaling_study(V.ScalingConfig(qubits=widths))
     want = ref.run_scaling_study(widths)
     for r, w in zip(recs, want):
