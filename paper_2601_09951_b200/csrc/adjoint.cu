@@ -17,6 +17,7 @@
 // gates are un-applied to each vector by the fused tile path (permutation
 // passes, tile.cu).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "adjoint.cuh"
@@ -368,6 +369,132 @@ __global__ void __launch_bounds__(kThreads) k_adj_ry_multi(typename V2<T>::type*
   }
 }
 
+// The same backward step for RYs when the vectors sit in a GF(2) frame
+// (logical index i = M p ^ c of physical slot p): the backward sweep
+// un-applies CNOT / X chains by updating the frame instead of moving data
+// (the gradient's inner products do not care where amplitudes sit).  RY on
+// logical bit b pairs slots p and p ^ vec (vec = M^-1 e_b); the slot holding
+// logical 0 is the one with parity(row & p) ^ cbit = 0, one orientation per
+// coset (vec_i . row_j = delta_ij), so a logical-1 base just swaps the pair.
+struct RyFrameGroup {
+  uint64_t vec[4], row[4];
+  uint32_t piv[4];  // ascending pivot bits of span{vec}
+  uint32_t cbits;
+  double c[4], s[4];
+  double* part[4];
+};
+
+template <typename T, int K>
+__global__ void __launch_bounds__(kThreads) k_adj_ry_frame(typename V2<T>::type* __restrict__ psi,
+                                                           typename V2<T>::type* __restrict__ lam, uint32_t n,
+                                                           const RyFrameGroup gr) {
+  using A = typename V2<T>::type;
+  constexpr int D = 1 << K;
+  uint64_t off[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    uint64_t o = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (r & (1 << j)) o ^= gr.vec[j];
+    off[r] = o;
+  }
+  double acc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) acc[j] = 0.0;
+  const uint64_t total = uint64_t{1} << (n - K);
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t k = (uint64_t)blockIdx.x * kThreads + threadIdx.x; k < total; k += stride) {
+    uint64_t base = k;
+#pragma unroll
+    for (int j = 0; j < K; ++j) base = insert_zero(base, gr.piv[j]);
+    A a[D], l[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      a[r] = psi[base ^ off[r]];
+      l[r] = lam[base ^ off[r]];
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const bool one = ((__popcll(gr.row[j] & base) ^ (gr.cbits >> j)) & 1u) != 0u;
+      const double c = gr.c[j], sn = gr.s[j];
+      const T ct = static_cast<T>(c), st = static_cast<T>(sn);
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        if (r & (1 << j)) continue;
+        // logical (0, 1) members of the pair
+        const A x = one ? a[r | (1 << j)] : a[r], y = one ? a[r] : a[r | (1 << j)];
+        const A lx = one ? l[r | (1 << j)] : l[r], ly = one ? l[r] : l[r | (1 << j)];
+        A pa, pb;  // psi' = G^dag psi
+        pa.x = fma(ct, x.x, st * y.x);
+        pa.y = fma(ct, x.y, st * y.y);
+        pb.x = fma(ct, y.x, -(st * x.x));
+        pb.y = fma(ct, y.y, -(st * x.y));
+        const double mar = fma(-sn, (double)pa.x, -(c * (double)pb.x)), mai = fma(-sn, (double)pa.y, -(c * (double)pb.y));
+        const double mbr = fma(c, (double)pa.x, -(sn * (double)pb.x)), mbi = fma(c, (double)pa.y, -(sn * (double)pb.y));
+        acc[j] = fma(0.5 * (double)lx.x, mar, fma(0.5 * (double)lx.y, mai,
+                 fma(0.5 * (double)ly.x, mbr, fma(0.5 * (double)ly.y, mbi, acc[j]))));
+        A qa, qb;  // lambda' = G^dag lambda
+        qa.x = fma(ct, lx.x, st * ly.x);
+        qa.y = fma(ct, lx.y, st * ly.y);
+        qb.x = fma(ct, ly.x, -(st * lx.x));
+        qb.y = fma(ct, ly.y, -(st * lx.y));
+        a[r] = one ? pb : pa;
+        a[r | (1 << j)] = one ? pa : pb;
+        l[r] = one ? qb : qa;
+        l[r | (1 << j)] = one ? qa : qb;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      psi[base ^ off[r]] = a[r];
+      lam[base ^ off[r]] = l[r];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double2 t = block_sum(make_double2(acc[j], 0.0));
+    if (threadIdx.x == 0) gr.part[j][blockIdx.x] = t.x;
+  }
+}
+
+// Host frame of the backward sweep (logical i = M p ^ c): rows of M (bit
+// b's parity mask over physical bits) and columns of M^-1 (bit b's pair
+// vector).
+struct SweepFrame {
+  uint32_t n;
+  std::vector<uint64_t> row, col;
+  uint64_t c = 0;
+  explicit SweepFrame(uint32_t n_) : n(n_), row(n_), col(n_) {
+    for (uint32_t b = 0; b < n; ++b) row[b] = col[b] = uint64_t{1} << b;
+  }
+  void cnot(uint32_t a, uint32_t b) {  // control bit a, target bit b
+    row[b] ^= row[a];
+    if ((c >> a) & 1u) c ^= uint64_t{1} << b;
+    col[a] ^= col[b];
+  }
+  void x(uint32_t b) { c ^= uint64_t{1} << b; }
+};
+
+// pivots (highest set bits after reduction, ascending) of independent vectors
+void frame_pivots(const uint64_t* v, int k, uint32_t* piv) {
+  std::vector<uint64_t> red;
+  std::vector<uint32_t> pv;
+  for (int j = 0; j < k; ++j) {
+    uint64_t w = v[j];
+    for (size_t i = 0; i < red.size(); ++i)
+      if ((w >> pv[i]) & 1u) w ^= red[i];
+    if (w == 0) throw Error(VQF_LOGIC_ERROR, "adjoint frame: dependent pair vectors");
+    const uint32_t pb = 63u - static_cast<uint32_t>(__builtin_clzll(w));
+    for (size_t i = 0; i < red.size(); ++i)
+      if ((red[i] >> pb) & 1u) red[i] ^= w;
+    red.push_back(w);
+    pv.push_back(pb);
+  }
+  std::sort(pv.begin(), pv.end());
+  for (int j = 0; j < k; ++j) piv[j] = pv[j];
+}
+
 // Self-inverse CNOT on both vectors in one pass.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_adj_cnot(typename V2<T>::type* __restrict__ psi,
@@ -441,8 +568,58 @@ void run_t(AdjointPlan& pl, const std::vector<AdjGate>& prog, const std::vector<
   const uint32_t B = pl.tile_bits;
   k_apply_ham<T><<<pl.nb_ham, kThreads, sizeof(double2) << B, st>>>(psi, lam, n, B, pl.hd, pl.epart);
   VQF_LAUNCHED();
-  // backward sweep
-  for (size_t gi = prog.size(); gi-- > 0;) {
+  // backward sweep.  Programs of RYs, CNOTs and Xs (the hardware-efficient
+  // ansatz) run in a GF(2) frame: CNOT / X chains only update the frame and
+  // every RY group is one frame-aware two-vector pass (no permutation passes
+  // over psi and lambda); other programs move the data.
+  bool frame_ok = !std::getenv("VQF_ADJ_NO_FRAME");
+  for (const AdjGate& g : prog)
+    frame_ok = frame_ok && ((g.kind == VQF_GATE_RY && g.param >= 0) || (g.kind == VQF_GATE_CNOT && g.param < 0) ||
+                            (g.kind == VQF_GATE_PAULI_X && g.param < 0));
+  if (frame_ok) {
+    SweepFrame fr(n);
+    const auto bit_of = [n](uint32_t w) { return n - 1 - w; };
+    for (size_t gi = prog.size(); gi-- > 0;) {
+      const AdjGate& g = prog[gi];
+      if (g.kind == VQF_GATE_CNOT) {
+        fr.cnot(bit_of(g.wires[0]), bit_of(g.wires[1]));
+        continue;
+      }
+      if (g.kind == VQF_GATE_PAULI_X) {
+        fr.x(bit_of(g.wires[0]));
+        continue;
+      }
+      size_t cnt = 1;  // consecutive RYs on distinct wires (they commute)
+      while (cnt < 4 && gi >= cnt && prog[gi - cnt].kind == VQF_GATE_RY) {
+        bool distinct = true;
+        for (size_t q = 0; q < cnt; ++q) distinct = distinct && prog[gi - cnt].wires[0] != prog[gi - q].wires[0];
+        if (!distinct) break;
+        ++cnt;
+      }
+      RyFrameGroup gr{};
+      for (size_t q = 0; q < cnt; ++q) {  // gate q of the group = prog[gi - q] (backward order)
+        const AdjGate& h = prog[gi - q];
+        const uint32_t b = bit_of(h.wires[0]);
+        const double th = theta[h.param];
+        gr.vec[q] = fr.col[b];
+        gr.row[q] = fr.row[b];
+        if ((fr.c >> b) & 1u) gr.cbits |= 1u << q;
+        gr.c[q] = std::cos(0.5 * th);
+        gr.s[q] = std::sin(0.5 * th);
+        gr.part[q] = pl.gpart + (size_t)h.param * pl.nb;
+      }
+      frame_pivots(gr.vec, static_cast<int>(cnt), gr.piv);
+      switch (cnt) {
+        case 1: k_adj_ry_frame<T, 1><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr); break;
+        case 2: k_adj_ry_frame<T, 2><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr); break;
+        case 3: k_adj_ry_frame<T, 3><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr); break;
+        default: k_adj_ry_frame<T, 4><<<pl.nb, kThreads, 0, st>>>(psi, lam, n, gr); break;
+      }
+      VQF_LAUNCHED();
+      gi -= cnt - 1;
+    }
+  }
+  for (size_t gi = frame_ok ? 0 : prog.size(); gi-- > 0;) {
     const AdjGate& g = prog[gi];
     const auto bit_of = [n](uint32_t w) { return n - 1 - w; };
     // a run of >= 2 parameter-free self-inverse gates (CNOT / X chains) is
