@@ -66,6 +66,7 @@ struct Shared {
   // per-iteration exchange
   double theta[kSmallMaxP];
   double2 cs[kSmallMaxP][3];  // (cos, sin) of 0.5 * (theta, theta + pi/2, theta - pi/2)
+  double init_state[16];      // PES whole-state lanes: basis_state(4, {1,1,0,0})
   double2 energy[2 * kSmallMaxP + 1];
   double grad[kSmallMaxP];
   int stop;
@@ -591,6 +592,8 @@ __device__ __forceinline__ bool prologue(Shared& sh, const SmallParams& p, int p
     __syncwarp();
   }
   build_tables(sh, D, lane);
+  if (lane < 16) sh.init_state[lane] = lane == 12 ? 1.0 : 0.0;  // basis_state(4, {1,1,0,0}) (vqe.hpp:77)
+  __syncwarp();
   gmark(prob, 2);
   return true;
 }
@@ -632,6 +635,10 @@ struct H2Lane {
   int fl[4], fs[4];
   double2 o0[4], o1[4];
   double in0, in1, q0, q1;  // |1100> and its DoubleExcitation partners
+  // G < 0 (whole-state lanes, PES): lane c < 3 holds circuit c's complete
+  // 16-amplitude state in registers; real operator tables of the diagonal
+  // group and the flip-15 group (XXYY-type strings), the input state
+  double fo0[16], fo1[16], fin[16];
 };
 
 // own: this lane's circuit total (lane 0 holds E(theta)); ep_re / em_re:
@@ -644,6 +651,31 @@ __device__ __forceinline__ void h2_energies(const Shared& sh, const H2Lane& L, d
   double sn, cs;
   if (FAST) sincos_reduced(0.5 * t, &sn, &cs);
   else sincos(0.5 * t, &sn, &cs);
+  if constexpr (G < 0) {
+    // whole-state lanes: the circuit's 16 amplitudes in this lane.
+    // DoubleExcitation(0,1,2,3) rotates indices 12 (wires 0,1 set) and 3
+    // (statevector.hpp:186-197); every other amplitude passes through.  The
+    // expectation runs over all 16 amplitudes: sum_i O_0(i) psi_i^2 +
+    // sum_i O_15(i) psi_i psi_{i^15}, eight independent partial sums.  No
+    // shuffle until the three circuit energies are exchanged.
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = L.fin[i];
+    x[12] = fma(cs, L.fin[12], -(sn * L.fin[3]));
+    x[3] = fma(sn, L.fin[12], cs * L.fin[3]);
+    double part[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) part[i] = L.fo0[i] * (x[i] * x[i]);
+#pragma unroll
+    for (int i = 8; i < 16; ++i) part[i & 7] = fma(L.fo0[i], x[i] * x[i], part[i & 7]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) part[i & 7] = fma(L.fo1[i], x[i] * x[i ^ 15], part[i & 7]);
+    const double e = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
+    own = make_double2(e, 0.0);  // real tables and amplitudes: no imaginary part (checked at setup)
+    ep_re = __shfl_sync(0xffffffffu, e, 1);
+    em_re = __shfl_sync(0xffffffffu, e, 2);
+    return;
+  }
   // DoubleExcitation(0,1,2,3) on the fixed input |1100>: indices 12 and 3
   // rotate; every other amplitude and its partner are zero, so the same
   // rotation formula on all lanes leaves them zero (no per-lane select).
@@ -719,6 +751,7 @@ __device__ __forceinline__ int h2_step(const Shared& sh, const SmallParams& p, i
   double2 own;
   double ep_re, em_re;
   h2_energies<G, FAST>(sh, L, s.th, own, ep_re, em_re);
+
   // gradient and the Adam update (vqe.hpp:152-174, t = iter + 1; bias
   // corrections as host-computed reciprocals 1 / (1 - beta^t)) are formed
   // first and committed after the checks, so their latency overlaps the vote
@@ -853,6 +886,25 @@ __global__ void __launch_bounds__(PES ? kPesThreads : 32, 1) k_h2(SmallParams p)
   L.in1 = L.sl == 4 ? 1.0 : 0.0;
   L.q0 = __shfl_xor_sync(0xffffffffu, L.in1, 7, 8);
   L.q1 = __shfl_xor_sync(0xffffffffu, L.in0, 7, 8);
+  // PES Hamiltonians (real Jordan-Wigner coefficients, a diagonal group and
+  // at most the flip-15 group) run with whole-state lanes: no reduction
+  // shuffles on the iteration's critical path
+  bool full = PES && L.G >= 1 && L.G <= 2 && sh.flip[0] == 0 && (L.G < 2 || sh.flip[1] == 15);
+  if (full)
+    for (int g = 0; g < L.G; ++g)
+      for (int i = 0; i < 16; ++i) full = full && sh.tab[g * 16 + i].y == 0.0;
+  if (full) {
+    L.circ = lane < 3 ? lane : 0;
+    L.shift = L.circ == 1 ? kShift : L.circ == 2 ? -kShift : 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      L.fo0[i] = sh.tab[i].x;
+      L.fo1[i] = L.G == 2 ? sh.tab[16 + i].x : 0.0;
+      L.fin[i] = sh.init_state[i];
+    }
+    h2_optimise<-1>(sh, p, prob, bc, L, g_entry, g_loop);
+    return;
+  }
   switch (L.G) {  // warp-uniform: one specialised loop per group count
     case 1: h2_optimise<1>(sh, p, prob, bc, L, g_entry, g_loop); break;
     case 2: h2_optimise<2>(sh, p, prob, bc, L, g_entry, g_loop); break;
