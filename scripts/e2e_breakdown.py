@@ -10,7 +10,7 @@ from paper_2601_09951_b200 import vqeforge as V  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 V.init(0)
-for traj in (False, True):
+for traj in ((False,) if os.environ.get("E2E_NOTRAJ") else (False, True)):
     buf = V.SweepBuffers(V.SweepConfig(), trajectories=traj)
     for _ in range(5):
         buf.run()
