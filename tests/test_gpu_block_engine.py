@@ -145,3 +145,18 @@ def test_scaling_study_mid_widths_match_reference(gpu, ref):
     for r, w in zip(recs, want):
         assert r["n_qubits"] == w["n_qubits"] and r["iterations_run"] == w["iterations_run"]
         assert abs(r["final_energy"] - w["final_energy"]) < E_TOL
+
+
+def test_run_vqe_batch_hea_routes_per_problem(gpu, ref):
+    """run_vqe_batch with a 5-qubit HEA(2) (32 amplitudes per lane would
+    spill the one-warp engine): each problem runs on the shared-memory
+    engine and matches run_vqe and the reference."""
+    V = gpu
+    n = 5
+    hs = [ref.build_tfim(n, 1.0, f) for f in (0.5, 0.9, 1.3)]
+    cfg = V.AdamConfig(learning_rate=0.05, max_iterations=6)
+    rs = V.run_vqe_batch([to_v(V, h) for h in hs], V.AnsatzSpec.hardware_efficient(2), cfg)
+    for h, r in zip(hs, rs):
+        want = ref.run_vqe(h, kind=1, layers=2, lr=0.05, max_iter=6)
+        assert np.max(np.abs(np.array(r.trajectory) - want["trajectory"])) < E_TOL
+        assert r.circuit_evaluations == want["circuit_evaluations"]
