@@ -137,7 +137,10 @@ constexpr int kMaxRot = 72;     // (cos, sin) entries per launch (kernel paramet
 constexpr int kMaxSteps = 56;   // register steps per launch
 constexpr int kMaxPhases = 12;  // register phases per launch
 constexpr size_t kPhaseRot = 20;  // rotations per phase (bounds its steps and table entries)
-constexpr int kMaxHigh = 7;
+#ifndef VQF_TILE_MAX_HIGH
+#define VQF_TILE_MAX_HIGH 7
+#endif
+constexpr int kMaxHigh = VQF_TILE_MAX_HIGH;
 constexpr int kTileBlocks = 148;  // persistent: one CTA per SM
 #ifndef VQF_TILE_GROUPS
 #define VQF_TILE_GROUPS 4  // independent consumer groups per CTA (128 threads each)
@@ -155,7 +158,10 @@ constexpr int kTileBlocks = 148;  // persistent: one CTA per SM
 #define VQF_TILE_R32 5
 #endif
 constexpr int kStages = VQF_TILE_STAGES;
-constexpr int kLB64 = VQF_TILE_LB, kLB32 = VQF_TILE_LB + 1;
+#ifndef VQF_TILE_LB32
+#define VQF_TILE_LB32 (VQF_TILE_LB + 1)
+#endif
+constexpr int kLB64 = VQF_TILE_LB, kLB32 = VQF_TILE_LB32;
 constexpr int kR64 = 4, kR32 = VQF_TILE_R32;  // register bits per phase (16 / 32 amplitudes per thread)
 // consumer groups per CTA: 4 x 128 threads (<= 128 registers each); measured for fp32 against
 // 2 x 256 threads with 16 registers of amplitudes (scripts/build_variant.sh): 24.5 vs 33.6 ms per n = 30 layer
