@@ -1,6 +1,7 @@
 // Shared-memory VQE engine: a whole run_vqe (vqe.hpp:194-254) in ONE
 // cooperative launch for registers that fit one CTA's shared memory
-// (4 <= n <= 13 complex128, <= 14 complex64).
+// (4 <= n <= 13 complex128, <= 14 complex64; one qubit more with the state in
+// an L2-resident global buffer per CTA).
 //
 // The reference evaluates every Adam iteration as 1 + 2P fresh circuits
 // (energy(theta), then E(theta +- pi/2 e_k), vqe.hpp:112-127, :226-243).

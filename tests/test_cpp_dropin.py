@@ -40,7 +40,7 @@ def test_block_engine_frame_compilation():
     """compile_block_program (csrc/vqe_block.cu) replayed on the host: the
     frame-tracked rotation passes and rewritten Pauli masks give the same
     energies as the direct HEA circuit + reference expectation formula
-    (tests/cpp/block_frame_check.cpp), n = 4..13, 1-3 layers, fp64/fp32 plans."""
+    (tests/cpp/block_frame_check.cpp), n = 4..15, 1-3 layers, fp64/fp32 plans."""
     exe = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"block_frame_check_{os.getpid()}")
     cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
            "-I", os.path.join(ROOT, "paper_2601_09951_b200", "csrc"), "-I", "/usr/local/cuda/include",

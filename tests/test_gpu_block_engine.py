@@ -1,6 +1,6 @@
 """GPU parity of the shared-memory VQE engine (csrc/vqe_block.cu): one
-cooperative launch per run_vqe for hardware-efficient registers of 4..13
-qubits (complex128) / 4..14 (complex64).  Compared with the reference's own
+cooperative launch per run_vqe for hardware-efficient registers of 4..14
+qubits (complex128) / 4..15 (complex64).  Compared with the reference's own
 run_vqe (oracle/_ref, vqe.hpp:194-254): trajectories, final energies and
 parameters within 1e-10 Ha (fp64) / 1e-5 (fp32), identical iteration and
 circuit-evaluation counts, the reference's error messages, and the HBM
