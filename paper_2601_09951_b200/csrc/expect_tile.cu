@@ -47,9 +47,25 @@ struct V2<float> {
   using type = float2;
 };
 
-// consumer groups per CTA: fp64 3 x 128 threads, fp32 2 x 256 threads
+// consumer groups per CTA (fp64 3 x 128 threads, fp32 2 x 256 threads) and
+// tile buffers per group (fp64 1, fp32 2: 227 KB with the accumulators;
+// fp64 2 x 2 measured 7 % slower than 3 x 1)
+#ifndef VQF_EXP_GROUPS64
+#define VQF_EXP_GROUPS64 3
+#endif
+#ifndef VQF_EXP_BUFS64
+#define VQF_EXP_BUFS64 1
+#endif
+#ifndef VQF_EXP_GROUPS32
+#define VQF_EXP_GROUPS32 2
+#endif
+#ifndef VQF_EXP_BUFS32
+#define VQF_EXP_BUFS32 2
+#endif
 template <typename T>
-constexpr int kEGroupsOf = sizeof(T) == 8 ? 3 : 2;
+constexpr int kEGroupsOf = sizeof(T) == 8 ? VQF_EXP_GROUPS64 : VQF_EXP_GROUPS32;
+template <typename T>
+constexpr int kEBufsOf = sizeof(T) == 8 ? VQF_EXP_BUFS64 : VQF_EXP_BUFS32;
 constexpr int kAcc = kExpPhases * kExpSlots * kExpTerms;
 constexpr int kEBlocks = 148;
 template <typename T>
@@ -64,42 +80,47 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
     k_expect_tile(const __grid_constant__ CUtensorMap map, const __grid_constant__ ExpTileParams p,
                   double* __restrict__ partials) {
   using A = typename V2<T>::type;
-  constexpr int kEGroups = kEGroupsOf<T>;
+  constexpr int kEGroups = kEGroupsOf<T>, kBufs = kEBufsOf<T>;
   constexpr uint32_t NT = 1u << (LB - kER), NL = 1u << LB, NR = 1u << kER;
   constexpr uint32_t tile_bytes = NL * sizeof(A);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const uint32_t group = threadIdx.x / NT, gt = threadIdx.x % NT;
-  A* t = reinterpret_cast<A*>(smem + (size_t)group * tile_bytes);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kEGroups * (size_t)tile_bytes) + group;  // 1 KB gap
+  // the group's ring of kBufs tile buffers and their mbarriers (1 KB gap)
+  A* const ring = reinterpret_cast<A*>(smem + (size_t)group * kBufs * tile_bytes);
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + kEGroups * kBufs * (size_t)tile_bytes) + group * kBufs;
   const uint64_t n_tiles = uint64_t{1} << (p.n - p.B - p.k);
   const uint32_t mid_bits = p.h - p.B;
   const uint64_t top_per_entry = uint64_t{1} << (p.n - p.h - p.k);
   if (gt == 0) {
     if (group == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
-    mbar_init(bar, 1);
+    for (int b = 0; b < kBufs; ++b) mbar_init(&bars[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   // tile T of the entry: mid = low (h - B) bits of T, top = the rest
-  const auto issue_load = [&](uint64_t tile) {
+  const uint64_t step = kEGroups * (uint64_t)gridDim.x;
+  // the group's i-th tile goes to buffer i % kBufs
+  const auto issue_load = [&](uint64_t tile, int b) {
     if (gt == 0) {
-      mbar_expect_tx(bar, tile_bytes);
-      tma_load_window(t, &map, static_cast<int32_t>(tile & ((uint64_t{1} << mid_bits) - 1)),
-                      static_cast<int32_t>((tile >> mid_bits) + blockIdx.y * top_per_entry), bar);
+      mbar_expect_tx(&bars[b], tile_bytes);
+      tma_load_window(ring + (size_t)b * NL, &map, static_cast<int32_t>(tile & ((uint64_t{1} << mid_bits) - 1)),
+                      static_cast<int32_t>((tile >> mid_bits) + blockIdx.y * top_per_entry), &bars[b]);
     }
   };
-  const uint64_t step = kEGroups * (uint64_t)gridDim.x;
   const uint64_t first = blockIdx.x + (uint64_t)group * gridDim.x;
-  if (first < n_tiles) issue_load(first);
+  for (int b = 0; b < kBufs; ++b)
+    if (first + b * step < n_tiles) issue_load(first + b * step, b);
   // one fp64 accumulator per (phase, slot, term) and thread, slot-major in
   // shared memory behind the tiles (consecutive threads, consecutive words)
   const uint32_t nthr = blockDim.x;
-  double* acc = reinterpret_cast<double*>(smem + kEGroups * (size_t)tile_bytes + 1024);
+  double* acc = reinterpret_cast<double*>(smem + kEGroups * kBufs * (size_t)tile_bytes + 1024);
   for (uint32_t q = 0; q < (uint32_t)kAcc; ++q) acc[q * nthr + threadIdx.x] = 0.0;
   uint64_t tile = first;
   for (uint32_t it = 0; tile < n_tiles; tile += step, ++it) {
-    mbar_wait(bar, it & 1u);
+    const int buf = static_cast<int>(it % kBufs);
+    const A* t = ring + (size_t)buf * NL;
+    mbar_wait(&bars[buf], (it / kBufs) & 1u);
     // global index of the tile's local index 0: (top << (h + k)) | (mid << B)
     const uint64_t g0 = ((tile >> mid_bits) << (p.h + p.k)) | ((tile & ((uint64_t{1} << mid_bits) - 1)) << p.B);
 #pragma unroll
@@ -126,15 +147,45 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
         x[r] = t[o];
       }
       if (ph + 1 == (int)p.n_phases) {
-        // every thread has read the tile: refill the buffer with the next one
+        // every thread has read the tile: refill its buffer kBufs tiles ahead
         group_sync<NT>(group);
-        if (tile + step < n_tiles) issue_load(tile + step);
+        if (tile + kBufs * step < n_tiles) issue_load(tile + kBufs * step, buf);
       }
       const uint64_t ib = g0 | ((uint64_t)(base_l >> p.B) << p.h) | (base_l & ((1u << p.B) - 1));
 #pragma unroll
       for (int j = 0; j < kExpSlots; ++j) {
         const ExpSlot& S = P.slot[j];
         if (S.n_terms == 0) continue;
+        if (S.n_terms == 1 && S.smask[0] == 0) {
+          // one term without Y / Z on the register bits (TFIM's X_q): the
+          // pair sum is FMA chains over Re(v) or Im(v), 2 ops per pair (fp64:
+          // four independent chains for latency; fp32 measured faster with one)
+          constexpr uint32_t kCh = sizeof(T) == 8 ? 4 : 1;
+          T pc[4] = {T(0), T(0), T(0), T(0)};
+          if (S.sigma[0]) {
+#pragma unroll
+            for (uint32_t r = 0, q = 0; r < NR; ++r) {
+              if (r & (1u << j)) continue;
+              const A a = x[r], b = x[r | (1u << j)];
+              pc[q % kCh] = fma(a.x, b.y, pc[q % kCh]);
+              pc[q % kCh] = fma(-a.y, b.x, pc[q % kCh]);
+              ++q;
+            }
+          } else {
+#pragma unroll
+            for (uint32_t r = 0, q = 0; r < NR; ++r) {
+              if (r & (1u << j)) continue;
+              const A a = x[r], b = x[r | (1u << j)];
+              pc[q % kCh] = fma(a.x, b.x, pc[q % kCh]);
+              pc[q % kCh] = fma(a.y, b.y, pc[q % kCh]);
+              ++q;
+            }
+          }
+          const T part = (pc[0] + pc[1]) + (pc[2] + pc[3]);
+          const double pd = static_cast<double>(part);
+          acc[((ph * kExpSlots + j) * kExpTerms) * nthr + threadIdx.x] += (__popcll(ib & S.yz[0]) & 1) ? -pd : pd;
+          continue;
+        }
         // pair products and the per-term sums over the thread's 8 pairs in
         // the storage precision (complex64 states: fp32, one conversion per
         // term instead of two per pair), accumulated across tiles in fp64
@@ -204,7 +255,7 @@ template <typename T>
 size_t exp_smem_bytes() {
   constexpr int LB = kELB<T>;
   constexpr int kEGroups = kEGroupsOf<T>;
-  const size_t tiles = kEGroups * (sizeof(typename V2<T>::type) << LB);
+  const size_t tiles = kEGroups * kEBufsOf<T> * (sizeof(typename V2<T>::type) << LB);
   const size_t accs = sizeof(double) * kAcc * (kEGroups << (LB - kER));
   return 1024 + tiles + 1024 + accs;  // align slack, tiles, mbarriers (in the 1 KB gap), accumulators
 }
