@@ -419,11 +419,19 @@ def run_ours(args, rank, world, local_rank):
     from paper_2601_09951_b200 import vqeforge as V
 
     dist = None
+    # VQF_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 over gloo, so
+    # the N > 1 path runs on a one-GPU box; NCCL refuses two ranks per GPU
+    shared = os.environ.get("VQF_BENCH_SHARE_GPU") == "1"
+    if shared:
+        local_rank = 0
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     V.init(local_rank)
 
@@ -433,7 +441,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(local_rank)
 
     def max_over_ranks(x):
-        return D.max_over_ranks(x, dist, f"cuda:{local_rank}")
+        return D.max_over_ranks(x, dist, "cpu" if shared else f"cuda:{local_rank}")
 
     clocks = ClockSampler(local_rank)
     cfg = V.SweepConfig(chunk_index=rank, n_chunks=world)
