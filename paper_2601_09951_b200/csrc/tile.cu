@@ -127,6 +127,39 @@ const CUtensorMap* cached_window_map(const vqf_statevector* sv, uint32_t h, uint
   maps.emplace_back(key, window_map(sv, h, k));
   return &maps.back().second;
 }
+CUtensorMap tile_map(const vqf_statevector* sv, uint32_t B, uint32_t h, uint32_t k) {
+  const bool f64 = sv->dtype == VQF_F64;
+  const uint64_t amp = f64 ? 16 : 8;
+  const uint32_t rb = f64 ? 3 : 4;  // bits of one 128 B row
+  const uint32_t n = sv->n_qubits;
+  if (B < rb || h < B || h + k > n || k > 8 || (1u << (B - rb + k)) > 256)
+    throw Error(VQF_LOGIC_ERROR, "tile map: bad window");
+  const cuuint64_t dims[5] = {f64 ? 16u : 32u, uint64_t{1} << (B - rb), uint64_t{1} << (h - B), uint64_t{1} << k,
+                              (uint64_t{1} << (n - h - k)) * sv->batch};
+  const cuuint64_t strides[4] = {128, (uint64_t{1} << B) * amp, (uint64_t{1} << h) * amp,
+                                 (uint64_t{1} << (h + k)) * amp};
+  const cuuint32_t box[5] = {f64 ? 16u : 32u, 1u << (B - rb), 1, 1u << k, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = encode_fn()(&m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+                                 sv->amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(VQF_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+const CUtensorMap* cached_tile_map(const vqf_statevector* sv, uint32_t B, uint32_t h, uint32_t k) {
+  static thread_local std::vector<std::pair<std::pair<const void*, uint64_t>, CUtensorMap>> maps;
+  const auto key = std::make_pair(static_cast<const void*>(sv->amps),
+                                  (uint64_t)h | ((uint64_t)k << 8) | ((uint64_t)B << 12) | ((uint64_t)sv->n_qubits << 16) |
+                                      ((uint64_t)sv->batch << 24) | ((uint64_t)sv->dtype << 62));
+  for (auto& e : maps)
+    if (e.first == key) return &e.second;
+  if (maps.size() > 64) maps.erase(maps.begin());
+  maps.emplace_back(key, tile_map(sv, B, h, k));
+  return &maps.back().second;
+}
 }  // namespace tma
 
 namespace {
@@ -260,6 +293,7 @@ struct TilePhase {
 struct TileParams {
   uint32_t n, B, k, batch, n_phases;
   uint32_t merge;  // hb[0..merge) = B, B+1, ...: 2^merge adjacent runs move as one TMA box
+  uint32_t win;    // 1: hb is one window [hb[0], hb[0] + k) and the map a tile map: one box per tile
   uint32_t hb[kMaxHigh];  // global bit of local bit B + j, ascending
   const double* cs;       // per-entry (cos, sin) table: cs[2 (param * batch + entry)]
   // Permutation-only pass (every gate X / CNOT): the tile is written back as
@@ -403,6 +437,13 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
   __shared__ volatile uint32_t issued[8];
   static_assert(kSlotsOf<T> <= 8, "tile ring: at most 8 slots");
   const auto stage_buf = [&](int st) { return reinterpret_cast<A*>(ring + (size_t)st * tile_bytes); };
+  // tile map coordinates (p.win): mid = the tile's bits below the window,
+  // top = the rest, batch entries stacked above
+  const uint32_t mid_bits = p.win ? p.hb[0] - p.B : 0;
+  const auto win_mid = [&](uint64_t tile) { return static_cast<int32_t>(tile & ((uint64_t{1} << mid_bits) - 1)); };
+  const auto win_top = [&](uint64_t tile) {
+    return static_cast<int32_t>((tile >> mid_bits) + ((uint64_t)entry << (p.n - p.hb[0] - p.k)));
+  };
   const auto issue_load = [&](uint64_t tile, int st) {
     const uint32_t lane = gt;
     if (lane == 0) {
@@ -410,6 +451,10 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
       issued[st] = static_cast<uint32_t>((tile - blockIdx.x) / gridDim.x);
     }
     unsigned char* dst = reinterpret_cast<unsigned char*>(stage_buf(st));
+    if (p.win) {
+      if (lane == 0) tma_load_tile(dst, &map, win_mid(tile), win_top(tile), &bar[st]);
+      return;
+    }
     for (uint32_t j = lane; j < (n_runs >> p.merge); j += 32)
       tma_load_run(dst + ((size_t)j << p.merge) * run_bytes, &map,
                    static_cast<int32_t>(run_start(p, tile, j << p.merge) / amps_per_row), entry, &bar[st]);
@@ -469,9 +514,13 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
         group_sync<NT>(group);
       }
       if (!direct && gt < 32) {
-        for (uint32_t j = gt; j < (n_runs >> p.merge); j += 32)
-          tma_store_run(reinterpret_cast<unsigned char*>(t) + ((size_t)j << p.merge) * run_bytes, &map,
-                        static_cast<int32_t>(run_start(p, tile, j << p.merge) / amps_per_row), entry);
+        if (p.win) {
+          if (gt == 0) tma_store_tile(t, &map, win_mid(tile), win_top(tile));
+        } else {
+          for (uint32_t j = gt; j < (n_runs >> p.merge); j += 32)
+            tma_store_run(reinterpret_cast<unsigned char*>(t) + ((size_t)j << p.merge) * run_bytes, &map,
+                          static_cast<int32_t>(run_start(p, tile, j << p.merge) / amps_per_row), entry);
+        }
         bulk_commit();
         bulk_wait_read();  // this lane's stores have read the buffer
         __syncwarp();
@@ -1055,11 +1104,17 @@ void launch_pass(vqf_statevector* sv, const std::vector<TGate>& gates, const Pas
   uint32_t merge = 0;
   while (merge < pass.hbits.size() && pass.hbits[merge] == B + merge && (run_bytes << (merge + 1)) <= 32768u) ++merge;
   if (sizeof(T) == 8 || std::getenv("VQF_TILE_NO_MERGE")) merge = 0;  // measured: fp32 +10%, fp64 -1.4%
-  const CUtensorMap* map = tma::cached_state_map(sv, run_bytes << merge);
+  // a pass whose gathered bits form one window moves each tile as one 5-d box
+  bool win = !pass.hbits.empty() && pass.hbits[0] >= B && !std::getenv("VQF_TILE_NO_WINDOW");
+  for (size_t m = 1; win && m < pass.hbits.size(); ++m) win = pass.hbits[m] == pass.hbits[0] + m;
+  if (win) merge = 0;
+  const CUtensorMap* map = win ? tma::cached_tile_map(sv, B, pass.hbits[0], static_cast<uint32_t>(pass.hbits.size()))
+                               : tma::cached_state_map(sv, run_bytes << merge);
   const size_t smem = kSlotsOf<T> * (sizeof(typename V2<T>::type) << LB) + 8 * kSlotsOf<T> + 1024;
   auto* amps = static_cast<typename V2<T>::type*>(sv->amps);
   for (TileParams& p : build_launches<T>(n, sv->batch, B, gates, pass, cs_dev)) {
     p.merge = merge;
+    p.win = win ? 1u : 0u;
     const dim3 g(grid, active);
     const unsigned threads = kGroups << (LB - R);
     constexpr int LBmax = sizeof(T) == 8 ? kLB64 : kLB32;

@@ -102,5 +102,27 @@ __device__ __forceinline__ void tma_load_window(void* dst, const CUtensorMap* ma
       : "memory");
 }
 
+// Tile map of a fused pass whose gathered bits are one window [h, h + k):
+// the state as {128 B row, run rows, mid, window, top x batch} with runs of
+// 2^B amplitudes (B >= the row's bits), so ONE 5-d box moves the whole tile
+// (2^(B + k) amplitudes, the run-by-run smem image: run w at w * run bytes).
+CUtensorMap tile_map(const vqf_statevector* sv, uint32_t B, uint32_t h, uint32_t k);
+const CUtensorMap* cached_tile_map(const vqf_statevector* sv, uint32_t B, uint32_t h, uint32_t k);
+
+// One tile of a tile map: coordinates {0, 0, mid, 0, top}.
+__device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* map, int32_t mid, int32_t top,
+                                              uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(0), "r"(0), "r"(mid), "r"(0), "r"(top), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_tile(const void* src, const CUtensorMap* map, int32_t mid, int32_t top) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(map),
+               "r"(0), "r"(0), "r"(mid), "r"(0), "r"(top), "r"(smem_addr(src))
+               : "memory");
+}
+
 }  // namespace tma
 }  // namespace vqf
