@@ -247,8 +247,24 @@ __device__ __forceinline__ void givens(P& a, P& b, T c, T s) {
   b.y = fma(s, u.y, c * v.y);
 }
 
+// Factored RY steps (fp32): every Givens rotation scales both outputs by the
+// same factor, so a slot's RY runs as
+//   |c| >= |s|: a' = u - k v, b' = v + k u   (k = s / c, factor c)
+//   else      : a' = k u - v, b' = u + k v   (k = c / s, factor s)
+// -- 2 FMAs per amplitude component instead of a multiply and an FMA -- and
+// the product of the factors, equal for all the thread's amplitudes, is
+// applied once at the end of the phase.  rts[q] = (k, factor), rform[q] =
+// the branch; entry 0 = (0, 1): identity, exact.  fp64 keeps the direct form
+// (the factored one spills there and measured 6 % slower).
+#ifndef VQF_TILE_FACTORED32
+#define VQF_TILE_FACTORED32 1
+#endif
+template <typename T>
+constexpr bool kFactored = sizeof(T) == 4 && VQF_TILE_FACTORED32;
+
 template <int R, typename P, typename T>
-__device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, const double2* rcs) {
+__device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, const double2* rcs, const double2* rts,
+                                         const uint8_t* rform, T& scale) {
   constexpr int NR = 1 << R;
   if (st.flags & 1u) {
     const double2 v = rcs[st.se];
@@ -262,11 +278,42 @@ __device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, con
   }
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    const double2 v = rcs[st.ry[j]];
-    const T c = static_cast<T>(v.x), sn = static_cast<T>(v.y);
+    if constexpr (kFactored<T>) {
+      const double2 v = rts[st.ry[j]];
+      const T k = static_cast<T>(v.x);
+      scale *= static_cast<T>(v.y);
+      if (rform[st.ry[j]] == 0) {
 #pragma unroll
-    for (int r = 0; r < NR; ++r)
-      if (!(r & (1 << j))) givens(x[r], x[r | (1 << j)], c, sn);
+        for (int r = 0; r < NR; ++r)
+          if (!(r & (1 << j))) {
+            P& a = x[r];
+            P& b = x[r | (1 << j)];
+            const P u = a;
+            a.x = fma(-k, b.x, u.x);
+            a.y = fma(-k, b.y, u.y);
+            b.x = fma(k, u.x, b.x);
+            b.y = fma(k, u.y, b.y);
+          }
+      } else {
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          if (!(r & (1 << j))) {
+            P& a = x[r];
+            P& b = x[r | (1 << j)];
+            const P u = a;
+            a.x = fma(k, u.x, -b.x);
+            a.y = fma(k, u.y, -b.y);
+            b.x = fma(k, b.x, u.x);
+            b.y = fma(k, b.y, u.y);
+          }
+      }
+    } else {
+      const double2 v = rcs[st.ry[j]];
+      const T c = static_cast<T>(v.x), sn = static_cast<T>(v.y);
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (!(r & (1 << j))) givens(x[r], x[r | (1 << j)], c, sn);
+    }
   }
 }
 
@@ -325,7 +372,8 @@ __device__ __forceinline__ uint64_t run_start(const TileParams& p, uint64_t tile
 // streams in while this one computes and stores.
 template <typename T, int R, int LB, int NT, typename Refill>
 __device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePhase& ph, const TileStep* steps,
-                                          const double2* rcs, uint32_t gt, uint32_t group,
+                                          const double2* rcs, const double2* rts, const uint8_t* rform,
+                                          uint32_t gt, uint32_t group,
                                           typename V2<T>::type* s, const uint64_t* run_off, uint32_t B,
                                           Refill&& refill) {
   using A = typename V2<T>::type;
@@ -359,7 +407,16 @@ __device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePha
     if (direct) refill();
   }
   const uint32_t n_steps = ph.n_steps, step0 = ph.step0;
-  for (uint32_t q = 0; q < n_steps; ++q) run_step<R, A, T>(x, steps[step0 + q], rcs);
+  T scale = T(1);
+  for (uint32_t q = 0; q < n_steps; ++q) run_step<R, A, T>(x, steps[step0 + q], rcs, rts, rform, scale);
+  if constexpr (kFactored<T>) {
+    if (n_steps != 0)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        x[r].x *= scale;
+        x[r].y *= scale;
+      }
+  }
   if (direct) {
     const uint32_t low = (1u << B) - 1;
 #pragma unroll
@@ -397,6 +454,8 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
   unsigned char* ring = smem;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSlots * (size_t)tile_bytes);
   __shared__ double2 rcs[kMaxRot];
+  __shared__ double2 rts[kFactored<T> ? kMaxRot : 1];
+  __shared__ uint8_t rform[kFactored<T> ? kMaxRot : 1];
   __shared__ uint16_t ftab[PERM ? 2 : 1][64];
   // run starts of the group's current tile (double-buffered: a fast thread
   // fills the next tile's while slow ones still store the current one)
@@ -427,6 +486,11 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
         v = *reinterpret_cast<const double2*>(p.cs + 2 * ((size_t)p.rot_param[q] * p.batch + blockIdx.y));
       if (p.rot_neg[q]) v.y = -v.y;
       rcs[q] = v;
+      if constexpr (kFactored<T>) {
+        const bool by_c = fabs(v.x) >= fabs(v.y);
+        rts[q] = by_c ? make_double2(v.y / v.x, v.x) : make_double2(v.x / v.y, v.y);
+        rform[q] = by_c ? 0 : 1;
+      }
     }
   }
   __syncthreads();
@@ -506,7 +570,7 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
         if (gt < 32 && ahead < n_tiles) issue_load(ahead, cur);
       };
       for (uint32_t ph = 0; ph < p.n_phases; ++ph) {
-        run_phase<T, R, LB, NT>(t, p.ph[ph], p.steps, rcs, gt, group, s, run_off, p.B, refill);
+        run_phase<T, R, LB, NT>(t, p.ph[ph], p.steps, rcs, rts, rform, gt, group, s, run_off, p.B, refill);
         if (ph + 1 == p.n_phases) {
           if (direct) break;
           fence_proxy_async();  // generic-proxy stores -> TMA store reads
