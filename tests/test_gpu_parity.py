@@ -114,6 +114,33 @@ def test_fused_wide_circuits_and_batches(gpu, n, batch):
     assert np.max(np.abs(a.amplitudes - b.amplitudes)) < 1e-12
 
 
+@pytest.mark.parametrize("n,dtype,batch", [(20, "f64", 1), (21, "f32", 1), (16, "f64", 3), (17, "f32", 2)])
+def test_fused_window_boxes_equal_run_boxes(gpu, n, dtype, batch, monkeypatch):
+    # passes whose gathered bits form one window move each tile as one 5-d
+    # TMA box (tile map); VQF_TILE_NO_WINDOW forces one box per run.  Same
+    # arithmetic, different data movement: bitwise equal, batched entries too
+    V = gpu
+    pr = random.Random(5150 + n)
+    hea = [V.Gate.ry(0.1 * (q + 1), q) for q in range(n)] + [V.Gate.cnot(q, q + 1) for q in range(n - 1)]
+    gates = hea + [gpu_gate(V, *g) for g in rand_gates(pr, n, 60)] + hea
+    rng = np.random.default_rng(n + 11)
+    psi0 = np.concatenate([random_state(rng, n) for _ in range(batch)])
+    out = []
+    for no_window in (False, True):
+        if no_window:
+            monkeypatch.setenv("VQF_TILE_NO_WINDOW", "1")
+        s = V.StateVector(n, dtype=dtype, batch=batch)
+        s.amplitudes = psi0
+        V.apply_circuit(s, gates)
+        out.append(s.amplitudes)
+    assert np.array_equal(out[0], out[1])
+    ref = V.StateVector(n, dtype=dtype, batch=batch)
+    ref.amplitudes = psi0
+    for g in gates:
+        V.apply_gate(ref, g)
+    assert np.max(np.abs(out[0] - ref.amplitudes)) < (1e-12 if dtype == "f64" else 2e-5)
+
+
 @pytest.mark.parametrize("n,dtype", [(5, "f64"), (12, "f64"), (16, "f64"), (19, "f32")])
 def test_fused_permutation_passes(gpu, n, dtype):
     # X / CNOT-only circuits: every tile pass is an affine index map applied
