@@ -75,7 +75,7 @@ constexpr int kEB = sizeof(T) == 8 ? 3 : 4;  // runs of 128 B
 constexpr int kER = kExpSlots;               // register bits per phase
 
 
-template <typename T, int LB>
+template <typename T, int LB, bool DIAG>
 __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
     k_expect_tile(const __grid_constant__ CUtensorMap map, const __grid_constant__ ExpTileParams p,
                   double* __restrict__ partials) {
@@ -116,6 +116,19 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
   const uint32_t nthr = blockDim.x;
   double* acc = reinterpret_cast<double*>(smem + kEGroups * kBufs * (size_t)tile_bytes + 1024);
   for (uint32_t q = 0; q < (uint32_t)kAcc; ++q) acc[q * nthr + threadIdx.x] = 0.0;
+  // folded diagonal group: sign of Z string t on the thread's amplitude r is
+  // parity(tile base) ^ parity(thread part) ^ parity(r & v_t); the thread
+  // parts are fixed (phase 0's layout), the tile parts come from one ballot
+  uint32_t thr_sig = 0;
+  double acc_diag = 0.0;
+  if constexpr (DIAG) {
+    uint32_t bl = 0;
+    for (int j = 0; j < LB - kER; ++j)
+      if ((gt >> j) & 1u) bl ^= p.ph[0].tb_l[j];
+    const uint64_t ti = ((uint64_t)(bl >> p.B) << p.h) | (bl & ((1u << p.B) - 1));
+    for (uint32_t q = 0; q < p.n_diag; ++q)
+      if (__popcll(ti & p.dmask[q]) & 1) thr_sig |= 1u << q;
+  }
   uint64_t tile = first;
   for (uint32_t it = 0; tile < n_tiles; tile += step, ++it) {
     const int buf = static_cast<int>(it % kBufs);
@@ -152,6 +165,35 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
         if (tile + kBufs * step < n_tiles) issue_load(tile + kBufs * step, buf);
       }
       const uint64_t ib = g0 | ((uint64_t)(base_l >> p.B) << p.h) | (base_l & ((1u << p.B) - 1));
+      if (DIAG && ph == 0) {
+        const uint32_t lane = threadIdx.x & 31u;
+        const bool tb = lane < p.n_diag && (__popcll(g0 & p.dmask[lane]) & 1);
+        const uint32_t sig = __ballot_sync(0xffffffffu, tb) ^ thr_sig;
+        // w[v] = sum_r (-1)^popc(r & v) |x_r|^2 (Walsh-Hadamard over the slots)
+        double w[NR];
+#pragma unroll
+        for (uint32_t r = 0; r < NR; ++r) {
+          const double re = static_cast<double>(x[r].x), im = static_cast<double>(x[r].y);
+          w[r] = fma(re, re, im * im);
+        }
+#pragma unroll
+        for (uint32_t hh = 1; hh < NR; hh <<= 1)
+#pragma unroll
+          for (uint32_t u = 0; u < NR; ++u)
+            if (!(u & hh)) {
+              const double l = w[u], r = w[u | hh];
+              w[u] = l + r;
+              w[u | hh] = l - r;
+            }
+        double d = 0.0;
+#pragma unroll
+        for (uint32_t v = 0; v < NR; ++v) {
+          double cv = 0.0;
+          for (uint32_t q = p.dv_off[v]; q < p.dv_off[v + 1]; ++q) cv += ((sig >> q) & 1u) ? -p.dc[q] : p.dc[q];
+          d = fma(cv, w[v], d);
+        }
+        acc_diag += d;
+      }
 #pragma unroll
       for (int j = 0; j < kExpSlots; ++j) {
         const ExpSlot& S = P.slot[j];
@@ -218,7 +260,20 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
     }
   }
   // fixed-order CTA reduction of the accumulators
+  __shared__ double diag_warp[32];
+  if constexpr (DIAG) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc_diag += __shfl_xor_sync(0xffffffffu, acc_diag, o);
+    if ((threadIdx.x & 31u) == 0) diag_warp[threadIdx.x >> 5] = acc_diag;
+  }
   __syncthreads();
+  if (DIAG && threadIdx.x == 0) {
+    double sd = 0.0;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) sd += diag_warp[w];
+    const size_t idx = ((size_t)blockIdx.y * p.G + 0) * p.nb + blockIdx.x;
+    partials[2 * idx] = sd;
+    partials[2 * idx + 1] = 0.0;
+  }
   const double* red = acc;
   __shared__ double term_sum[kAcc];
   if (threadIdx.x < (uint32_t)kAcc) {
@@ -371,8 +426,10 @@ std::vector<ExpTileParams> plan_expect_tiles(const CompiledHam& h, uint32_t n, i
         P.tb_s[j] = static_cast<uint16_t>(f64 ? tma::swz<double>(1u << tb[j]) : tma::swz<float>(1u << tb[j]));
         P.tb_l[j] = static_cast<uint16_t>(1u << tb[j]);
       }
-      for (uint32_t j = 0; j < (uint32_t)kExpSlots; ++j)
+      for (uint32_t j = 0; j < (uint32_t)kExpSlots; ++j) {
         P.rv_s[j] = static_cast<uint16_t>(f64 ? tma::swz<double>(1u << regs[j]) : tma::swz<float>(1u << regs[j]));
+        p.reg_gbit[p.n_phases - 1][j] = static_cast<uint8_t>(global_of(regs[j]));
+      }
       for (size_t s = 0; s < std::min<size_t>(kExpSlots, mine.size() - c0); ++s) {
         const uint32_t g = mine[c0 + s].second;
         ExpSlot& S = P.slot[s];
@@ -406,13 +463,48 @@ std::vector<ExpTileParams> plan_expect_tiles(const CompiledHam& h, uint32_t n, i
   return out;
 }
 
+bool fold_diag_into_tiles(std::vector<ExpTileParams>& passes, const CompiledHam& h, int32_t dtype) {
+  if (dtype != VQF_F64 || passes.empty() || h.group_flip.empty() || h.group_flip[0] != 0 ||
+      std::getenv("VQF_NO_DIAG_FOLD"))
+    return false;
+  const uint32_t t0 = h.group_offset[0], t1 = h.group_offset[1];
+  if (t1 <= t0 || t1 - t0 > (uint32_t)kExpDiag) return false;
+  for (uint32_t t = t0; t < t1; ++t)
+    if (h.terms[t].cb_im != 0.0) return false;
+  // the pass with the fewest register phases (the last one among equals)
+  size_t best = 0;
+  for (size_t i = 0; i < passes.size(); ++i)
+    if (passes[i].n_phases <= passes[best].n_phases) best = i;
+  ExpTileParams& p = passes[best];
+  std::vector<std::pair<uint32_t, uint32_t>> byv;  // (register pattern, term)
+  for (uint32_t t = t0; t < t1; ++t) {
+    uint32_t v = 0;
+    for (uint32_t j = 0; j < (uint32_t)kExpSlots; ++j)
+      if ((h.terms[t].yz >> p.reg_gbit[0][j]) & 1u) v |= 1u << j;
+    byv.emplace_back(v, t);
+  }
+  std::stable_sort(byv.begin(), byv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  p.n_diag = t1 - t0;
+  for (uint32_t v = 0, q = 0; v <= 16; ++v) {
+    while (q < byv.size() && byv[q].first < v) ++q;
+    p.dv_off[v] = q;
+  }
+  for (size_t q = 0; q < byv.size(); ++q) {
+    p.dmask[q] = h.terms[byv[q].second].yz;
+    p.dc[q] = h.terms[byv[q].second].cb_re;
+  }
+  return true;
+}
+
 namespace {
 template <typename T>
 void launch_t(vqf_statevector* sv, std::vector<ExpTileParams>& passes, double* partials, uint32_t G, uint32_t nb) {
   constexpr int LB = kELB<T>;
   static thread_local int opted = -1;
   if (opted != sv->device) {
-    VQF_CUDA(cudaFuncSetAttribute(k_expect_tile<T, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    VQF_CUDA(cudaFuncSetAttribute(k_expect_tile<T, LB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(exp_smem_bytes<T>())));
+    VQF_CUDA(cudaFuncSetAttribute(k_expect_tile<T, LB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(exp_smem_bytes<T>())));
     opted = sv->device;
   }
@@ -422,8 +514,10 @@ void launch_t(vqf_statevector* sv, std::vector<ExpTileParams>& passes, double* p
     p.G = G;
     p.nb = nb;
     const CUtensorMap* map = tma::cached_window_map(sv, p.h, p.k);
-    k_expect_tile<T, LB><<<dim3(grid, sv->batch), kEGroupsOf<T> << (LB - kER), exp_smem_bytes<T>(), sv->stream>>>(
-        *map, p, partials);
+    const dim3 g(grid, sv->batch);
+    const unsigned threads = kEGroupsOf<T> << (LB - kER);
+    if (p.n_diag) k_expect_tile<T, LB, true><<<g, threads, exp_smem_bytes<T>(), sv->stream>>>(*map, p, partials);
+    else k_expect_tile<T, LB, false><<<g, threads, exp_smem_bytes<T>(), sv->stream>>>(*map, p, partials);
     VQF_LAUNCHED();
   }
 }

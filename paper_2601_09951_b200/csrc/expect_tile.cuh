@@ -11,6 +11,7 @@ namespace vqf {
 constexpr int kExpPhases = 3;  // register phases per tile pass
 constexpr int kExpSlots = 4;   // register bits (flip groups) per phase
 constexpr int kExpTerms = 2;   // terms per flip group
+constexpr int kExpDiag = 32;   // diagonal terms one pass can fold in (TFIM's Z Z to n = 33)
 
 // One single-bit flip group in a register slot of a phase.
 struct ExpSlot {
@@ -34,6 +35,14 @@ struct ExpPhase {
 struct ExpTileParams {
   uint32_t n, B, k, h, n_phases, G, nb;
   ExpPhase ph[kExpPhases];
+  uint8_t reg_gbit[kExpPhases][kExpSlots];  // global index bit of each register slot
+  // Folded diagonal group (one pass at most; n_diag = 0 elsewhere): real
+  // coefficients dc of Z strings dmask, sorted by their register-slot pattern
+  // v in phase 0 (terms [dv_off[v], dv_off[v + 1])).
+  uint32_t n_diag;
+  uint32_t dv_off[17];
+  uint64_t dmask[kExpDiag];
+  double dc[kExpDiag];
 };
 
 // Groups whose flip is one index bit and that hold <= kExpTerms terms are read
@@ -41,6 +50,13 @@ struct ExpTileParams {
 // ONE read of the state.  Returns the passes; `taken[g]` marks the groups.
 std::vector<ExpTileParams> plan_expect_tiles(const CompiledHam& h, uint32_t n, int32_t dtype,
                                              std::vector<char>& taken);
+
+// Folds the diagonal group (group 0) into the pass with the fewest register
+// phases when it holds 1..kExpDiag Z strings with real coefficients, so the
+// separate diagonal read of the state goes away (fp64 only: measured TFIM
+// n = 30 16.7 -> 14.6 ms, n = 28 equal; in fp32 the folded pass turns
+// instruction-bound, n = 28 2.33 -> 2.78 ms).  Returns whether it did.
+bool fold_diag_into_tiles(std::vector<ExpTileParams>& passes, const CompiledHam& h, int32_t dtype);
 
 // Enqueues the passes on sv's stream; each writes per-CTA complex partials
 // of its groups to partials[((entry * G) + group) * nb + block].

@@ -982,7 +982,9 @@ ExpPlan plan_expectation(const CompiledHam& h, uint32_t n, int32_t dtype = VQF_F
   std::vector<char> on_tiles;
   pl.tiles = plan_expect_tiles(h, n, dtype, on_tiles);
   pl.all = h.terms;
-  if (G > 0 && h.group_offset[1] > h.group_offset[0]) {
+  // a small real diagonal group rides along in one tile pass
+  const bool diag_folded = fold_diag_into_tiles(pl.tiles, h, dtype);
+  if (!diag_folded && G > 0 && h.group_offset[1] > h.group_offset[0]) {
     // tiled split: support all below / all above the 2048-amplitude tile, mixed
     pl.B = std::min<uint32_t>(n, 11);
     const uint64_t lo_mask = (uint64_t{1} << pl.B) - 1;

@@ -188,12 +188,13 @@ def test_expectation_plan_packs_flip_groups(V):
         assert p["multi_passes"] == -(-high // 4)
         assert p["state_passes"] == 1 + p["multi_passes"]
     # from 11 qubits: gathered-tile passes (expect_tile.cu), up to 3 phases x 4
-    # single-bit groups each, windows of contiguous high bits
+    # single-bit groups each, windows of contiguous high bits; the fp64 plan
+    # folds the n - 1 real Z Z terms into one of them (no diagonal pass)
     for n, passes in [(11, 1), (12, 2), (20, 3), (26, 3), (30, 4), (33, 4)]:
         p = V.expectation_plan(V.build_tfim(n, 1.0, 1.0))
         assert p["flip_groups"] == n
         assert p["multi_passes"] == passes, (n, p)
-        assert p["state_passes"] == 1 + passes
+        assert p["state_passes"] == passes
     assert V.expectation_plan(V.build_z_sum(24)) == {"state_passes": 1, "flip_groups": 0, "multi_passes": 0}
     # below 9 qubits there are no register passes: one pass per group
     p = V.expectation_plan(V.build_tfim(6, 1.0, 1.0))

@@ -769,3 +769,34 @@ def test_expectation_tile_passes_single_bit_flips(gpu, orc, n, dtype):
     assert abs(got - want) < (E_TOL if dtype == "f64" else 1e-5 * max(1.0, abs(want)))
     plan = V.expectation_plan(to_v(V, h))
     assert plan["state_passes"] < n  # groups share tile passes
+
+
+@pytest.mark.parametrize("n,batch,n_diag", [(11, 1, 10), (14, 2, 32), (20, 1, 24), (22, 3, 45)])
+def test_expectation_diagonal_folded_into_tile_pass(gpu, orc, n, batch, n_diag, monkeypatch):
+    """fp64: a real diagonal group of <= 32 Z strings is evaluated inside one
+    gathered-tile pass (Walsh-Hadamard over the register slots, tile signs
+    by ballot) instead of its own pass; Z strings on every kind of bit
+    (register slots, thread bits, tile bits), batched entries, against the
+    oracle and against the unfolded plan (more than 32 strings: not folded)."""
+    V = gpu
+    pr = random.Random(900 + n)
+    terms = [(pr.uniform(-2, 2), [(q, 1)]) for q in range(n)]  # single-bit flip groups -> tile passes
+    for _ in range(n_diag):
+        ws = sorted(pr.sample(range(n), pr.randint(1, 4)))
+        terms.append((pr.uniform(-2, 2), [(w, 3) for w in ws]))
+    h = orc.canonicalize(Ham(n, terms))
+    n_z = sum(1 for _, axes in h.terms if axes and all(p == 3 for _, p in axes))
+    hv = to_v(V, h)
+    rng = np.random.default_rng(n + 5)
+    psis = [random_state(rng, n) for _ in range(batch)]
+    s = V.StateVector(n, batch=batch)
+    s.amplitudes = np.concatenate(psis)
+    folded = V.expectation_plan(hv)["state_passes"]
+    got = np.atleast_1d(V.expectation(s, hv))
+    for g, p in zip(got, psis):
+        assert abs(g - orc.expectation(n, p, h)) < E_TOL
+    monkeypatch.setenv("VQF_NO_DIAG_FOLD", "1")
+    unfolded = V.expectation_plan(hv)["state_passes"]
+    assert unfolded == folded + (1 if n_z <= 32 else 0)
+    got2 = np.atleast_1d(V.expectation(s, hv))
+    assert max(abs(a - b) for a, b in zip(got, got2)) < 1e-11
