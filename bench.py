@@ -323,10 +323,10 @@ def configs_3_4(V, torch, device, n_big, steps, warmup, peak, cpu_ok, cpu_second
         if ref is not None:
             rh = ref.canonicalize(ref.random_hamiltonian(20260804, n, 32))
             rnd = V.QubitHamiltonian(n, [V.PauliTerm(c, a) for c, a in rh.terms])
-        tp = V.expectation_plan(tfim)["state_passes"]
+        tp = V.expectation_plan(tfim, dtype)["state_passes"]
         kernels["tfim_expectation"] = (lambda: V.expectation(psi, tfim), Sd * tp)
         if rnd is not None:
-            rp = V.expectation_plan(rnd)["state_passes"]
+            rp = V.expectation_plan(rnd, dtype)["state_passes"]
             kernels["random32_expectation"] = (lambda: V.expectation(psi, rnd), Sd * rp)
         res = {"n_qubits": n, "state_bytes": Sd}
         for name, (fn, alg) in kernels.items():

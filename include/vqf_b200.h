@@ -290,6 +290,11 @@ int vqf_circuit_plan(uint32_t n_qubits, int32_t dtype, const vqf_gate* gates, ui
  * flip groups each.  Any out pointer may be NULL. */
 int vqf_expectation_plan(const vqf_hamiltonian* h, uint32_t* state_passes, uint32_t* flip_groups,
                          uint32_t* multi_passes);
+/* The same for a state of the given dtype (VQF_F64 / VQF_F32: the tile
+ * geometry and the folding of the diagonal group differ); the plain call
+ * plans for VQF_F64. */
+int vqf_expectation_plan_ex(const vqf_hamiltonian* h, int32_t dtype, uint32_t* state_passes, uint32_t* flip_groups,
+                            uint32_t* multi_passes);
 /* Raw device address and byte size of the amplitudes (for exchanging
  * shards with NCCL / peer copies; the handle keeps ownership). */
 int vqf_sv_device_ptr(vqf_sv sv, void** ptr, uint64_t* bytes);

@@ -141,6 +141,7 @@ SIGNATURES = [
     ("vqf_expectation_complex", C.c_int, [SV, C.POINTER(Hamiltonian), dp]),
     ("vqf_circuit_plan", C.c_int, [C.c_uint32, C.c_int32, C.POINTER(Gate), C.c_uint32, u32p, u32p]),
     ("vqf_expectation_plan", C.c_int, [C.POINTER(Hamiltonian), u32p, u32p, u32p]),
+    ("vqf_expectation_plan_ex", C.c_int, [C.POINTER(Hamiltonian), C.c_int32, u32p, u32p, u32p]),
     ("vqf_sv_device_ptr", C.c_int, [SV, C.POINTER(C.c_void_p), u64p]),
     ("vqf_cross_expectation", C.c_int, [SV, SV, C.POINTER(Hamiltonian), dp]),
     ("vqf_prepare_ansatz", C.c_int, [C.c_int32, C.c_uint32, dp, C.c_uint32, SV]),

@@ -1602,10 +1602,16 @@ int vqf_circuit_plan(uint32_t n_qubits, int32_t dtype, const vqf_gate* gates, ui
 
 int vqf_expectation_plan(const vqf_hamiltonian* h, uint32_t* state_passes, uint32_t* flip_groups,
                          uint32_t* multi_passes) {
+  return vqf_expectation_plan_ex(h, VQF_F64, state_passes, flip_groups, multi_passes);
+}
+
+int vqf_expectation_plan_ex(const vqf_hamiltonian* h, int32_t dtype, uint32_t* state_passes, uint32_t* flip_groups,
+                            uint32_t* multi_passes) {
   return guarded([&] {
     if (h == nullptr) throw_invalid("null hamiltonian");
+    if (dtype != VQF_F64 && dtype != VQF_F32) throw_invalid("expectation plan: unknown dtype");
     const CompiledHam c = compile_hamiltonian(h);
-    const ExpPlan pl = plan_expectation(c, h->n_qubits);
+    const ExpPlan pl = plan_expectation(c, h->n_qubits, dtype);
     uint32_t groups = 0;
     for (size_t g = 1; g < c.group_flip.size(); ++g) groups += c.group_offset[g + 1] > c.group_offset[g] ? 1 : 0;
     if (state_passes) *state_passes = pl.state_passes();

@@ -246,13 +246,15 @@ def circuit_plan(n_qubits: int, gates: Sequence[Gate], dtype: str = "f64") -> di
     return {"passes": p.value, "fused_ops": f.value}
 
 
-def expectation_plan(h: QubitHamiltonian) -> dict:
-    """How expectation() reads the state for h: HBM passes over the state,
-    distinct flip groups (the reference's per-group passes, statevector.hpp:
-    235-241) and the multi-group register passes among them.  Host only."""
+def expectation_plan(h: QubitHamiltonian, dtype: str = "f64") -> dict:
+    """How expectation() reads a `dtype` state for h: HBM passes over the
+    state, distinct flip groups (the reference's per-group passes,
+    statevector.hpp:235-241) and the multi-group register passes among them.
+    Host only."""
     keep, hs = h.as_c()
     sp, fg, mp = C.c_uint32(), C.c_uint32(), C.c_uint32()
-    check(lib.vqf_expectation_plan(C.byref(hs), C.byref(sp), C.byref(fg), C.byref(mp)))
+    check(lib.vqf_expectation_plan_ex(C.byref(hs), A.F64 if dtype == "f64" else A.F32, C.byref(sp), C.byref(fg),
+                                      C.byref(mp)))
     return {"state_passes": sp.value, "flip_groups": fg.value, "multi_passes": mp.value}
 
 

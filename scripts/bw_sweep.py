@@ -79,7 +79,7 @@ def main():
             ]:
                 t = timed(stream, lambda: V.expectation(psi, h), reps=3)
                 rows.append(("expect:" + name, (), S * groups, t))
-                plans["expect:" + name] = V.expectation_plan(h)
+                plans["expect:" + name] = V.expectation_plan(h, "f32" if f32 else "f64")
             import random
 
             rh = random_hamiltonian(random.Random(20260804), n, 32)
@@ -90,7 +90,7 @@ def main():
                 flips.add(f)
             t = timed(stream, lambda: V.expectation(psi, hv), reps=3)
             rows.append(("expect:random32", (), S * len(flips | {0}), t))
-            plans["expect:random32"] = V.expectation_plan(hv)
+            plans["expect:random32"] = V.expectation_plan(hv, "f32" if f32 else "f64")
         for kind, wires, alg, t in rows:
             gbs = alg / t / 1e9
             rec = {"n": n, "dtype": "f32" if f32 else "f64", "kernel": kind, "wires": list(wires), "alg_bytes": alg,

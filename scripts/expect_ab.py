@@ -21,6 +21,6 @@ for n in [int(a) for a in sys.argv[1:]] or [28, 30]:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s); e = V.expectation(psi, h); e1.record(s); torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
-        print(f"{os.environ.get('TAG', '')} {dt} n={n} {name} passes={V.expectation_plan(h)['state_passes']}: {statistics.median(ts[2:]):.3f} ms  E={e!r}", flush=True)
+        print(f"{os.environ.get('TAG', '')} {dt} n={n} {name} passes={V.expectation_plan(h, dt)['state_passes']}: {statistics.median(ts[2:]):.3f} ms  E={e!r}", flush=True)
     del psi
     torch.cuda.empty_cache()
