@@ -511,6 +511,19 @@ struct HbmEngine {
   }
 };
 
+// Device memory size, queried once per device.
+size_t total_device_bytes(int device) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, size_t>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& e : cache)
+    if (e.first == device) return e.second;
+  cudaDeviceProp prop{};
+  VQF_CUDA(cudaGetDeviceProperties(&prop, device));
+  cache.emplace_back(device, prop.totalGlobalMem);
+  return prop.totalGlobalMem;
+}
+
 // Memory a new state batch can take: the driver's free bytes plus what the
 // device's stream-ordered pool holds reserved but unused (the pool keeps
 // freed states mapped, sv.cu retain_pool, so after a wide run cudaMemGetInfo
@@ -547,7 +560,14 @@ struct ShiftEvaluator {
   ShiftEvaluator(uint32_t n_, int32_t kind_, uint32_t layers_, int device_, int32_t dtype = VQF_F64)
       : n(n_), P(ansatz_params(kind_, layers_, n_)), NC(2 * P + 1), kind(kind_), layers(layers_), device(device_) {
     const double entry = (double)(uint64_t{1} << n) * (dtype == VQF_F64 ? 16.0 : 8.0);
-    K = static_cast<uint32_t>(std::max(1.0, std::min<double>(NC, std::floor(0.6 * (double)free_device_bytes(device) / entry))));
+    // a family far below the device's memory needs no free-memory query
+    // (cudaMemGetInfo measured 0.4-9 ms per call once many pool allocations
+    // exist: it dominated the n = 16 studies' jitter)
+    if ((double)NC * entry <= (double)total_device_bytes(device) / 32)
+      K = NC;
+    else
+      K = static_cast<uint32_t>(
+          std::max(1.0, std::min<double>(NC, std::floor(0.6 * (double)free_device_bytes(device) / entry))));
     if (const char* cap = std::getenv("VQF_SHIFT_MAX_BATCH")) K = std::max(1u, std::min<uint32_t>(K, std::atoi(cap)));
     batched = K == NC;
     // a chunk recomputes the base circuit: below 8 entries per chunk one

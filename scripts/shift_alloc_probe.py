@@ -52,6 +52,11 @@ def runs(tag, k=7, profile=False, each=False):
               flush=True)
 
 
+if os.environ.get("AFTER_BENCH"):
+    import bench
+    bench.configs_3_4(V, torch, 0, 30, 3, 3, 6548.2, False, 0)
+    runs("after-bench")
+    runs("after-bench-prof", k=5, each=True)
 if os.environ.get("AFTER_N26"):
     for nq in (20, 24, 26):
         h = V.build_tfim(nq, 1.0, 1.0)
