@@ -262,6 +262,17 @@ __device__ __forceinline__ void givens(P& a, P& b, T c, T s) {
 template <typename T>
 constexpr bool kFactored = sizeof(T) == 4 && VQF_TILE_FACTORED32;
 
+// VQF_TILE_SKIP_ID=1 skips slots without an RY in the step (table entry 0)
+// on a uniform branch instead of rotating them by the identity (exact either
+// way).  Measured (scripts/ab_tile.sh, HEA layer): fp32 n = 30 15.46 vs
+// 14.86-15.03 ms, n = 28 4.08 vs 3.94-4.11 ms, fp64 equal -- the fp32 pass is
+// not bound by the rotation FMAs, and the branch costs the LB = 12 instance
+// registers (152 B of spills vs 68 B), so the default keeps the identities.
+#ifndef VQF_TILE_SKIP_ID
+#define VQF_TILE_SKIP_ID 0
+#endif
+constexpr bool kSkipIdentity = VQF_TILE_SKIP_ID;
+
 template <int R, typename P, typename T>
 __device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, const double2* rcs, const double2* rts,
                                          const uint8_t* rform, T& scale) {
@@ -278,6 +289,7 @@ __device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, con
   }
 #pragma unroll
   for (int j = 0; j < R; ++j) {
+    if (kSkipIdentity && st.ry[j] == 0) continue;  // CTA-uniform: no divergence
     if constexpr (kFactored<T>) {
       const double2 v = rts[st.ry[j]];
       const T k = static_cast<T>(v.x);
