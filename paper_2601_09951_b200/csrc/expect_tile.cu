@@ -129,6 +129,34 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
     for (uint32_t q = 0; q < p.n_diag; ++q)
       if (__popcll(ti & p.dmask[q]) & 1) thr_sig |= 1u << q;
   }
+  // Slot metadata, constant over the pass, hoisted out of the tile loop: bit
+  // s = ph * kExpSlots + j of live / xtype / sig0 = the slot has terms / is
+  // one X-type term (smask 0) / that term's sigma.  Term signs split as
+  // parity(i & yz) = parity(g0 & yz) ^ parity(thread part & yz): the thread
+  // parts are fixed (thr_par, bit s * kExpTerms + k), the tile part comes
+  // from one ballot per tile (lane s * kExpTerms + k holds that term's yz).
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t live = 0, xtype = 0, sig0 = 0, thr_par = 0;
+  uint64_t my_yz = 0;
+  for (uint32_t ph = 0; ph < p.n_phases; ++ph) {
+    uint32_t bl = 0;
+    for (int j = 0; j < LB - kER; ++j)
+      if ((gt >> j) & 1u) bl ^= p.ph[ph].tb_l[j];
+    const uint64_t tpart = ((uint64_t)(bl >> p.B) << p.h) | (bl & ((1u << p.B) - 1));
+    for (int j = 0; j < kExpSlots; ++j) {
+      const ExpSlot& S = p.ph[ph].slot[j];
+      const uint32_t sl = ph * kExpSlots + j;
+      if (S.n_terms) live |= 1u << sl;
+      if (S.n_terms == 1 && S.smask[0] == 0) xtype |= 1u << sl;
+      if (S.sigma[0]) sig0 |= 1u << sl;
+      for (uint32_t k = 0; k < S.n_terms && k < (uint32_t)kExpTerms; ++k) {
+        const uint32_t ti = sl * kExpTerms + k;
+        if (__popcll(tpart & S.yz[k]) & 1) thr_par |= 1u << ti;
+        if (lane == ti) my_yz = S.yz[k];
+      }
+    }
+  }
+  static_assert(kExpPhases * kExpSlots * kExpTerms <= 32, "term signs in one ballot");
   uint64_t tile = first;
   for (uint32_t it = 0; tile < n_tiles; tile += step, ++it) {
     const int buf = static_cast<int>(it % kBufs);
@@ -136,17 +164,15 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
     mbar_wait(&bars[buf], (it / kBufs) & 1u);
     // global index of the tile's local index 0: (top << (h + k)) | (mid << B)
     const uint64_t g0 = ((tile >> mid_bits) << (p.h + p.k)) | ((tile & ((uint64_t{1} << mid_bits) - 1)) << p.B);
+    const uint32_t neg = __ballot_sync(0xffffffffu, __popcll(g0 & my_yz) & 1) ^ thr_par;
 #pragma unroll
     for (int ph = 0; ph < kExpPhases; ++ph) {
       if (ph >= (int)p.n_phases) break;
       const ExpPhase& P = p.ph[ph];
-      uint32_t base_s = 0, base_l = 0;
+      uint32_t base_s = 0;
 #pragma unroll
       for (int j = 0; j < LB - kER; ++j)
-        if ((gt >> j) & 1u) {
-          base_s ^= P.tb_s[j];
-          base_l ^= P.tb_l[j];
-        }
+        if ((gt >> j) & 1u) base_s ^= P.tb_s[j];
       uint32_t rv[kER];
 #pragma unroll
       for (int j = 0; j < kER; ++j) rv[j] = P.rv_s[j];
@@ -164,9 +190,12 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
         group_sync<NT>(group);
         if (tile + kBufs * step < n_tiles) issue_load(tile + kBufs * step, buf);
       }
-      const uint64_t ib = g0 | ((uint64_t)(base_l >> p.B) << p.h) | (base_l & ((1u << p.B) - 1));
+      // the phase's first-term accumulators, loaded while the pairs are formed
+      double* const acc_ph = acc + (size_t)(ph * kExpSlots * kExpTerms) * nthr + threadIdx.x;
+      double a0[kExpSlots];
+#pragma unroll
+      for (int j = 0; j < kExpSlots; ++j) a0[j] = acc_ph[(size_t)(j * kExpTerms) * nthr];
       if (DIAG && ph == 0) {
-        const uint32_t lane = threadIdx.x & 31u;
         const bool tb = lane < p.n_diag && (__popcll(g0 & p.dmask[lane]) & 1);
         const uint32_t sig = __ballot_sync(0xffffffffu, tb) ^ thr_sig;
         // w[v] = sum_r (-1)^popc(r & v) |x_r|^2 (Walsh-Hadamard over the slots)
@@ -196,15 +225,15 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
       }
 #pragma unroll
       for (int j = 0; j < kExpSlots; ++j) {
-        const ExpSlot& S = P.slot[j];
-        if (S.n_terms == 0) continue;
-        if (S.n_terms == 1 && S.smask[0] == 0) {
+        const uint32_t sl = ph * kExpSlots + j;
+        if (!((live >> sl) & 1u)) continue;
+        if ((xtype >> sl) & 1u) {
           // one term without Y / Z on the register bits (TFIM's X_q): the
           // pair sum is FMA chains over Re(v) or Im(v), 2 ops per pair (fp64:
           // four independent chains for latency; fp32 measured faster with one)
           constexpr uint32_t kCh = sizeof(T) == 8 ? 4 : 1;
           T pc[4] = {T(0), T(0), T(0), T(0)};
-          if (S.sigma[0]) {
+          if ((sig0 >> sl) & 1u) {
 #pragma unroll
             for (uint32_t r = 0, q = 0; r < NR; ++r) {
               if (r & (1u << j)) continue;
@@ -225,9 +254,10 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
           }
           const T part = (pc[0] + pc[1]) + (pc[2] + pc[3]);
           const double pd = static_cast<double>(part);
-          acc[((ph * kExpSlots + j) * kExpTerms) * nthr + threadIdx.x] += (__popcll(ib & S.yz[0]) & 1) ? -pd : pd;
+          a0[j] += ((neg >> (sl * kExpTerms)) & 1u) ? -pd : pd;
           continue;
         }
+        const ExpSlot& S = P.slot[j];
         // pair products and the per-term sums over the thread's 8 pairs in
         // the storage precision (complex64 states: fp32, one conversion per
         // term instead of two per pair), accumulated across tiles in fp64
@@ -254,9 +284,13 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
             ++q;
           }
           const double pd = static_cast<double>(part);
-          acc[((ph * kExpSlots + j) * kExpTerms + k) * nthr + threadIdx.x] += (__popcll(ib & S.yz[k]) & 1) ? -pd : pd;
+          const double sd = ((neg >> (sl * kExpTerms + k)) & 1u) ? -pd : pd;
+          if (k == 0) a0[j] += sd;
+          else acc_ph[(size_t)(j * kExpTerms + k) * nthr] += sd;
         }
       }
+#pragma unroll
+      for (int j = 0; j < kExpSlots; ++j) acc_ph[(size_t)(j * kExpTerms) * nthr] = a0[j];
     }
   }
   // fixed-order CTA reduction of the accumulators
