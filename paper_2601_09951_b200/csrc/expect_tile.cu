@@ -190,11 +190,6 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
         group_sync<NT>(group);
         if (tile + kBufs * step < n_tiles) issue_load(tile + kBufs * step, buf);
       }
-      // the phase's first-term accumulators, loaded while the pairs are formed
-      double* const acc_ph = acc + (size_t)(ph * kExpSlots * kExpTerms) * nthr + threadIdx.x;
-      double a0[kExpSlots];
-#pragma unroll
-      for (int j = 0; j < kExpSlots; ++j) a0[j] = acc_ph[(size_t)(j * kExpTerms) * nthr];
       if (DIAG && ph == 0) {
         const bool tb = lane < p.n_diag && (__popcll(g0 & p.dmask[lane]) & 1);
         const uint32_t sig = __ballot_sync(0xffffffffu, tb) ^ thr_sig;
@@ -218,11 +213,19 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
 #pragma unroll
         for (uint32_t v = 0; v < NR; ++v) {
           double cv = 0.0;
-          for (uint32_t q = p.dv_off[v]; q < p.dv_off[v + 1]; ++q) cv += ((sig >> q) & 1u) ? -p.dc[q] : p.dc[q];
+          for (uint32_t e = p.dv_off[v]; e < p.dv_off[v + 1]; ++e) {
+            const uint32_t m = p.dq[e];
+            cv = fma(p.dc[e], static_cast<double>(__popc(m) - 2 * __popc(sig & m)), cv);
+          }
           d = fma(cv, w[v], d);
         }
         acc_diag += d;
       }
+      // the phase's first-term accumulators, loaded while the pairs are formed
+      double* const acc_ph = acc + (size_t)(ph * kExpSlots * kExpTerms) * nthr + threadIdx.x;
+      double a0[kExpSlots];
+#pragma unroll
+      for (int j = 0; j < kExpSlots; ++j) a0[j] = acc_ph[(size_t)(j * kExpTerms) * nthr];
 #pragma unroll
       for (int j = 0; j < kExpSlots; ++j) {
         const uint32_t sl = ph * kExpSlots + j;
@@ -498,7 +501,7 @@ std::vector<ExpTileParams> plan_expect_tiles(const CompiledHam& h, uint32_t n, i
 }
 
 bool fold_diag_into_tiles(std::vector<ExpTileParams>& passes, const CompiledHam& h, int32_t dtype) {
-  if (dtype != VQF_F64 || passes.empty() || h.group_flip.empty() || h.group_flip[0] != 0 ||
+  if ((dtype != VQF_F64 && !std::getenv("VQF_DIAG_FOLD32")) || passes.empty() || h.group_flip.empty() || h.group_flip[0] != 0 ||
       std::getenv("VQF_NO_DIAG_FOLD"))
     return false;
   const uint32_t t0 = h.group_offset[0], t1 = h.group_offset[1];
@@ -519,14 +522,24 @@ bool fold_diag_into_tiles(std::vector<ExpTileParams>& passes, const CompiledHam&
   }
   std::stable_sort(byv.begin(), byv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
   p.n_diag = t1 - t0;
-  for (uint32_t v = 0, q = 0; v <= 16; ++v) {
-    while (q < byv.size() && byv[q].first < v) ++q;
-    p.dv_off[v] = q;
+  for (size_t q = 0; q < byv.size(); ++q) p.dmask[q] = h.terms[byv[q].second].yz;
+  // classes of equal (v, coefficient), in order of first appearance per v
+  uint32_t n_cls = 0;
+  for (uint32_t v = 0, q = 0; v < 16; ++v) {
+    p.dv_off[v] = n_cls;
+    const uint32_t first = n_cls;
+    for (; q < byv.size() && byv[q].first == v; ++q) {
+      const double c = h.terms[byv[q].second].cb_re;
+      uint32_t e = first;
+      while (e < n_cls && p.dc[e] != c) ++e;
+      if (e == n_cls) {
+        p.dc[n_cls] = c;
+        p.dq[n_cls++] = 0;
+      }
+      p.dq[e] |= 1u << q;
+    }
   }
-  for (size_t q = 0; q < byv.size(); ++q) {
-    p.dmask[q] = h.terms[byv[q].second].yz;
-    p.dc[q] = h.terms[byv[q].second].cb_re;
-  }
+  p.dv_off[16] = n_cls;
   return true;
 }
 

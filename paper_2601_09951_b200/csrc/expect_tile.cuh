@@ -36,13 +36,16 @@ struct ExpTileParams {
   uint32_t n, B, k, h, n_phases, G, nb;
   ExpPhase ph[kExpPhases];
   uint8_t reg_gbit[kExpPhases][kExpSlots];  // global index bit of each register slot
-  // Folded diagonal group (one pass at most; n_diag = 0 elsewhere): real
-  // coefficients dc of Z strings dmask, sorted by their register-slot pattern
-  // v in phase 0 (terms [dv_off[v], dv_off[v + 1])).
+  // Folded diagonal group (one pass at most; n_diag = 0 elsewhere): Z
+  // strings dmask[q] with real coefficients, gathered into classes of equal
+  // coefficient dc[e] and equal register-slot pattern v in phase 0 (classes
+  // [dv_off[v], dv_off[v + 1]); dq[e] = the class's terms as bits q), so a
+  // class adds dc (|class| - 2 * #negative terms) with two popcounts.
   uint32_t n_diag;
   uint32_t dv_off[17];
   uint64_t dmask[kExpDiag];
   double dc[kExpDiag];
+  uint32_t dq[kExpDiag];
 };
 
 // Groups whose flip is one index bit and that hold <= kExpTerms terms are read
@@ -55,7 +58,9 @@ std::vector<ExpTileParams> plan_expect_tiles(const CompiledHam& h, uint32_t n, i
 // phases when it holds 1..kExpDiag Z strings with real coefficients, so the
 // separate diagonal read of the state goes away (fp64 only: measured TFIM
 // n = 30 16.7 -> 14.6 ms, n = 28 equal; in fp32 the folded pass turns
-// instruction-bound, n = 28 2.33 -> 2.78 ms).  Returns whether it did.
+// instruction-bound: with the hoisted slot metadata and coefficient classes,
+// VQF_DIAG_FOLD32=1 measured n = 30 9.01 -> 8.82 ms but n = 28 2.01 -> 2.28
+// ms, so fp32 keeps its diagonal pass).  Returns whether it did.
 bool fold_diag_into_tiles(std::vector<ExpTileParams>& passes, const CompiledHam& h, int32_t dtype);
 
 // Enqueues the passes on sv's stream; each writes per-CTA complex partials
