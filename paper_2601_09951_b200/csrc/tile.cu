@@ -253,9 +253,11 @@ __device__ __forceinline__ void givens(P& a, P& b, T c, T s) {
 //   else      : a' = k u - v, b' = u + k v   (k = c / s, factor s)
 // -- 2 FMAs per amplitude component instead of a multiply and an FMA -- and
 // the product of the factors, equal for all the thread's amplitudes, is
-// applied once at the end of the phase.  rts[q] = (k, factor), rform[q] =
-// the branch; entry 0 = (0, 1): identity, exact.  fp64 keeps the direct form
-// (the factored one spills there and measured 6 % slower).
+// applied once at the end of the phase.  rk[q] = k (in the state's
+// precision), rform[q] = the branch, and the kernel prologue multiplies each
+// phase's factors once per CTA (pscale); entry 0 = (k 0, factor 1): identity,
+// exact.  fp64 keeps the direct form (the factored one spills there and
+// measured 6 % slower).
 #ifndef VQF_TILE_FACTORED32
 #define VQF_TILE_FACTORED32 1
 #endif
@@ -274,8 +276,8 @@ constexpr bool kFactored = sizeof(T) == 4 && VQF_TILE_FACTORED32;
 constexpr bool kSkipIdentity = VQF_TILE_SKIP_ID;
 
 template <int R, typename P, typename T>
-__device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, const double2* rcs, const double2* rts,
-                                         const uint8_t* rform, T& scale) {
+__device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, const double2* rcs, const T* rk,
+                                         const uint8_t* rform) {
   constexpr int NR = 1 << R;
   if (st.flags & 1u) {
     const double2 v = rcs[st.se];
@@ -291,9 +293,7 @@ __device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, con
   for (int j = 0; j < R; ++j) {
     if (kSkipIdentity && st.ry[j] == 0) continue;  // CTA-uniform: no divergence
     if constexpr (kFactored<T>) {
-      const double2 v = rts[st.ry[j]];
-      const T k = static_cast<T>(v.x);
-      scale *= static_cast<T>(v.y);
+      const T k = rk[st.ry[j]];
       if (rform[st.ry[j]] == 0) {
 #pragma unroll
         for (int r = 0; r < NR; ++r)
@@ -371,6 +371,10 @@ static_assert(sizeof(TileParams) <= 4096, "kernel parameter limit");
 
 // Global start index of run j (0 <= j < 2^k) of tile `tile`.
 __device__ __forceinline__ uint64_t run_start(const TileParams& p, uint64_t tile, uint32_t j) {
+  if (p.win) {  // gathered bits = the window [h, h + k): closed form
+    const uint32_t h = p.hb[0], mid = h - p.B;
+    return ((tile >> mid) << (h + p.k)) | ((tile & ((uint64_t{1} << mid) - 1)) << p.B) | ((uint64_t)j << h);
+  }
   uint64_t base = tile << p.B;
   for (uint32_t m = 0; m < p.k; ++m) base = insert_zero64(base, p.hb[m]);
   for (uint32_t m = 0; m < p.k; ++m) base |= (uint64_t)((j >> m) & 1u) << p.hb[m];
@@ -384,7 +388,7 @@ __device__ __forceinline__ uint64_t run_start(const TileParams& p, uint64_t tile
 // streams in while this one computes and stores.
 template <typename T, int R, int LB, int NT, typename Refill>
 __device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePhase& ph, const TileStep* steps,
-                                          const double2* rcs, const double2* rts, const uint8_t* rform,
+                                          const double2* rcs, const T* rk, const uint8_t* rform, T pscale,
                                           uint32_t gt, uint32_t group,
                                           typename V2<T>::type* s, const uint64_t* run_off, uint32_t B,
                                           Refill&& refill) {
@@ -419,8 +423,8 @@ __device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePha
     if (direct) refill();
   }
   const uint32_t n_steps = ph.n_steps, step0 = ph.step0;
-  T scale = T(1);
-  for (uint32_t q = 0; q < n_steps; ++q) run_step<R, A, T>(x, steps[step0 + q], rcs, rts, rform, scale);
+  const T scale = pscale;  // product of the phase's factors (kernel prologue)
+  for (uint32_t q = 0; q < n_steps; ++q) run_step<R, A, T>(x, steps[step0 + q], rcs, rk, rform);
   if constexpr (kFactored<T>) {
     if (n_steps != 0)
 #pragma unroll
@@ -466,7 +470,9 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
   unsigned char* ring = smem;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSlots * (size_t)tile_bytes);
   __shared__ double2 rcs[kMaxRot];
-  __shared__ double2 rts[kFactored<T> ? kMaxRot : 1];
+  __shared__ T rk[kFactored<T> ? kMaxRot : 1];          // factored form: k per rotation
+  __shared__ double rfac[kFactored<T> ? kMaxRot : 1];    // and its factor
+  __shared__ T pscale[kFactored<T> ? kMaxPhases : 1];    // product of a phase's factors
   __shared__ uint8_t rform[kFactored<T> ? kMaxRot : 1];
   __shared__ uint16_t ftab[PERM ? 2 : 1][64];
   // run starts of the group's current tile (double-buffered: a fast thread
@@ -500,8 +506,20 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
       rcs[q] = v;
       if constexpr (kFactored<T>) {
         const bool by_c = fabs(v.x) >= fabs(v.y);
-        rts[q] = by_c ? make_double2(v.y / v.x, v.x) : make_double2(v.x / v.y, v.y);
+        rk[q] = static_cast<T>(by_c ? v.y / v.x : v.x / v.y);
+        rfac[q] = by_c ? v.x : v.y;
         rform[q] = by_c ? 0 : 1;
+      }
+    }
+    if constexpr (kFactored<T>) {
+      // each phase's factors multiplied once per CTA, in the order the steps
+      // used to apply them (step by step, slot by slot)
+      __syncthreads();
+      for (uint32_t ph = threadIdx.x; ph < p.n_phases; ph += blockDim.x) {
+        T sc = T(1);
+        for (uint32_t q = p.ph[ph].step0; q < p.ph[ph].step0 + p.ph[ph].n_steps; ++q)
+          for (int j = 0; j < R; ++j) sc *= static_cast<T>(rfac[p.steps[q].ry[j]]);
+        pscale[ph] = sc;
       }
     }
   }
@@ -582,7 +600,8 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
         if (gt < 32 && ahead < n_tiles) issue_load(ahead, cur);
       };
       for (uint32_t ph = 0; ph < p.n_phases; ++ph) {
-        run_phase<T, R, LB, NT>(t, p.ph[ph], p.steps, rcs, rts, rform, gt, group, s, run_off, p.B, refill);
+        run_phase<T, R, LB, NT>(t, p.ph[ph], p.steps, rcs, rk, rform, kFactored<T> ? pscale[ph] : T(1), gt, group, s,
+                                run_off, p.B, refill);
         if (ph + 1 == p.n_phases) {
           if (direct) break;
           fence_proxy_async();  // generic-proxy stores -> TMA store reads
