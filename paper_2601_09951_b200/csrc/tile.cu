@@ -276,8 +276,8 @@ constexpr bool kFactored = sizeof(T) == 4 && VQF_TILE_FACTORED32;
 constexpr bool kSkipIdentity = VQF_TILE_SKIP_ID;
 
 template <int R, typename P, typename T>
-__device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, const double2* rcs, const T* rk,
-                                         const uint8_t* rform) {
+__device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, const double2* rcs, const T* sk,
+                                         uint32_t fm) {
   constexpr int NR = 1 << R;
   if (st.flags & 1u) {
     const double2 v = rcs[st.se];
@@ -293,8 +293,8 @@ __device__ __forceinline__ void run_step(P (&x)[1 << R], const TileStep& st, con
   for (int j = 0; j < R; ++j) {
     if (kSkipIdentity && st.ry[j] == 0) continue;  // CTA-uniform: no divergence
     if constexpr (kFactored<T>) {
-      const T k = rk[st.ry[j]];
-      if (rform[st.ry[j]] == 0) {
+      const T k = sk[j];  // the step's slot-j k and form, gathered in the prologue
+      if (!((fm >> j) & 1u)) {
 #pragma unroll
         for (int r = 0; r < NR; ++r)
           if (!(r & (1 << j))) {
@@ -388,7 +388,7 @@ __device__ __forceinline__ uint64_t run_start(const TileParams& p, uint64_t tile
 // streams in while this one computes and stores.
 template <typename T, int R, int LB, int NT, typename Refill>
 __device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePhase& ph, const TileStep* steps,
-                                          const double2* rcs, const T* rk, const uint8_t* rform, T pscale,
+                                          const double2* rcs, const T* sk, const uint32_t* sform, T pscale,
                                           uint32_t gt, uint32_t group,
                                           typename V2<T>::type* s, const uint64_t* run_off, uint32_t B,
                                           Refill&& refill) {
@@ -424,7 +424,8 @@ __device__ __forceinline__ void run_phase(typename V2<T>::type* t, const TilePha
   }
   const uint32_t n_steps = ph.n_steps, step0 = ph.step0;
   const T scale = pscale;  // product of the phase's factors (kernel prologue)
-  for (uint32_t q = 0; q < n_steps; ++q) run_step<R, A, T>(x, steps[step0 + q], rcs, rk, rform);
+  for (uint32_t q = step0; q < step0 + n_steps; ++q)
+    run_step<R, A, T>(x, steps[q], rcs, sk + (size_t)q * R, kFactored<T> ? sform[q] : 0u);
   if constexpr (kFactored<T>) {
     if (n_steps != 0)
 #pragma unroll
@@ -473,6 +474,8 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
   __shared__ T rk[kFactored<T> ? kMaxRot : 1];          // factored form: k per rotation
   __shared__ double rfac[kFactored<T> ? kMaxRot : 1];    // and its factor
   __shared__ T pscale[kFactored<T> ? kMaxPhases : 1];    // product of a phase's factors
+  __shared__ T sk[kFactored<T> ? kMaxSteps * R : 1];     // k of step q, slot j at q * R + j
+  __shared__ uint32_t sform[kFactored<T> ? kMaxSteps : 1];  // bit j: slot j's form
   __shared__ uint8_t rform[kFactored<T> ? kMaxRot : 1];
   __shared__ uint16_t ftab[PERM ? 2 : 1][64];
   // run starts of the group's current tile (double-buffered: a fast thread
@@ -520,6 +523,13 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
         for (uint32_t q = p.ph[ph].step0; q < p.ph[ph].step0 + p.ph[ph].n_steps; ++q)
           for (int j = 0; j < R; ++j) sc *= static_cast<T>(rfac[p.steps[q].ry[j]]);
         pscale[ph] = sc;
+      }
+      for (uint32_t e = threadIdx.x; e < (uint32_t)(kMaxSteps * R); e += blockDim.x)
+        sk[e] = rk[p.steps[e / R].ry[e % R]];
+      for (uint32_t q = threadIdx.x; q < (uint32_t)kMaxSteps; q += blockDim.x) {
+        uint32_t fm = 0;
+        for (int j = 0; j < R; ++j) fm |= (uint32_t)rform[p.steps[q].ry[j]] << j;
+        sform[q] = fm;
       }
     }
   }
@@ -600,7 +610,7 @@ __global__ void __launch_bounds__(kGroupsOf<T> << (LB - R), 1)
         if (gt < 32 && ahead < n_tiles) issue_load(ahead, cur);
       };
       for (uint32_t ph = 0; ph < p.n_phases; ++ph) {
-        run_phase<T, R, LB, NT>(t, p.ph[ph], p.steps, rcs, rk, rform, kFactored<T> ? pscale[ph] : T(1), gt, group, s,
+        run_phase<T, R, LB, NT>(t, p.ph[ph], p.steps, rcs, sk, sform, kFactored<T> ? pscale[ph] : T(1), gt, group, s,
                                 run_off, p.B, refill);
         if (ph + 1 == p.n_phases) {
           if (direct) break;
