@@ -157,6 +157,16 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
     }
   }
   static_assert(kExpPhases * kExpSlots * kExpTerms <= 32, "term signs in one ballot");
+  // first-term accumulators of every (phase, slot) in registers across the
+  // tiles (the phase loop is unrolled), written to shared memory at the end;
+  // the folded-diagonal pass (more registers live) keeps them in shared
+  // memory, loaded and stored once per phase
+  constexpr bool kRegAcc = !DIAG;
+  double ra[kExpPhases][kExpSlots];
+#pragma unroll
+  for (int ph = 0; ph < kExpPhases; ++ph)
+#pragma unroll
+    for (int j = 0; j < kExpSlots; ++j) ra[ph][j] = 0.0;
   uint64_t tile = first;
   for (uint32_t it = 0; tile < n_tiles; tile += step, ++it) {
     const int buf = static_cast<int>(it % kBufs);
@@ -221,11 +231,12 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
         }
         acc_diag += d;
       }
-      // the phase's first-term accumulators, loaded while the pairs are formed
       double* const acc_ph = acc + (size_t)(ph * kExpSlots * kExpTerms) * nthr + threadIdx.x;
-      double a0[kExpSlots];
+      double a0s[kExpSlots];
+      if constexpr (!kRegAcc)
 #pragma unroll
-      for (int j = 0; j < kExpSlots; ++j) a0[j] = acc_ph[(size_t)(j * kExpTerms) * nthr];
+        for (int j = 0; j < kExpSlots; ++j) a0s[j] = acc_ph[(size_t)(j * kExpTerms) * nthr];
+      double (&a0)[kExpSlots] = kRegAcc ? ra[ph] : a0s;
 #pragma unroll
       for (int j = 0; j < kExpSlots; ++j) {
         const uint32_t sl = ph * kExpSlots + j;
@@ -292,10 +303,16 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
           else acc_ph[(size_t)(j * kExpTerms + k) * nthr] += sd;
         }
       }
+      if constexpr (!kRegAcc)
 #pragma unroll
-      for (int j = 0; j < kExpSlots; ++j) acc_ph[(size_t)(j * kExpTerms) * nthr] = a0[j];
+        for (int j = 0; j < kExpSlots; ++j) acc_ph[(size_t)(j * kExpTerms) * nthr] = a0s[j];
     }
   }
+  if constexpr (kRegAcc)
+#pragma unroll
+  for (int ph = 0; ph < kExpPhases; ++ph)
+#pragma unroll
+    for (int j = 0; j < kExpSlots; ++j) acc[(size_t)((ph * kExpSlots + j) * kExpTerms) * nthr + threadIdx.x] = ra[ph][j];
   // fixed-order CTA reduction of the accumulators
   __shared__ double diag_warp[32];
   if constexpr (DIAG) {
