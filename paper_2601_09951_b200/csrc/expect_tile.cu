@@ -121,7 +121,9 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
   // parts are fixed (phase 0's layout), the tile parts come from one ballot
   uint32_t thr_sig = 0;
   double acc_diag = 0.0;
+  uint64_t my_dmask = 0;  // lane q < n_diag: string q's Z mask (tile parities by ballot)
   if constexpr (DIAG) {
+    if ((threadIdx.x & 31u) < p.n_diag) my_dmask = p.dmask[threadIdx.x & 31u];
     uint32_t bl = 0;
     for (int j = 0; j < LB - kER; ++j)
       if ((gt >> j) & 1u) bl ^= p.ph[0].tb_l[j];
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
         if (tile + kBufs * step < n_tiles) issue_load(tile + kBufs * step, buf);
       }
       if (DIAG && ph == 0) {
-        const bool tb = lane < p.n_diag && (__popcll(g0 & p.dmask[lane]) & 1);
+        const bool tb = __popcll(g0 & my_dmask) & 1;
         const uint32_t sig = __ballot_sync(0xffffffffu, tb) ^ thr_sig;
         // w[v] = sum_r (-1)^popc(r & v) |x_r|^2 (Walsh-Hadamard over the slots)
         double w[NR];
@@ -222,12 +224,16 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
         double d = 0.0;
 #pragma unroll
         for (uint32_t v = 0; v < NR; ++v) {
-          double cv = 0.0;
-          for (uint32_t e = p.dv_off[v]; e < p.dv_off[v + 1]; ++e) {
-            const uint32_t m = p.dq[e];
-            cv = fma(p.dc[e], static_cast<double>(__popc(m) - 2 * __popc(sig & m)), cv);
-          }
-          d = fma(cv, w[v], d);
+          if (!((p.v_live >> v) & 1u)) continue;  // uniform
+          const uint32_t m = p.dq1[v];
+          d = fma(p.dc1[v] * static_cast<double>(__popc(m) - 2 * __popc(sig & m)), w[v], d);
+        }
+        for (uint32_t e = 0; e < p.n_ov; ++e) {  // further classes (none for TFIM)
+          const uint32_t m = p.ov_dq[e], ve = p.ov_v[e];
+          double wv = w[0];
+#pragma unroll
+          for (uint32_t u = 1; u < NR; ++u) wv = ve == u ? w[u] : wv;
+          d = fma(p.ov_dc[e] * static_cast<double>(__popc(m) - 2 * __popc(sig & m)), wv, d);
         }
         acc_diag += d;
       }
@@ -540,23 +546,33 @@ bool fold_diag_into_tiles(std::vector<ExpTileParams>& passes, const CompiledHam&
   std::stable_sort(byv.begin(), byv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
   p.n_diag = t1 - t0;
   for (size_t q = 0; q < byv.size(); ++q) p.dmask[q] = h.terms[byv[q].second].yz;
-  // classes of equal (v, coefficient), in order of first appearance per v
-  uint32_t n_cls = 0;
+  // classes of equal (v, coefficient), in order of first appearance per v:
+  // the first at index v, the others in the overflow list
+  p.v_live = 0;
+  p.n_ov = 0;
   for (uint32_t v = 0, q = 0; v < 16; ++v) {
-    p.dv_off[v] = n_cls;
-    const uint32_t first = n_cls;
+    p.dq1[v] = 0;
+    p.dc1[v] = 0.0;
+    const uint32_t ov0 = p.n_ov;
     for (; q < byv.size() && byv[q].first == v; ++q) {
       const double c = h.terms[byv[q].second].cb_re;
-      uint32_t e = first;
-      while (e < n_cls && p.dc[e] != c) ++e;
-      if (e == n_cls) {
-        p.dc[n_cls] = c;
-        p.dq[n_cls++] = 0;
+      if (!((p.v_live >> v) & 1u) || p.dc1[v] == c) {
+        p.v_live |= 1u << v;
+        p.dc1[v] = c;
+        p.dq1[v] |= 1u << q;
+        continue;
       }
-      p.dq[e] |= 1u << q;
+      uint32_t e = ov0;
+      while (e < p.n_ov && p.ov_dc[e] != c) ++e;
+      if (e == p.n_ov) {
+        p.ov_dc[e] = c;
+        p.ov_v[e] = v;
+        p.ov_dq[e] = 0;
+        ++p.n_ov;
+      }
+      p.ov_dq[e] |= 1u << q;
     }
   }
-  p.dv_off[16] = n_cls;
   return true;
 }
 

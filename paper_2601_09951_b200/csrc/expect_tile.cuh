@@ -38,14 +38,17 @@ struct ExpTileParams {
   uint8_t reg_gbit[kExpPhases][kExpSlots];  // global index bit of each register slot
   // Folded diagonal group (one pass at most; n_diag = 0 elsewhere): Z
   // strings dmask[q] with real coefficients, gathered into classes of equal
-  // coefficient dc[e] and equal register-slot pattern v in phase 0 (classes
-  // [dv_off[v], dv_off[v + 1]); dq[e] = the class's terms as bits q), so a
-  // class adds dc (|class| - 2 * #negative terms) with two popcounts.
-  uint32_t n_diag;
-  uint32_t dv_off[17];
+  // coefficient and equal register-slot pattern v in phase 0 (a class's
+  // terms as bits q), so a class adds dc (|class| - 2 * #negative terms)
+  // with two popcounts.
+  // The first class of each pattern sits at index v (dq1[v] = 0: none),
+  // further classes in the overflow list.
+  uint32_t n_diag, v_live, n_ov;  // v_live bit v: pattern v has a class
   uint64_t dmask[kExpDiag];
-  double dc[kExpDiag];
-  uint32_t dq[kExpDiag];
+  uint32_t dq1[16];
+  double dc1[16];
+  uint32_t ov_dq[kExpDiag], ov_v[kExpDiag];
+  double ov_dc[kExpDiag];
 };
 
 // Groups whose flip is one index bit and that hold <= kExpTerms terms are read
