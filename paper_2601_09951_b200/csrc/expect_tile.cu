@@ -524,7 +524,7 @@ std::vector<ExpTileParams> plan_expect_tiles(const CompiledHam& h, uint32_t n, i
 }
 
 bool fold_diag_into_tiles(std::vector<ExpTileParams>& passes, const CompiledHam& h, int32_t dtype) {
-  if ((dtype != VQF_F64 && !std::getenv("VQF_DIAG_FOLD32")) || passes.empty() || h.group_flip.empty() || h.group_flip[0] != 0 ||
+  if ((dtype != VQF_F64 && std::getenv("VQF_NO_DIAG_FOLD32")) || passes.empty() || h.group_flip.empty() || h.group_flip[0] != 0 ||
       std::getenv("VQF_NO_DIAG_FOLD"))
     return false;
   const uint32_t t0 = h.group_offset[0], t1 = h.group_offset[1];

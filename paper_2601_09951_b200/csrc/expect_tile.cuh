@@ -59,11 +59,11 @@ std::vector<ExpTileParams> plan_expect_tiles(const CompiledHam& h, uint32_t n, i
 
 // Folds the diagonal group (group 0) into the pass with the fewest register
 // phases when it holds 1..kExpDiag Z strings with real coefficients, so the
-// separate diagonal read of the state goes away (fp64 only: measured TFIM
-// n = 30 16.7 -> 14.6 ms, n = 28 equal; in fp32 the folded pass turns
-// instruction-bound: with the hoisted slot metadata and coefficient classes,
-// VQF_DIAG_FOLD32=1 measured n = 30 9.01 -> 8.82 ms but n = 28 2.01 -> 2.28
-// ms, so fp32 keeps its diagonal pass).  Returns whether it did.
+// separate diagonal read of the state goes away.  Measured TFIM fp64 n = 30
+// 16.7 -> 14.6 ms at introduction; fp32 folds too since the class table
+// (VQF_NO_DIAG_FOLD32=1 keeps the diagonal pass: n = 26 / 28 / 30 / 32 fp32
+// 0.67 / 1.94 / 8.77 / 34.0 ms unfolded vs 0.63 / 1.75 / 7.38 / 28.5 ms
+// folded).  Returns whether it did.
 bool fold_diag_into_tiles(std::vector<ExpTileParams>& passes, const CompiledHam& h, int32_t dtype);
 
 // Enqueues the passes on sv's stream; each writes per-CTA complex partials
