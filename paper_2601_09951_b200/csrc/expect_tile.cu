@@ -140,6 +140,16 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
   const uint32_t lane = threadIdx.x & 31u;
   uint32_t live = 0, xtype = 0, sig0 = 0, thr_par = 0;
   uint64_t my_yz = 0;
+  // (the slot masks read kernel parameters only: CTA-uniform, so the slot
+  // tests below can run on the uniform datapath)
+  for (uint32_t ph = 0; ph < p.n_phases; ++ph)
+    for (int j = 0; j < kExpSlots; ++j) {
+      const ExpSlot& S = p.ph[ph].slot[j];
+      const uint32_t sl = ph * kExpSlots + j;
+      if (S.n_terms) live |= 1u << sl;
+      if (S.n_terms == 1 && S.smask[0] == 0) xtype |= 1u << sl;
+      if (S.sigma[0]) sig0 |= 1u << sl;
+    }
   for (uint32_t ph = 0; ph < p.n_phases; ++ph) {
     uint32_t bl = 0;
     for (int j = 0; j < LB - kER; ++j)
@@ -148,9 +158,6 @@ __global__ void __launch_bounds__(kEGroupsOf<T> << (LB - kER), 1)
     for (int j = 0; j < kExpSlots; ++j) {
       const ExpSlot& S = p.ph[ph].slot[j];
       const uint32_t sl = ph * kExpSlots + j;
-      if (S.n_terms) live |= 1u << sl;
-      if (S.n_terms == 1 && S.smask[0] == 0) xtype |= 1u << sl;
-      if (S.sigma[0]) sig0 |= 1u << sl;
       for (uint32_t k = 0; k < S.n_terms && k < (uint32_t)kExpTerms; ++k) {
         const uint32_t ti = sl * kExpTerms + k;
         if (__popcll(tpart & S.yz[k]) & 1) thr_par |= 1u << ti;
