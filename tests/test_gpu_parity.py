@@ -800,3 +800,34 @@ def test_expectation_diagonal_folded_into_tile_pass(gpu, orc, n, batch, n_diag, 
     assert unfolded == folded + (1 if n_z <= 32 else 0)
     got2 = np.atleast_1d(V.expectation(s, hv))
     assert max(abs(a - b) for a, b in zip(got, got2)) < 1e-11
+
+
+@pytest.mark.parametrize("n,batch,n_diag", [(12, 1, 20), (16, 2, 32), (21, 1, 28)])
+def test_expectation_diagonal_folded_fp32(gpu, orc, n, batch, n_diag, monkeypatch):
+    """fp32 (complex64) states fold the diagonal group into a gathered-tile
+    pass too.  Z strings with distinct coefficients give several coefficient
+    classes per register pattern (the overflow list), and a shared
+    coefficient gives multi-string classes; against the fp64 oracle at the
+    fp32 bar and against the unfolded fp32 plan (VQF_NO_DIAG_FOLD32)."""
+    V = gpu
+    pr = random.Random(1300 + n)
+    terms = [(pr.uniform(-2, 2), [(q, 1)]) for q in range(n)]
+    for i in range(n_diag):
+        ws = sorted(pr.sample(range(n), pr.randint(1, 3)))
+        c = -0.75 if i % 3 == 0 else pr.uniform(-2, 2)  # every third string shares one coefficient
+        terms.append((c, [(w, 3) for w in ws]))
+    h = orc.canonicalize(Ham(n, terms))
+    hv = to_v(V, h)
+    rng = np.random.default_rng(n + 11)
+    psis = [random_state(rng, n) for _ in range(batch)]
+    s = V.StateVector(n, batch=batch, dtype="f32")
+    s.amplitudes = np.concatenate(psis)
+    folded = V.expectation_plan(hv, "f32")["state_passes"]
+    got = np.atleast_1d(V.expectation(s, hv))
+    bar = 1e-5 * max(1.0, len(h.terms) / 10)
+    for g, p in zip(got, psis):
+        assert abs(g - orc.expectation(n, p, h)) < bar
+    monkeypatch.setenv("VQF_NO_DIAG_FOLD32", "1")
+    assert V.expectation_plan(hv, "f32")["state_passes"] == folded + 1
+    got2 = np.atleast_1d(V.expectation(s, hv))
+    assert max(abs(a - b) for a, b in zip(got, got2)) < bar
